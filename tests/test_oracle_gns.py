@@ -1,0 +1,122 @@
+"""Pins for oracle/gns.py (Eq. 10, Theorem 1, B_noise) against hand values, closed forms and Monte Carlo."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import aggregate as agg
+from oracle import gns
+
+
+def test_local_estimates_spec_hand_values(golden):
+    ex = golden["local_estimates"]
+    b = [ex["b_i"], ex["B"] - ex["b_i"]]
+    Gi, Si = gns.local_estimates([ex["local_sq"], 0.0], ex["global_sq"], b)
+    assert math.isclose(Gi[0], ex["G_i"], rel_tol=1e-15)
+    assert math.isclose(Si[0], ex["S_i"], rel_tol=1e-15)
+
+
+def test_weight_matrix_spec_hand_values(golden):
+    ex = golden["weight_matrices"]
+    AG, AS = gns.weight_matrices(ex["b"])
+    assert math.isclose(AG[0, 0], ex["aG00"], rel_tol=1e-15)
+    assert math.isclose(AG[0, 1], ex["aG01"], rel_tol=1e-15)
+    assert math.isclose(AS[0, 0], ex["aS00"], rel_tol=1e-15)
+    assert AS[0, 1] == ex["aS01"]
+
+
+def test_weight_matrices_symmetric_and_scale():
+    """Entries scale: (b, B) -> (c b, c B) scales A_G by 1/c and A_S by c."""
+    b = np.array([32.0, 64.0, 96.0])
+    AG, AS = gns.weight_matrices(b)
+    AG2, AS2 = gns.weight_matrices(3 * b)
+    assert np.allclose(AG, AG.T, rtol=0, atol=0)
+    assert np.allclose(AS, AS.T, rtol=0, atol=0)
+    assert np.allclose(AG2, AG / 3, rtol=1e-14)
+    assert np.allclose(AS2, AS * 3, rtol=1e-14)
+
+
+@pytest.mark.parametrize("b", [[25, 75], [10, 90], [33, 41]])
+def test_two_node_closed_form_weights(b):
+    """n = 2 closed forms derived by hand from Theorem 1 with B = b0 + b1:
+    A_G = [[(B+2b0)/(B b1), 2/B], [2/B, (B+2b1)/(B b0)]]  =>  w^G ∝ ((3b1-b0)/b0, (3b0-b1)/b1)
+    A_S = diag(B b0/b1, B b1/b0)                         =>  w^S ∝ (b1^2, b0^2)."""
+    b0, b1 = b
+    wg = np.array([(3 * b1 - b0) / b0, (3 * b0 - b1) / b1])
+    ws = np.array([b1 * b1, b0 * b0], dtype=float)
+    wg /= wg.sum()
+    ws /= ws.sum()
+    AG, AS = gns.weight_matrices(b)
+    assert np.allclose(gns.optimal_weights(AG), wg, rtol=1e-12, atol=1e-14)
+    assert np.allclose(gns.optimal_weights(AS), ws, rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("n,bi", [(2, 50), (4, 16), (8, 7)])
+def test_homogeneous_weights_uniform(n, bi):
+    """equal b_i => exactly uniform weights (symmetry of A)."""
+    AG, AS = gns.weight_matrices([bi] * n)
+    assert np.allclose(gns.optimal_weights(AG), 1.0 / n, atol=1e-14)
+    assert np.allclose(gns.optimal_weights(AS), 1.0 / n, atol=1e-14)
+
+
+def test_weights_scale_invariant_and_sum_to_one():
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        n = int(rng.integers(2, 9))
+        b = rng.integers(1, 200, size=n).astype(float)
+        wg = gns.optimal_weights(gns.weight_matrices(b)[0])
+        wg5 = gns.optimal_weights(gns.weight_matrices(5 * b)[0])
+        assert abs(wg.sum() - 1.0) < 1e-12
+        assert np.allclose(wg, wg5, rtol=1e-9, atol=1e-12)
+
+
+def test_zero_noise_gives_zero_S():
+    """noiseless gradients -> S = 0, B_noise = 0, G = |G|^2."""
+    b = [32, 64, 96]
+    r = gns.gns_estimate([1.7, 1.7, 1.7], 1.7, b)
+    assert abs(r["trS"]) < 1e-12 and abs(r["B_noise"]) < 1e-12
+    assert math.isclose(r["G2"], 1.7, rel_tol=1e-12)
+
+
+def test_domain_errors():
+    with pytest.raises(ValueError):
+        gns.gns_estimate([1.0], 1.0, [5])
+    with pytest.raises(ValueError):
+        gns.local_estimates([1.0, 1.0], 1.0, [0, 5])
+
+
+@pytest.mark.parametrize("b", [[32, 64, 96], [25, 75], [5, 20, 40, 7]])
+def test_unbiased_monte_carlo(b):
+    """North-star check 2 / P:343: on Gaussian gradients with known |G|^2 and tr(Sigma), the
+    Theorem-1 aggregate has E[G] = |G|^2 and E[S] = tr(Sigma): within 4 empirical standard errors.
+    Per-node means are drawn exactly as the mean of b_i samples of N(G, (trS/d) I) (Eq. 1)."""
+    d, trials, G2, trS = 256, 6000, 1.0, 100.0
+    rng = np.random.default_rng(1234 + len(b))
+    z = rng.standard_normal(d)
+    G = z * np.sqrt(G2 / (z @ z))
+    B = sum(b)
+    r = agg.ratios(b)
+    Gs, Ss = [], []
+    for _ in range(trials):
+        gi = [G + np.sqrt(trS / (d * bi)) * rng.standard_normal(d) for bi in b]
+        g = agg.weighted_sum(gi, r)
+        est = gns.gns_estimate([agg.sq_norm(x) for x in gi], agg.sq_norm(g), b)
+        Gs.append(est["G2"])
+        Ss.append(est["trS"])
+    Gs, Ss = np.array(Gs), np.array(Ss)
+    seG = Gs.std(ddof=1) / np.sqrt(trials)
+    seS = Ss.std(ddof=1) / np.sqrt(trials)
+    assert abs(Gs.mean() - G2) < 4 * seG, (Gs.mean(), seG)
+    assert abs(Ss.mean() - trS) < 4 * seS, (Ss.mean(), seS)
+    # a dropped term would bias by O(trS/B) -- far outside the band:
+    assert 4 * seG < 0.25 * trS / B
+
+
+def test_noise_scale_ratio():
+    b = [32, 64, 96]
+    r = gns.gns_estimate([1.0 + 100 / 32, 1.0 + 100 / 64, 1.0 + 100 / 96], 1.0 + 100 / 192, b)
+    # at the expectations, every G_i = 1 and S_i = 100 exactly, so any weights summing to 1 give
+    # G = 1, S = 100, B_noise = 100
+    assert math.isclose(r["G2"], 1.0, rel_tol=1e-12)
+    assert math.isclose(r["trS"], 100.0, rel_tol=1e-12)
+    assert math.isclose(r["B_noise"], 100.0, rel_tol=1e-12)

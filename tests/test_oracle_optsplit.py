@@ -1,0 +1,187 @@
+"""Pins for oracle/optsplit.py and oracle/pipeline.py against SPEC/paper hand values, the event
+pipeline, brute force, KKT equal-time conditions and grid search."""
+import math
+
+import numpy as np
+import pytest
+
+import cannikin_synth as synth
+from oracle import optsplit as osp
+from oracle import pipeline
+
+
+def test_eq3_to_eq6_hand_values(golden):
+    ex = golden["node_model"]
+    node, b = ex["node"], ex["b"]
+    assert math.isclose(osp.compute_time(node, b), ex["compute_time"], rel_tol=1e-12)
+    assert math.isclose(osp.sync_start(node, (ex["gamma"], 0, 0), b), ex["sync_start"], rel_tol=1e-12)
+    assert math.isclose(osp.node_time(node, ex["compute_bound_comm"], b), ex["compute_bound_time"], rel_tol=1e-12)
+    assert osp.is_compute_bound(node, ex["compute_bound_comm"], b)
+    assert math.isclose(osp.node_time(node, ex["comm_bound_comm"], b), ex["comm_bound_time"], rel_tol=1e-12)
+    assert not osp.is_compute_bound(node, ex["comm_bound_comm"], b)
+    ex2 = golden["compute_time_2"]
+    assert math.isclose(osp.compute_time(ex2["node"], ex2["b"]), ex2["compute_time"], rel_tol=1e-12)
+    ex3 = golden["classify_comm"]
+    assert osp.is_compute_bound(ex3["node"], ex3["comm"], ex3["b"]) == ex3["compute_bound"]
+
+
+def test_classification_tie_is_compute():
+    """P:191 '>=': (1-gamma) P == T_o counts as compute-bound."""
+    node = (0.0, 0.0, 0.01, 0.0)
+    assert osp.is_compute_bound(node, (0.5, 0.25, 0.0), 50)   # (0.5)(0.5) = 0.25
+
+
+def test_pipeline_spec_traces(golden):
+    for ex in golden["pipeline"]:
+        T = pipeline.simulate([ex["node"]], ex["comm"], [ex["b"]], ex["n_buckets"])
+        assert math.isclose(T, ex["T"], rel_tol=1e-12)
+
+
+def test_closed_form_equals_pipeline_and_eq7():
+    """A.2 / S:490: the bucket pipeline of §3.2.3 equals Eq. 7 = max_i f_i(b_i) for any parameters."""
+    rng = np.random.default_rng(7)
+    for _ in range(500):
+        n = int(rng.integers(1, 9))
+        nodes, comm = synth.random_cluster(rng, n)
+        b = rng.integers(0, 200, size=n).astype(float)
+        nb = int(rng.integers(2, 12))
+        T_pipe = pipeline.simulate(nodes, comm, b, nb)
+        T_f = osp.cluster_time(nodes, comm, b)
+        assert abs(T_pipe - T_f) <= 1e-12 * max(1.0, T_f)
+        assert abs(osp.eq7_time(nodes, comm, b) - T_f) <= 1e-12 * max(1.0, T_f)
+
+
+def test_check1_all_compute(golden):
+    ex = golden["solve_equal_compute"]
+    b, T, labels = osp.real_split(ex["nodes"], ex["comm"], ex["B"])
+    assert np.allclose(b, ex["b"], rtol=0, atol=1e-9)
+    assert math.isclose(T, ex["t"], rel_tol=1e-12)
+    assert labels == [1, 1]
+
+
+def test_check2_all_comm(golden):
+    ex = golden["solve_equal_syncstart"]
+    b, T, labels = osp.real_split(ex["nodes"], ex["comm"], ex["B"])
+    assert np.allclose(b, ex["b"], rtol=0, atol=1e-9)
+    gamma, t_o, t_u = ex["comm"]
+    assert math.isclose(T - t_o - t_u, ex["sync_start"], rel_tol=1e-12)
+    assert labels == [0, 0]
+    for i in range(2):
+        assert math.isclose(osp.sync_start(ex["nodes"][i], ex["comm"], b[i]), ex["sync_start"], rel_tol=1e-12)
+
+
+def test_rounding_regression(golden):
+    ex = golden["rounding_regression"]
+    b, T, _ = osp.real_split(ex["nodes"], ex["comm"], ex["B"])
+    assert np.allclose(b, ex["b_real"], atol=1e-12)
+    assert math.isclose(T, ex["T_real"], rel_tol=1e-12)
+    bp = osp.round_paper(b, ex["B"])
+    assert bp == ex["b_paper"]
+    assert math.isclose(osp.cluster_time(ex["nodes"], ex["comm"], bp), ex["T_paper"], rel_tol=1e-12)
+    bi, Ti = osp.int_split_greedy(ex["nodes"], ex["comm"], ex["B"])
+    assert bi == ex["b_int"] and math.isclose(Ti, ex["T_int"], rel_tol=1e-12)
+
+
+def test_round_paper_spec(golden):
+    for ex in golden["round_allocation"]:
+        assert osp.round_paper(ex["b_real"], ex["B"]) == ex["b"]
+
+
+def test_warmup_spec(golden):
+    for ex in golden["warmup"]:
+        assert np.allclose(osp.warmup_split(ex["t_sample"], ex["B"]), ex["b"], rtol=1e-12)
+
+
+def test_greedy_equals_brute_force():
+    """North-star check 3: the integer split agrees with brute-force enumeration on 2-3 node clusters."""
+    rng = np.random.default_rng(2024)
+    for trial in range(150):
+        n = int(rng.integers(2, 4))
+        nodes, comm = synth.random_cluster(rng, n)
+        B = int(rng.integers(n, 40 if n == 3 else 60))
+        lo = cap = None
+        if trial % 5 == 0:
+            cap = [int(x) for x in rng.integers(max(1, B // n), B, size=n)]
+            if sum(cap) < B:
+                cap = None
+        bg, Tg = osp.int_split_greedy(nodes, comm, B, lo, cap)
+        bb, Tb = osp.int_split_brute(nodes, comm, B, lo, cap)
+        assert bg == bb, (nodes, comm, B, bg, bb)
+        assert Tg == Tb
+
+
+def test_brute_force_minimises_eq7():
+    """The brute force's primary criterion is Eq. 7 itself: no split has a smaller max finish time."""
+    rng = np.random.default_rng(99)
+    for _ in range(40):
+        nodes, comm = synth.random_cluster(rng, 2)
+        B = int(rng.integers(2, 50))
+        bb, Tb = osp.int_split_brute(nodes, comm, B)
+        best = min(osp.cluster_time(nodes, comm, [j, B - j]) for j in range(1, B))
+        assert Tb == best
+
+
+def test_real_split_equal_finish_times_and_bounds():
+    """KKT (App. A): unclamped nodes finish together; the integer optimum lies
+    within one sample's slope of the relaxation."""
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        n = int(rng.integers(2, 9))
+        nodes, comm = synth.random_cluster(rng, n)
+        B = int(rng.integers(4 * n, 1600))
+        b, T, labels = osp.real_split(nodes, comm, B)
+        assert abs(sum(b) - B) < 1e-7 * B
+        times = [osp.node_time(nodes[i], comm, b[i]) for i in range(n) if b[i] > 1.0]
+        if len(times) >= 2:
+            assert max(times) - min(times) <= 1e-11 * T
+        bi, Ti = osp.int_split_greedy(nodes, comm, B)
+        slope = max(q + k for q, s, k, m in nodes)
+        assert T <= Ti * (1 + 1e-12) and Ti < T + slope + 1e-12
+        # mixed patterns: compute-bound nodes share t_compute, comm-bound share syncStart,
+        # t_compute = syncStart + T_o
+        gamma, t_o, t_u = comm
+        tc = [osp.compute_time(nodes[i], b[i]) for i in range(n) if labels[i] and b[i] > 1.0]
+        ss = [osp.sync_start(nodes[i], comm, b[i]) for i in range(n) if not labels[i] and b[i] > 1.0]
+        if tc and ss:
+            assert abs(tc[0] - (ss[0] + t_o)) <= 1e-10 * T
+
+
+def test_real_split_beats_grid():
+    """Optimality of the relaxation on 2 nodes against a fine grid over b_0."""
+    rng = np.random.default_rng(11)
+    for _ in range(30):
+        nodes, comm = synth.random_cluster(rng, 2)
+        B = 100
+        b, T, _ = osp.real_split(nodes, comm, B)
+        grid = np.linspace(1.0, B - 1.0, 20001)
+        Tg = min(osp.cluster_time(nodes, comm, [x, B - x]) for x in grid)
+        assert T <= Tg + 1e-12
+        assert T >= Tg - 0.01 * max(q + k for q, s, k, m in nodes)
+
+
+def test_homogeneous_even_split_extra_to_low_ranks():
+    nodes = [(0.001, 0.01, 0.002, 0.02)] * 4
+    comm = (0.3, 0.05, 0.01)
+    b, T = osp.int_split_greedy(nodes, comm, 103)
+    assert b == [26, 26, 26, 25]
+    br, Tr, _ = osp.real_split(nodes, comm, 100)
+    assert np.allclose(br, 25.0, atol=1e-9)
+
+
+def test_single_node():
+    b, T = osp.int_split_greedy([(0.001, 0.01, 0.002, 0.02)], (0.3, 0.05, 0.01), 77)
+    assert b == [77]
+    br, Tr, _ = osp.real_split([(0.001, 0.01, 0.002, 0.02)], (0.3, 0.05, 0.01), 77)
+    assert br == [77.0]
+
+
+def test_errors():
+    nodes = [(0.001, 0.01, 0.002, 0.02)] * 2
+    with pytest.raises(ValueError):
+        osp.int_split_greedy(nodes, (0.3, 0.05, 0.01), 1)          # sum(lo) = 2 > B
+    with pytest.raises(ValueError):
+        osp.int_split_greedy(nodes, (1.0, 0.05, 0.01), 10)          # gamma out of [0,1)
+    with pytest.raises(ZeroDivisionError):
+        osp.int_split_greedy([(0.0, 0.01, 0.0, 0.02)] * 2, (0.3, 0.05, 0.01), 10)
+    with pytest.raises(ValueError):
+        osp.int_split_greedy(nodes, (0.3, 0.05, 0.01), 10, cap=[3, 3])
