@@ -1,0 +1,225 @@
+/*
+ * cannikin.h -- C ABI of the B200-native data-parallel hot path of Cannikin (arXiv 2402.05302).
+ *
+ * The library (libcannikin.so, sm_100a) implements, per training step:
+ *   - the weighted gradient aggregation  g = sum_i r_i g_i,  r_i = b_i / B
+ *       (§4.3 Eq. 9; r_i defined at P:151, §3.1),
+ *   - in the same pass the squared norms |g_i|^2 of every rank's local mean gradient g_i (Eq. 1,
+ *     P:125-130) and |g|^2 of the aggregate -- the inputs of Eq. 10,
+ *   - on the host, the heterogeneous gradient-noise-scale estimator (Eq. 10, Theorem 1 / Eq. 11,
+ *     B_noise = S/G),
+ *   - on the host, the exact local-batch split r_opt that minimises the Eq. 7 batch time
+ *     (§3; Alg. 1; integer batches P:419-420).
+ *
+ * Conventions shared by every call
+ *   - No CUDA, NCCL or torch types appear here.  `stream` is a cudaStream_t passed as void*
+ *     (NULL = the legacy default stream).  "device pointer" = CUDA global memory of the ctx's
+ *     device; "host pointer" = ordinary CPU memory.
+ *   - Every call returns a cannikin_status and never throws or aborts across the ABI.  Arguments
+ *     are validated before anything is enqueued; on failure nothing was launched and
+ *     cannikin_last_error() returns a thread-local message.
+ *   - Ownership: the caller owns buckets (unless allocated with cannikin_alloc_bucket), streams and
+ *     all output buffers.  A ctx owns its NCCL communicator, the peer-mapped symmetric heap, the
+ *     signal/partial pads, scratch and the norm-statistics accumulator; it must outlive every
+ *     operation enqueued on it.  Calls on one ctx must be ordered on one stream (or externally
+ *     synchronised).
+ *   - Determinism: for a fixed ctx grid, device results are bitwise reproducible run to run, and in
+ *     the multi-GPU path bitwise identical on every rank.
+ *   - Precision: fp32 or bf16 gradients; every sum over ranks is accumulated in fp32 in fixed rank
+ *     order 0..n-1 and rounded once to the bucket dtype; squared norms are accumulated per thread
+ *     in fp32 over one 16-byte vector and in fp64 beyond, then reduced by a fixed-order fp64 tree.
+ */
+#ifndef CANNIKIN_H
+#define CANNIKIN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CANNIKIN_VERSION 10000      /* 1.0.0 */
+#define CANNIKIN_MAX_WORLD 8        /* ranks of one NVSwitch box */
+#define CANNIKIN_MAX_EMULATED 16    /* emulated ranks of cannikin_weighted_sum_local */
+#define CANNIKIN_MAX_GNS_NODES 64
+
+typedef enum {
+  CANNIKIN_OK = 0,
+  CANNIKIN_ERR_INVALID = 1,     /* null pointer, size/alignment/limit violation, bad handle      */
+  CANNIKIN_ERR_DOMAIN = 2,      /* value outside the model's domain (gamma, b_i, negative coeff.) */
+  CANNIKIN_ERR_INFEASIBLE = 3,  /* sum(lo) > B or sum(cap) < B                                    */
+  CANNIKIN_ERR_SINGULAR = 4,    /* singular Theorem-1 matrix, or a node time independent of b     */
+  CANNIKIN_ERR_CUDA = 5,        /* CUDA runtime error (text in cannikin_last_error)                */
+  CANNIKIN_ERR_NCCL = 6,        /* NCCL error                                                     */
+  CANNIKIN_ERR_UNSUPPORTED = 7  /* dtype / rank count / feature not built                         */
+} cannikin_status;
+
+typedef enum { CANNIKIN_F32 = 0, CANNIKIN_BF16 = 1 } cannikin_dtype;
+
+typedef struct cannikin_ctx cannikin_ctx; /* opaque; one per (process, device) */
+
+/* Thread-local text of the last failure on this thread ("" if none).  Never NULL. */
+const char* cannikin_last_error(void);
+int cannikin_version(void);
+
+/* ------------------------------------------------------------------------------------------
+ * Lifecycle
+ * ------------------------------------------------------------------------------------------ */
+
+/* Writes a 128-byte NCCL unique id to `out_id` (host).  Call on rank 0 only, then broadcast the
+ * bytes to every rank over the caller's own process group (e.g. torch.distributed). */
+cannikin_status cannikin_get_unique_id(void* out_id);
+
+/* Create a ctx for `rank` of `world` (1 <= world <= CANNIKIN_MAX_WORLD) on CUDA `device`.
+ * world == 1: no communicator is created and `unique_id` may be NULL (single-GPU use:
+ *   cannikin_weighted_sum_local, host solvers, and a trivial weighted_allreduce).
+ * world  > 1: COLLECTIVE -- every rank calls it with the same unique_id and heap_bytes.  It
+ *   creates an NCCL communicator, allocates `heap_bytes` of device memory (the symmetric heap) plus
+ *   a control region, and maps every peer's heap into this process over NVLink (CUDA IPC handles
+ *   exchanged through NCCL).  Buckets carved from the heap (cannikin_alloc_bucket) are reduced
+ *   zero-copy; other device buffers are staged through a heap scratch area of the same size.
+ * `grid` (0 = default 148) fixes the CTA count of the reduction kernels (determinism contract).
+ * `flags`: reserved, pass 0.
+ * Errors: INVALID (rank/world/device out of range, out == NULL), CUDA, NCCL. */
+cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world, const void* unique_id,
+                              int device, size_t heap_bytes, int grid, unsigned flags);
+
+/* Destroy a ctx (synchronises its device first).  NULL is accepted and ignored. */
+cannikin_status cannikin_destroy(cannikin_ctx* ctx);
+
+/* COLLECTIVE for world > 1: every rank must issue the same sequence of alloc/free calls with the
+ * same sizes; the returned buffers then sit at the same heap offset on every rank, which is what
+ * lets the reduction kernel address a peer's copy.  Alignment: 256 bytes.  Errors: INVALID (no
+ * space, bytes == 0). */
+cannikin_status cannikin_alloc_bucket(cannikin_ctx* ctx, size_t bytes, void** dptr);
+cannikin_status cannikin_free_bucket(cannikin_ctx* ctx, void* dptr);
+
+/* ------------------------------------------------------------------------------------------
+ * Hot path (device, stream-ordered, no host synchronisation)
+ * ------------------------------------------------------------------------------------------ */
+
+/* Weighted all-reduce of one gradient bucket -- Eq. 9.
+ *   bucket : device pointer to n elements of `dt` holding this rank's MEAN local gradient g_i
+ *            (Eq. 1; a sum-reduced gradient would break |g_i|^2, reading Q4).
+ *            Overwritten in place with g = sum_j r_j g_j, bitwise identical on every rank.
+ *            16-byte aligned.  n * sizeof(dt) <= heap_bytes.  n == 0 is a no-op.
+ *   r_i    : this rank's share b_i / B.  Trusted (not re-normalised).
+ * Side effect: the norm statistics of this bucket -- |g_j|^2 restricted to the bucket for every
+ * rank j, and |g|^2 restricted to the bucket -- are added (fixed bucket order) to the ctx
+ * accumulator that cannikin_gns_stats reads.  Implementation: two-shot reduce-scatter/all-gather
+ * over NVLink peer memory with the scaling, the fp32 accumulation, both norms and the partial
+ * exchange fused into one kernel.  world == 1: g = r_0 g_0 in place.
+ * Errors: INVALID (NULL, misaligned, too large), UNSUPPORTED (dtype), CUDA. */
+cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* bucket, size_t n,
+                                            cannikin_dtype dt, double r_i, void* stream);
+
+/* Read and reset the norm statistics accumulated since the previous call (Eq. 10 inputs):
+ *   out_local_sq[j] = |g_j|^2 for j = 0..world-1, *out_global_sq = |g|^2   (host pointers).
+ * Identical bits on every rank.  Synchronises `stream`.
+ * The north-star signature carried b_i; batch sizes are not needed to finalise the norms and are
+ * passed to cannikin_gns_estimate instead.  Errors: INVALID, CUDA. */
+cannikin_status cannikin_gns_stats(cannikin_ctx* ctx, void* stream, double* out_local_sq,
+                                   double* out_global_sq);
+
+/* Stream-ordered variant: copies the (world+1) accumulated doubles [local_sq..., global_sq] to the
+ * DEVICE buffer d_out and resets the accumulator, without host synchronisation. */
+cannikin_status cannikin_gns_stats_async(cannikin_ctx* ctx, double* d_out, void* stream);
+
+/* Single-GPU fused pass over n_ranks emulated ranks (the 1-B200 metric kernel; reading of
+ * SURVEY §8(a) row a5):
+ *   in    : host array of n_ranks device pointers, each n elements of `dt` (16-byte aligned)
+ *   r     : host array of n_ranks shares r_j
+ *   out   : device pointer, n elements of `dt`:  out = sum_j r_j in[j]   (fp32 accumulate, rank order)
+ *           out may alias in[j] (in-place).
+ *   d_local_sq  : device pointer, n_ranks doubles: |in[j]|^2
+ *   d_global_sq : device pointer, 1 double: |out|^2 taken from the fp32 accumulator (reading Q2)
+ *   flags & CANNIKIN_ACCUMULATE: add to d_local_sq/d_global_sq instead of overwriting (multi-bucket)
+ * 1 <= n_ranks <= CANNIKIN_MAX_EMULATED.  Errors: INVALID, UNSUPPORTED, CUDA. */
+#define CANNIKIN_ACCUMULATE 1u
+cannikin_status cannikin_weighted_sum_local(cannikin_ctx* ctx, const void* const* in, int n_ranks,
+                                            const double* r, void* out, size_t n, cannikin_dtype dt,
+                                            double* d_local_sq, double* d_global_sq, unsigned flags,
+                                            void* stream);
+
+/* Baseline for the step-time comparison: equal-split DDP semantics (Eq. 2) -- an NCCL
+ * sum all-reduce of the bucket followed by a division by world (scale kernel).  In place. */
+cannikin_status cannikin_ddp_allreduce_mean(cannikin_ctx* ctx, void* bucket, size_t n,
+                                            cannikin_dtype dt, void* stream);
+
+/* Number of CUDA kernels the last hot-path call on this ctx enqueued (for launch accounting). */
+int cannikin_last_launch_count(cannikin_ctx* ctx);
+
+/* ------------------------------------------------------------------------------------------
+ * Host solvers (pure, thread-safe, no CUDA)
+ * ------------------------------------------------------------------------------------------ */
+
+#define CANNIKIN_GNS_G_NONPOSITIVE 1u /* aggregated G <= 0: B_noise = S/G is not meaningful */
+
+typedef struct {
+  double G2;                          /* G  = sum_i wG_i G_i   (estimate of |G|^2)      */
+  double trS;                         /* S  = sum_i wS_i S_i   (estimate of tr(Sigma))  */
+  double B_noise;                     /* S / G                                 */
+  double Gi[CANNIKIN_MAX_GNS_NODES];  /* Eq. 10 local estimates                          */
+  double Si[CANNIKIN_MAX_GNS_NODES];
+  double wG[CANNIKIN_MAX_GNS_NODES];  /* Theorem 1 weights (sum to 1)                    */
+  double wS[CANNIKIN_MAX_GNS_NODES];
+  int n;
+  unsigned flags;
+} cannikin_gns_result;
+
+/* Heterogeneous GNS estimate, exactly as PAPER.md §4.4 defines it:
+ *   G_i = (B|g|^2 - b_i|g_i|^2)/(B - b_i),  S_i = b_i B/(B - b_i) (|g_i|^2 - |g|^2)    (Eq. 10)
+ *   w = 1^T A^{-1} / (1^T A^{-1} 1) with the printed Theorem-1 matrices A_G, A_S       (Eq. 11)
+ *   G = sum w^G_i G_i,  S = sum w^S_i S_i,  B_noise = S / G.
+ * local_sq[n], b[n] host arrays; B = sum b.  2 <= n <= 64.
+ * Errors: INVALID (NULL, n out of range), DOMAIN (b_i outside [1, B-1], non-finite input),
+ * SINGULAR (zero pivot in the Gaussian elimination).  G <= 0 is not an error: status OK with
+ * CANNIKIN_GNS_G_NONPOSITIVE set. */
+cannikin_status cannikin_gns_estimate(const double* local_sq, double global_sq, const int64_t* b,
+                                      int n, cannikin_gns_result* out);
+
+/* Per-node performance model, Eq. 3:
+ *   a_i = q b + s  (parameter update + data loading + forward),  P_i = k b + m  (backprop). */
+typedef struct { double q, s, k, m; } cannikin_node_model;
+/* Communication model: overlap ratio gamma in [0,1), T_o (overlappable sync
+ * of all buckets but the last), T_u (last bucket).  T_comm = T_o + T_u. */
+typedef struct { double gamma, t_o, t_u; } cannikin_comm_model;
+
+/* Per-node batch time, Eq. 5-7, under the frozen evaluation contract
+ *   P = k*b + m;  A = q*b + s;  X = gamma*P + t_o;  f = (A + max(P, X)) + t_u
+ * (binary64, left to right, no FMA).  Returns NaN on NULL arguments. */
+double cannikin_node_time(const cannikin_node_model* node, const cannikin_comm_model* cm, double b);
+
+#define CANNIKIN_ROUND_PAPER 1u /* integer split = largest-remainder rounding of b_real */
+
+/* OptPerf split (§3.1-3.3, Alg. 1).
+ *   nodes[n], cm : models;  B >= 1 total batch;  lo[n] (NULL -> all 1), cap[n] (NULL -> all B)
+ * Outputs (host, any may be NULL):
+ *   b_real_out[n] : the relaxation's optimum -- unclamped nodes finish together (App. A
+ *                   P:726-762): compute-bound nodes share t_compute, comm-bound nodes share
+ *                   syncStart, t_compute = syncStart + T_o.  Exact breakpoint solve, O(n log n).
+ *   b_out[n]      : integer split.  Default: the exact integer minimiser of Eq. 7 with the
+ *                   canonical tie-break (reading Q12) -- equal to the greedy "next sample
+ *                   to argmin_i (f_i(b_i+1), i)" and to brute force.  With CANNIKIN_ROUND_PAPER:
+ *                   largest-remainder rounding of b_real, ties to the lower index.
+ *   t_out[2]      : { Eq. 7 at b_real, Eq. 7 at b_out }
+ *   label_out[n]  : 1 = compute-bound at b_real ((1-gamma) P_i >= T_o), 0 = comm-bound.
+ * Errors: INVALID (NULL nodes/cm, n < 1, B < 1), DOMAIN (gamma outside [0,1), negative or
+ * non-finite coefficient, lo < 0, lo > cap), INFEASIBLE (sum lo > B or sum cap < B),
+ * SINGULAR (q + gamma k == 0: a node whose comm-bound time does not grow with b). */
+cannikin_status cannikin_opt_split(const cannikin_node_model* nodes, int n,
+                                   const cannikin_comm_model* cm, int64_t B, const int64_t* lo,
+                                   const int64_t* cap, unsigned flags, int64_t* b_out,
+                                   double* b_real_out, double* t_out, int* label_out);
+
+/* Eq. 8 warm-up split when no performance model exists yet:
+ *   b_i = (sum_j t_j / t_i) (sum_l sum_j t_j / t_l)^{-1} B,  rounded by largest remainder.
+ * t_sample[n] > 0 host.  Errors: INVALID, DOMAIN (t <= 0 or non-finite). */
+cannikin_status cannikin_warmup_split(const double* t_sample, int n, int64_t B, double* b_real_out,
+                                      int64_t* b_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CANNIKIN_H */

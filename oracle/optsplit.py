@@ -96,7 +96,9 @@ def _check_models(nodes, comm):
     for q, s, k, m in nodes:
         if min(q, s, k, m) < 0.0:
             raise ValueError("domain: negative coefficient")
-        if q + k == 0.0:
+        if q + k == 0.0 or q + gamma * k == 0.0:
+            # f must grow with b on both branches (Eq. 5 slope q+k, Eq. 6 slope q+gamma k),
+            # otherwise the relaxation has a flat stretch and r_opt is not unique (Q18)
             raise ZeroDivisionError("singular: node time independent of b")
 
 

@@ -1,0 +1,243 @@
+"""B200-native hot path of Cannikin (arXiv 2402.05302): thin Python binding of libcannikin.so.
+
+Argument marshalling only -- every step of the path runs in the CUDA library (device kernels) or
+its C++ host solvers.  There is no fallback: if the library is missing this import fails.
+
+Entry points mirror include/cannikin.h:
+    Context(...)                      cannikin_init / cannikin_destroy
+    Context.alloc_bucket / free_bucket
+    Context.weighted_allreduce        Eq. 9 + fused |g_i|^2, |g|^2
+    Context.gns_stats                 finalise the norm statistics
+    Context.weighted_sum_local        emulated ranks on one GPU
+    gns_estimate                      Eq. 10 + Theorem 1
+    opt_split                         OptPerf split
+    warmup_split, node_time           Eq. 8; Eq. 5-7 frozen evaluation
+Torch-tensor conveniences live in ``paper_2402_05302_b200.torch_api``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = [
+    "CannikinError", "Context", "F32", "BF16", "ACCUMULATE", "ROUND_PAPER", "lib", "lib_path",
+    "get_unique_id", "gns_estimate", "opt_split", "node_time", "warmup_split", "MAX_WORLD",
+    "MAX_EMULATED",
+]
+
+F32, BF16 = 0, 1
+ACCUMULATE = 1
+ROUND_PAPER = 1
+GNS_G_NONPOSITIVE = 1
+MAX_WORLD = 8
+MAX_EMULATED = 16
+MAX_GNS = 64
+
+_STATUS = {0: "OK", 1: "INVALID", 2: "DOMAIN", 3: "INFEASIBLE", 4: "SINGULAR", 5: "CUDA", 6: "NCCL",
+           7: "UNSUPPORTED"}
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def lib_path() -> str:
+    return os.path.join(_HERE, "libcannikin.so")
+
+
+class CannikinError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"cannikin {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = _STATUS.get(status, str(status))
+
+
+class _GnsResult(ctypes.Structure):
+    _fields_ = [("G2", ctypes.c_double), ("trS", ctypes.c_double), ("B_noise", ctypes.c_double),
+                ("Gi", ctypes.c_double * MAX_GNS), ("Si", ctypes.c_double * MAX_GNS),
+                ("wG", ctypes.c_double * MAX_GNS), ("wS", ctypes.c_double * MAX_GNS),
+                ("n", ctypes.c_int), ("flags", ctypes.c_uint)]
+
+
+class _NodeModel(ctypes.Structure):
+    _fields_ = [("q", ctypes.c_double), ("s", ctypes.c_double), ("k", ctypes.c_double),
+                ("m", ctypes.c_double)]
+
+
+class _CommModel(ctypes.Structure):
+    _fields_ = [("gamma", ctypes.c_double), ("t_o", ctypes.c_double), ("t_u", ctypes.c_double)]
+
+
+_LIB = None
+
+# Every symbol include/cannikin.h declares, with (restype, argtypes).
+_P, _D, _I, _U, _Z, _L = (ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_uint,
+                          ctypes.c_size_t, ctypes.c_int64)
+_DP, _LP, _IP = (ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
+                 ctypes.POINTER(ctypes.c_int))
+SIGNATURES = {
+    "cannikin_last_error": (ctypes.c_char_p, []),
+    "cannikin_version": (_I, []),
+    "cannikin_get_unique_id": (_I, [_P]),
+    "cannikin_init": (_I, [ctypes.POINTER(_P), _I, _I, _P, _I, _Z, _I, _U]),
+    "cannikin_destroy": (_I, [_P]),
+    "cannikin_alloc_bucket": (_I, [_P, _Z, ctypes.POINTER(_P)]),
+    "cannikin_free_bucket": (_I, [_P, _P]),
+    "cannikin_weighted_allreduce": (_I, [_P, _P, _Z, _I, _D, _P]),
+    "cannikin_gns_stats": (_I, [_P, _P, _DP, _DP]),
+    "cannikin_gns_stats_async": (_I, [_P, _P, _P]),
+    "cannikin_weighted_sum_local": (_I, [_P, ctypes.POINTER(_P), _I, _DP, _P, _Z, _I, _P, _P, _U, _P]),
+    "cannikin_ddp_allreduce_mean": (_I, [_P, _P, _Z, _I, _P]),
+    "cannikin_last_launch_count": (_I, [_P]),
+    "cannikin_gns_estimate": (_I, [_DP, _D, _LP, _I, ctypes.POINTER(_GnsResult)]),
+    "cannikin_node_time": (_D, [ctypes.POINTER(_NodeModel), ctypes.POINTER(_CommModel), _D]),
+    "cannikin_opt_split": (_I, [ctypes.POINTER(_NodeModel), _I, ctypes.POINTER(_CommModel), _L, _LP,
+                                _LP, _U, _LP, _DP, _DP, _IP]),
+    "cannikin_warmup_split": (_I, [_DP, _I, _L, _DP, _LP]),
+}
+
+
+def lib() -> ctypes.CDLL:
+    """Load libcannikin.so (built in-tree by paper_2402_05302_b200.build).  No fallback."""
+    global _LIB
+    if _LIB is None:
+        path = lib_path()
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: run `python -m paper_2402_05302_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _LIB = L
+    return _LIB
+
+
+def _check(status: int):
+    if status != 0:
+        raise CannikinError(status, lib().cannikin_last_error().decode())
+
+
+def _dbl(xs):
+    return (ctypes.c_double * len(xs))(*[float(x) for x in xs])
+
+
+def _i64(xs):
+    return (ctypes.c_int64 * len(xs))(*[int(x) for x in xs])
+
+
+def _stream(s) -> int | None:
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    return int(getattr(s, "cuda_stream"))
+
+
+# ----------------------------------------------------------------------------- device context
+class Context:
+    """A cannikin_ctx: one per (process, GPU).  world > 1 is collective (see cannikin_init)."""
+
+    def __init__(self, rank: int = 0, world: int = 1, unique_id: bytes | None = None,
+                 device: int = 0, heap_bytes: int = 0, grid: int = 0):
+        L = lib()
+        h = ctypes.c_void_p()
+        uid = None
+        if unique_id is not None:
+            assert len(unique_id) == 128
+            uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(L.cannikin_init(ctypes.byref(h), rank, world, uid, device, heap_bytes, grid, 0))
+        self._h = h
+        self.rank, self.world, self.device = rank, world, device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _check(lib().cannikin_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def alloc_bucket(self, nbytes: int) -> int:
+        p = ctypes.c_void_p()
+        _check(lib().cannikin_alloc_bucket(self._h, nbytes, ctypes.byref(p)))
+        return int(p.value)
+
+    def free_bucket(self, ptr: int):
+        _check(lib().cannikin_free_bucket(self._h, ptr))
+
+    def weighted_allreduce(self, ptr: int, n: int, dtype: int, r_i: float, stream=None):
+        _check(lib().cannikin_weighted_allreduce(self._h, ptr, n, dtype, r_i, _stream(stream)))
+
+    def gns_stats(self, stream=None):
+        out = (ctypes.c_double * self.world)()
+        g = ctypes.c_double()
+        _check(lib().cannikin_gns_stats(self._h, _stream(stream), out, ctypes.byref(g)))
+        return list(out), g.value
+
+    def gns_stats_async(self, d_out: int, stream=None):
+        _check(lib().cannikin_gns_stats_async(self._h, d_out, _stream(stream)))
+
+    def weighted_sum_local(self, in_ptrs, r, out_ptr: int, n: int, dtype: int, d_local_sq: int,
+                           d_global_sq: int, accumulate: bool = False, stream=None):
+        arr = (ctypes.c_void_p * len(in_ptrs))(*in_ptrs)
+        _check(lib().cannikin_weighted_sum_local(self._h, arr, len(in_ptrs), _dbl(r), out_ptr, n,
+                                                 dtype, d_local_sq, d_global_sq,
+                                                 ACCUMULATE if accumulate else 0, _stream(stream)))
+
+    def ddp_allreduce_mean(self, ptr: int, n: int, dtype: int, stream=None):
+        _check(lib().cannikin_ddp_allreduce_mean(self._h, ptr, n, dtype, _stream(stream)))
+
+    def last_launch_count(self) -> int:
+        return int(lib().cannikin_last_launch_count(self._h))
+
+
+def get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().cannikin_get_unique_id(buf))
+    return buf.raw
+
+
+# ----------------------------------------------------------------------------- host solvers
+def gns_estimate(local_sq, global_sq: float, b) -> dict:
+    n = len(b)
+    res = _GnsResult()
+    _check(lib().cannikin_gns_estimate(_dbl(local_sq), float(global_sq), _i64(b), n,
+                                       ctypes.byref(res)))
+    return {"G2": res.G2, "trS": res.trS, "B_noise": res.B_noise, "Gi": list(res.Gi[:n]),
+            "Si": list(res.Si[:n]), "wG": list(res.wG[:n]), "wS": list(res.wS[:n]),
+            "flags": res.flags}
+
+
+def _models(nodes, comm):
+    arr = (_NodeModel * len(nodes))(*[_NodeModel(*map(float, nd)) for nd in nodes])
+    return arr, _CommModel(*map(float, comm))
+
+
+def node_time(node, comm, b: float) -> float:
+    nd = _NodeModel(*map(float, node))
+    cm = _CommModel(*map(float, comm))
+    return lib().cannikin_node_time(ctypes.byref(nd), ctypes.byref(cm), float(b))
+
+
+def opt_split(nodes, comm, B: int, lo=None, cap=None, round_paper: bool = False) -> dict:
+    n = len(nodes)
+    arr, cm = _models(nodes, comm)
+    b = (ctypes.c_int64 * n)()
+    br = (ctypes.c_double * n)()
+    t = (ctypes.c_double * 2)()
+    lab = (ctypes.c_int * n)()
+    _check(lib().cannikin_opt_split(arr, n, ctypes.byref(cm), int(B),
+                                    _i64(lo) if lo is not None else None,
+                                    _i64(cap) if cap is not None else None,
+                                    ROUND_PAPER if round_paper else 0, b, br, t, lab))
+    return {"b": list(b), "b_real": list(br), "T_real": t[0], "T_int": t[1], "labels": list(lab)}
+
+
+def warmup_split(t_sample, B: int):
+    n = len(t_sample)
+    br = (ctypes.c_double * n)()
+    b = (ctypes.c_int64 * n)()
+    _check(lib().cannikin_warmup_split(_dbl(t_sample), n, int(B), br, b))
+    return list(b), list(br)

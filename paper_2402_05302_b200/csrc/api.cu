@@ -1,0 +1,318 @@
+// C ABI of the device path: ctx lifecycle (NCCL communicator, peer-mapped symmetric heap),
+// bucket allocator, weighted all-reduce, norm statistics, emulated-rank pass, DDP baseline.
+// See include/cannikin.h for the contract of every entry point.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "common.h"
+#include "ctx.h"
+
+using cannikin::fail;
+
+namespace cannikin {
+cudaError_t launch_wsum_local(cannikin_ctx* ctx, const void* const* in, int nr, const double* r,
+                              void* out, size_t n, cannikin_dtype dt, double* d_local_sq,
+                              double* d_global_sq, bool accumulate, int grid_override,
+                              cudaStream_t st);
+cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
+                           cudaStream_t st);
+}  // namespace cannikin
+
+#define CK_CUDA(expr)                                                                     \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(CANNIKIN_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),    \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+#define CK_NCCL(expr)                                                                     \
+  do {                                                                                    \
+    ncclResult_t r_ = (expr);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      return fail(CANNIKIN_ERR_NCCL, "%s: %s (%s:%d)", #expr, ncclGetErrorString(r_),     \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+static inline size_t elem_size(cannikin_dtype dt) { return dt == CANNIKIN_F32 ? 4 : 2; }
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" cannikin_status cannikin_get_unique_id(void* out_id) {
+  if (!out_id) return fail(CANNIKIN_ERR_INVALID, "get_unique_id: NULL");
+  ncclUniqueId id;
+  CK_NCCL(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "unique id is 128 bytes");
+  std::memcpy(out_id, &id, sizeof id);
+  return CANNIKIN_OK;
+}
+
+static cannikin_status destroy_partial(cannikin_ctx* ctx) {
+  if (!ctx) return CANNIKIN_OK;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (int j = 0; j < ctx->world; ++j)
+    if (j != ctx->rank && ctx->peer_base[j]) cudaIpcCloseMemHandle(ctx->peer_base[j]);
+  if (ctx->nccl_comm) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl_comm));
+  if (ctx->base) cudaFree(ctx->base);
+  if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
+  delete ctx;
+  return CANNIKIN_OK;
+}
+
+extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world,
+                                         const void* unique_id, int device, size_t heap_bytes,
+                                         int grid, unsigned flags) {
+  (void)flags;
+  if (!out) return fail(CANNIKIN_ERR_INVALID, "init: out == NULL");
+  *out = nullptr;
+  if (world < 1 || world > CANNIKIN_MAX_WORLD || rank < 0 || rank >= world)
+    return fail(CANNIKIN_ERR_INVALID, "init: rank=%d world=%d (world must be 1..%d)", rank, world,
+                CANNIKIN_MAX_WORLD);
+  if (world > 1 && !unique_id) return fail(CANNIKIN_ERR_INVALID, "init: world > 1 needs a unique id");
+  int ndev = 0;
+  CK_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev)
+    return fail(CANNIKIN_ERR_INVALID, "init: device %d of %d", device, ndev);
+  CK_CUDA(cudaSetDevice(device));
+  cannikin_ctx* ctx = new cannikin_ctx();
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->device = device;
+  cudaError_t ce = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (ce != cudaSuccess) { destroy_partial(ctx); CK_CUDA(ce); }
+  ctx->grid_ar = grid > 0 ? grid : ctx->num_sms;
+  if (ctx->grid_ar > cannikin::kMaxArBlocks) ctx->grid_ar = cannikin::kMaxArBlocks;
+  if (const char* t = std::getenv("CANNIKIN_SPIN_TIMEOUT_MS"))
+    ctx->spin_timeout_ns = (uint64_t)std::strtoull(t, nullptr, 10) * 1000000ull;
+  ctx->heap_bytes = align_up(heap_bytes, 256);
+  ctx->ctrl_bytes = align_up(sizeof(cannikin::Ctrl), 4096);
+  ctx->user_off = ctx->ctrl_bytes;
+  ctx->scratch_off = ctx->user_off + ctx->heap_bytes;
+  ctx->total_bytes = ctx->scratch_off + (world > 1 ? ctx->heap_bytes : 0);
+  ce = cudaMalloc(&ctx->base, ctx->total_bytes);
+  if (ce == cudaSuccess) ce = cudaMemset(ctx->base, 0, ctx->ctrl_bytes);
+  if (ce == cudaSuccess) ce = cudaMallocHost(&ctx->h_stats, sizeof(double) * (cannikin::kMaxWorld + 1));
+  if (ce != cudaSuccess) { destroy_partial(ctx); CK_CUDA(ce); }
+  ctx->ctrl = reinterpret_cast<cannikin::Ctrl*>(ctx->base);
+  if (ctx->heap_bytes) ctx->free_blocks[0] = ctx->heap_bytes;
+  ctx->peer_base[rank] = ctx->base;
+
+  if (world > 1) {
+    ncclComm_t comm;
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof id);
+    ncclResult_t nr = ncclCommInitRank(&comm, world, id, rank);
+    if (nr != ncclSuccess) {
+      destroy_partial(ctx);
+      return fail(CANNIKIN_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(nr));
+    }
+    ctx->nccl_comm = comm;
+    // exchange CUDA IPC handles of every rank's allocation through NCCL, then map the peers
+    cudaIpcMemHandle_t mine;
+    char* d_handles = nullptr;
+    cudaStream_t st = nullptr;
+    ce = cudaIpcGetMemHandle(&mine, ctx->base);
+    if (ce == cudaSuccess) ce = cudaMalloc(&d_handles, sizeof(cudaIpcMemHandle_t) * world);
+    if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (ce == cudaSuccess)
+      ce = cudaMemcpy(d_handles + sizeof mine * rank, &mine, sizeof mine, cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) {
+      if (d_handles) cudaFree(d_handles);
+      destroy_partial(ctx);
+      CK_CUDA(ce);
+    }
+    nr = ncclAllGather(d_handles + sizeof mine * rank, d_handles, sizeof mine, ncclUint8, comm, st);
+    cudaIpcMemHandle_t all[cannikin::kMaxWorld];
+    if (nr == ncclSuccess) {
+      ce = cudaStreamSynchronize(st);
+      if (ce == cudaSuccess)
+        ce = cudaMemcpy(all, d_handles, sizeof mine * world, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(d_handles);
+    cudaStreamDestroy(st);
+    if (nr != ncclSuccess) {
+      destroy_partial(ctx);
+      return fail(CANNIKIN_ERR_NCCL, "ncclAllGather(ipc handles): %s", ncclGetErrorString(nr));
+    }
+    if (ce != cudaSuccess) { destroy_partial(ctx); CK_CUDA(ce); }
+    for (int j = 0; j < world; ++j) {
+      if (j == rank) continue;
+      void* p = nullptr;
+      ce = cudaIpcOpenMemHandle(&p, all[j], cudaIpcMemLazyEnablePeerAccess);
+      if (ce != cudaSuccess) { destroy_partial(ctx); CK_CUDA(ce); }
+      ctx->peer_base[j] = static_cast<char*>(p);
+    }
+    // every rank has mapped every peer before anyone launches a kernel that touches peers
+    int* d_one = nullptr;
+    ce = cudaMalloc(&d_one, sizeof(int));
+    if (ce == cudaSuccess) {
+      nr = ncclAllReduce(d_one, d_one, 1, ncclInt32, ncclSum, comm, 0);
+      ce = cudaDeviceSynchronize();
+      cudaFree(d_one);
+    }
+    if (nr != ncclSuccess) { destroy_partial(ctx); return fail(CANNIKIN_ERR_NCCL, "barrier: %s", ncclGetErrorString(nr)); }
+    if (ce != cudaSuccess) { destroy_partial(ctx); CK_CUDA(ce); }
+  }
+  *out = ctx;
+  cannikin::clear_error();
+  return CANNIKIN_OK;
+}
+
+extern "C" cannikin_status cannikin_destroy(cannikin_ctx* ctx) { return destroy_partial(ctx); }
+
+extern "C" cannikin_status cannikin_alloc_bucket(cannikin_ctx* ctx, size_t bytes, void** dptr) {
+  if (!ctx || !dptr || bytes == 0) return fail(CANNIKIN_ERR_INVALID, "alloc_bucket: bad arguments");
+  const size_t need = align_up(bytes, 256);
+  for (auto it = ctx->free_blocks.begin(); it != ctx->free_blocks.end(); ++it) {
+    if (it->second >= need) {
+      const size_t off = it->first, sz = it->second;
+      ctx->free_blocks.erase(it);
+      if (sz > need) ctx->free_blocks[off + need] = sz - need;
+      ctx->used_blocks[off] = need;
+      *dptr = ctx->base + ctx->user_off + off;
+      return CANNIKIN_OK;
+    }
+  }
+  return fail(CANNIKIN_ERR_INVALID, "alloc_bucket: %zu bytes do not fit in the %zu-byte heap", bytes,
+              ctx->heap_bytes);
+}
+
+extern "C" cannikin_status cannikin_free_bucket(cannikin_ctx* ctx, void* dptr) {
+  if (!ctx || !dptr) return fail(CANNIKIN_ERR_INVALID, "free_bucket: bad arguments");
+  char* p = static_cast<char*>(dptr);
+  if (p < ctx->base + ctx->user_off || p >= ctx->base + ctx->user_off + ctx->heap_bytes)
+    return fail(CANNIKIN_ERR_INVALID, "free_bucket: pointer not from this ctx");
+  const size_t off = p - (ctx->base + ctx->user_off);
+  auto it = ctx->used_blocks.find(off);
+  if (it == ctx->used_blocks.end()) return fail(CANNIKIN_ERR_INVALID, "free_bucket: not allocated");
+  size_t sz = it->second;
+  ctx->used_blocks.erase(it);
+  size_t o = off;
+  auto nx = ctx->free_blocks.find(o + sz);
+  if (nx != ctx->free_blocks.end()) { sz += nx->second; ctx->free_blocks.erase(nx); }
+  auto pv = ctx->free_blocks.lower_bound(o);
+  if (pv != ctx->free_blocks.begin()) {
+    --pv;
+    if (pv->first + pv->second == o) { o = pv->first; sz += pv->second; ctx->free_blocks.erase(pv); }
+  }
+  ctx->free_blocks[o] = sz;
+  return CANNIKIN_OK;
+}
+
+extern "C" cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* bucket, size_t n,
+                                                       cannikin_dtype dt, double r_i,
+                                                       void* stream) {
+  if (!ctx) return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce: ctx == NULL");
+  ctx->last_launches = 0;
+  if (dt != CANNIKIN_F32 && dt != CANNIKIN_BF16)
+    return fail(CANNIKIN_ERR_UNSUPPORTED, "weighted_allreduce: dtype %d", (int)dt);
+  if (n == 0) return CANNIKIN_OK;
+  if (!bucket) return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce: bucket == NULL");
+  if (reinterpret_cast<uintptr_t>(bucket) % 16)
+    return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce: bucket not 16-byte aligned");
+  if (!(r_i == r_i)) return fail(CANNIKIN_ERR_DOMAIN, "weighted_allreduce: r_i is NaN");
+  const size_t bytes = n * elem_size(dt);
+  CK_CUDA(cudaSetDevice(ctx->device));
+  if (ctx->world == 1) {
+    // g = r_0 g_0 in place; |g_0|^2 and |g|^2 accumulate into stats[0], stats[1]
+    const void* in[1] = {bucket};
+    const double r[1] = {r_i};
+    CK_CUDA(cannikin::launch_wsum_local(ctx, in, 1, r, bucket, n, dt, &ctx->ctrl->stats[0],
+                                        &ctx->ctrl->stats[1], true, 0, S(stream)));
+    ctx->last_launches = 1;
+    return CANNIKIN_OK;
+  }
+  if (bytes > ctx->heap_bytes)
+    return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce: %zu bytes > heap %zu", bytes,
+                ctx->heap_bytes);
+  char* p = static_cast<char*>(bucket);
+  char* heap_lo = ctx->base + ctx->user_off;
+  if (p >= heap_lo && p + bytes <= heap_lo + ctx->heap_bytes) {
+    CK_CUDA(cannikin::launch_twoshot(ctx, p - ctx->base, n, dt, r_i, S(stream)));
+    ctx->last_launches = 1;
+    return CANNIKIN_OK;
+  }
+  // not peer-mapped: stage through the scratch half of the heap (same offset on every rank)
+  char* scratch = ctx->base + ctx->scratch_off;
+  CK_CUDA(cudaMemcpyAsync(scratch, bucket, bytes, cudaMemcpyDeviceToDevice, S(stream)));
+  CK_CUDA(cannikin::launch_twoshot(ctx, ctx->scratch_off, n, dt, r_i, S(stream)));
+  CK_CUDA(cudaMemcpyAsync(bucket, scratch, bytes, cudaMemcpyDeviceToDevice, S(stream)));
+  ctx->last_launches = 1;
+  return CANNIKIN_OK;
+}
+
+extern "C" cannikin_status cannikin_gns_stats(cannikin_ctx* ctx, void* stream,
+                                              double* out_local_sq, double* out_global_sq) {
+  if (!ctx || !out_local_sq || !out_global_sq)
+    return fail(CANNIKIN_ERR_INVALID, "gns_stats: NULL argument");
+  CK_CUDA(cudaSetDevice(ctx->device));
+  const int W = ctx->world;
+  const size_t bytes = sizeof(double) * (W + 1);
+  CK_CUDA(cudaMemcpyAsync(ctx->h_stats, ctx->ctrl->stats, bytes, cudaMemcpyDeviceToHost, S(stream)));
+  CK_CUDA(cudaMemsetAsync(ctx->ctrl->stats, 0, bytes, S(stream)));
+  CK_CUDA(cudaStreamSynchronize(S(stream)));
+  int code = 0;
+  CK_CUDA(cudaMemcpy(&code, &ctx->ctrl->error_code, sizeof code, cudaMemcpyDeviceToHost));
+  if (code) return fail(CANNIKIN_ERR_CUDA, "gns_stats: device protocol error %d", code);
+  for (int j = 0; j < W; ++j) out_local_sq[j] = ctx->h_stats[j];
+  *out_global_sq = ctx->h_stats[W];
+  return CANNIKIN_OK;
+}
+
+extern "C" cannikin_status cannikin_gns_stats_async(cannikin_ctx* ctx, double* d_out, void* stream) {
+  if (!ctx || !d_out) return fail(CANNIKIN_ERR_INVALID, "gns_stats_async: NULL argument");
+  CK_CUDA(cudaSetDevice(ctx->device));
+  const size_t bytes = sizeof(double) * (ctx->world + 1);
+  CK_CUDA(cudaMemcpyAsync(d_out, ctx->ctrl->stats, bytes, cudaMemcpyDeviceToDevice, S(stream)));
+  CK_CUDA(cudaMemsetAsync(ctx->ctrl->stats, 0, bytes, S(stream)));
+  return CANNIKIN_OK;
+}
+
+extern "C" cannikin_status cannikin_weighted_sum_local(cannikin_ctx* ctx, const void* const* in,
+                                                       int n_ranks, const double* r, void* out,
+                                                       size_t n, cannikin_dtype dt,
+                                                       double* d_local_sq, double* d_global_sq,
+                                                       unsigned flags, void* stream) {
+  if (!ctx) return fail(CANNIKIN_ERR_INVALID, "weighted_sum_local: ctx == NULL");
+  ctx->last_launches = 0;
+  if (dt != CANNIKIN_F32 && dt != CANNIKIN_BF16)
+    return fail(CANNIKIN_ERR_UNSUPPORTED, "weighted_sum_local: dtype %d", (int)dt);
+  if (n_ranks < 1 || n_ranks > CANNIKIN_MAX_EMULATED)
+    return fail(CANNIKIN_ERR_UNSUPPORTED, "weighted_sum_local: n_ranks=%d outside 1..%d", n_ranks,
+                CANNIKIN_MAX_EMULATED);
+  if (!in || !r || !d_local_sq || !d_global_sq)
+    return fail(CANNIKIN_ERR_INVALID, "weighted_sum_local: NULL argument");
+  if (n > 0 && !out) return fail(CANNIKIN_ERR_INVALID, "weighted_sum_local: out == NULL");
+  for (int j = 0; j < n_ranks; ++j) {
+    if (n > 0 && !in[j]) return fail(CANNIKIN_ERR_INVALID, "weighted_sum_local: in[%d] == NULL", j);
+    if (reinterpret_cast<uintptr_t>(in[j]) % 16)
+      return fail(CANNIKIN_ERR_INVALID, "weighted_sum_local: in[%d] not 16-byte aligned", j);
+    if (!(r[j] == r[j])) return fail(CANNIKIN_ERR_DOMAIN, "weighted_sum_local: r[%d] is NaN", j);
+  }
+  if (reinterpret_cast<uintptr_t>(out) % 16)
+    return fail(CANNIKIN_ERR_INVALID, "weighted_sum_local: out not 16-byte aligned");
+  CK_CUDA(cudaSetDevice(ctx->device));
+  CK_CUDA(cannikin::launch_wsum_local(ctx, in, n_ranks, r, out, n, dt, d_local_sq, d_global_sq,
+                                      (flags & CANNIKIN_ACCUMULATE) != 0, 0, S(stream)));
+  ctx->last_launches = 1;
+  return CANNIKIN_OK;
+}
+
+extern "C" cannikin_status cannikin_ddp_allreduce_mean(cannikin_ctx* ctx, void* bucket, size_t n,
+                                                       cannikin_dtype dt, void* stream) {
+  if (!ctx) return fail(CANNIKIN_ERR_INVALID, "ddp_allreduce_mean: ctx == NULL");
+  ctx->last_launches = 0;
+  if (dt != CANNIKIN_F32 && dt != CANNIKIN_BF16)
+    return fail(CANNIKIN_ERR_UNSUPPORTED, "ddp_allreduce_mean: dtype %d", (int)dt);
+  if (n == 0 || ctx->world == 1) return CANNIKIN_OK;
+  if (!bucket) return fail(CANNIKIN_ERR_INVALID, "ddp_allreduce_mean: bucket == NULL");
+  CK_CUDA(cudaSetDevice(ctx->device));
+  CK_NCCL(ncclAllReduce(bucket, bucket, n, dt == CANNIKIN_F32 ? ncclFloat32 : ncclBfloat16, ncclAvg,
+                        static_cast<ncclComm_t>(ctx->nccl_comm), S(stream)));
+  return CANNIKIN_OK;
+}
+
+extern "C" int cannikin_last_launch_count(cannikin_ctx* ctx) { return ctx ? ctx->last_launches : 0; }

@@ -1,0 +1,54 @@
+// Internal definition of cannikin_ctx and of the per-rank control region that lives at the start
+// of every rank's peer-mapped allocation.  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+
+#include "cannikin.h"
+
+namespace cannikin {
+
+constexpr int kMaxWorld = CANNIKIN_MAX_WORLD;
+constexpr int kMaxArBlocks = 256;      // grid cap of the two-shot kernel
+constexpr int kMaxLocalBlocks = 2048;  // grid cap of the emulated-rank kernel
+constexpr int kMaxEmu = CANNIKIN_MAX_EMULATED;
+
+// Control region of one rank.  Fields marked [peer] are written by peers over NVLink; fields
+// marked [local] only by this rank's own kernels.  Flags carry monotonically increasing epochs
+// (never reset), so back-to-back buckets need no re-initialisation (no reset races).
+struct Ctrl {
+  uint64_t entry[kMaxArBlocks][kMaxWorld];                   // [peer] "bucket ready" epoch
+  uint64_t exit_[kMaxArBlocks][kMaxWorld];                   // [peer] "shard pushed" epoch
+  double rv[kMaxArBlocks][kMaxWorld];                        // [peer] r_src for this bucket
+  uint64_t meta[kMaxArBlocks][kMaxWorld];                    // [peer] (heap offset, n) check word
+  double part[kMaxWorld][kMaxArBlocks][kMaxWorld + 1];       // [peer] norm partials [src][blk][j]
+  uint64_t epoch[kMaxArBlocks];                              // [local] per-block epoch counter
+  unsigned ticket_ar;                                        // [local] last-block-done ticket
+  unsigned ticket_local;
+  int error_code;                                            // [local] protocol error (trap reason)
+  int pad_;
+  double stats[kMaxWorld + 1];                               // [local] accumulated |g_j|^2, |g|^2
+  double local_part[kMaxLocalBlocks][kMaxEmu + 1];           // [local] emulated-kernel partials
+};
+
+}  // namespace cannikin
+
+struct cannikin_ctx {
+  int rank = 0, world = 1, device = 0;
+  int grid_ar = 148;
+  int num_sms = 148;
+  size_t heap_bytes = 0;
+  // local allocation = [Ctrl | user heap (heap_bytes) | scratch (heap_bytes)]
+  char* base = nullptr;
+  size_t ctrl_bytes = 0, user_off = 0, scratch_off = 0, total_bytes = 0;
+  char* peer_base[cannikin::kMaxWorld] = {};
+  cannikin::Ctrl* ctrl = nullptr;
+  void* nccl_comm = nullptr;  // ncclComm_t
+  std::map<size_t, size_t> free_blocks;  // offset -> size within the user heap
+  std::map<size_t, size_t> used_blocks;
+  double* h_stats = nullptr;  // pinned host staging for gns_stats
+  int last_launches = 0;
+  uint64_t spin_timeout_ns = 20ull * 1000 * 1000 * 1000;
+};

@@ -1,0 +1,147 @@
+// Device helpers: 16-byte vector memory ops, dtype packing, deterministic block reductions and
+// system-scope flag operations for the NVLink peer-memory protocol.  sm_100a only.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cannikin {
+namespace dev {
+
+// ------------------------------------------------------------------ 16-byte memory operations
+// Streaming loads/stores: every gradient byte is touched exactly once per launch, so L1 is bypassed.
+__device__ __forceinline__ uint4 ld16(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st16(void* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// ------------------------------------------------------------------ dtype traits (16-byte vectors)
+template <typename T>
+struct Vec;
+
+template <>
+struct Vec<float> {
+  static constexpr int E = 4;  // elements per 16-byte vector
+  __device__ __forceinline__ static void unpack(const uint4& v, float (&f)[4]) {
+    f[0] = __uint_as_float(v.x);
+    f[1] = __uint_as_float(v.y);
+    f[2] = __uint_as_float(v.z);
+    f[3] = __uint_as_float(v.w);
+  }
+  __device__ __forceinline__ static uint4 pack(const float (&f)[4]) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                      __float_as_uint(f[3]));
+  }
+  __device__ __forceinline__ static float load1(const void* p) {
+    return *reinterpret_cast<const float*>(p);
+  }
+  __device__ __forceinline__ static void store1(void* p, float x) {
+    *reinterpret_cast<float*>(p) = x;
+  }
+};
+
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int E = 8;
+  // a bf16 is the upper half of an fp32: widening is a shift (exact)
+  __device__ __forceinline__ static void unpack(const uint4& v, float (&f)[8]) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+  // round-to-nearest-even, once, from the fp32 accumulator
+  __device__ __forceinline__ static uint4 pack(const float (&f)[8]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  __device__ __forceinline__ static float load1(const void* p) {
+    return __uint_as_float(uint32_t(*reinterpret_cast<const uint16_t*>(p)) << 16);
+  }
+  __device__ __forceinline__ static void store1(void* p, float x) {
+    *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(x);
+  }
+};
+
+// ------------------------------------------------------------------ deterministic reductions
+// Butterfly over the 32 lanes: every lane ends with the same, order-fixed sum.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Reduce NV doubles over the block; the result is valid in thread 0.  `smem` holds >= 32*NV
+// doubles.  Fixed order (butterfly within warps, then warps 0..nw-1 in sequence).
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) smem[warp * NV + j] = v[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += smem[w * NV + j];
+      v[j] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// Sum of `count` doubles at base[i*stride] (i = 0..count-1) over the whole block, fixed order:
+// thread t sums i = t, t+T, t+2T, ... then the block butterfly/warp-order reduction.
+// Loads go to L2 (.cg): the values were written by other CTAs / other GPUs during this launch.
+// Result valid in thread 0.
+__device__ __forceinline__ double block_strided_sum(const double* base, int count, int stride,
+                                                    double* smem) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) s += __ldcg(base + (size_t)i * stride);
+  double v[1] = {s};
+  block_sum<1>(v, smem);
+  return v[0];
+}
+
+// ------------------------------------------------------------------ system-scope flags
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys_f64(double* p, double v) {
+  asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+}  // namespace dev
+}  // namespace cannikin

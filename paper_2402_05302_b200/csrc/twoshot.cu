@@ -1,0 +1,258 @@
+// K3: fused weighted all-reduce over NVLink peer memory (two-shot), with the GNS norm statistics.
+//
+// For W ranks, rank k owns the contiguous shard S_k of the bucket.  One kernel:
+//   0. entry barrier: every CTA b publishes (r_k, bucket identity) and an epoch flag to CTA b of
+//      every peer, then waits for theirs ("all g_j are ready");
+//   1. reduce-scatter (row a2): for e in S_k, acc_e = sum_{j=0..W-1} r_j g_j[e] in fp32, reading
+//      g_j from peer j's bucket over NVLink (Eq. 9), and in the same loop
+//      L_k[j] = sum_{e in S_k} g_j[e]^2 (every rank's local norm on this shard, Eq. 10 input) and
+//      Gg_k = sum_{e in S_k} acc_e^2;
+//   2. all-gather (row a3): the reduced vector (rounded ONCE to the bucket dtype) is pushed into
+//      every peer's bucket at the same place, so all ranks end with identical bits;
+//   3. the CTA's W+1 norm partials are pushed into every peer's partial pad (row a4);
+//   4. exit barrier: "my shard and partials have landed at every peer";
+//   5. the last CTA to finish sums all ranks' partials in fixed (rank, CTA) order and adds them
+//      to the ctx accumulator -- identical bits on every rank (K5).
+// Only rank k ever reads or writes region S_k of any bucket, so two barriers suffice.  Flags are
+// monotonically increasing epochs (no reset), making back-to-back buckets and CUDA-graph replay
+// safe.  NVLink bytes per rank and direction: 2 (W-1)/W N s -- the ring all-reduce's volume
+// (P:167), with the scaling and both norms fused at zero extra bytes.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "ctx.h"
+#include "device_utils.cuh"
+
+namespace cannikin {
+
+struct ArArgs {
+  char* bucket[kMaxWorld];  // this bucket as seen in each rank's mapping (own included)
+  Ctrl* pctrl[kMaxWorld];   // control regions of all ranks (own included), mapped
+  Ctrl* ctrl;               // own control region
+  size_t nvec, n;           // full 16-byte vectors / elements
+  size_t shard_lo, shard_hi;  // this rank's vector range
+  uint64_t meta;            // identity of (offset, n, dtype, grid): must agree on every rank
+  uint64_t timeout_ns;
+  double r_me;
+  int rank;
+};
+
+__device__ __forceinline__ void spin_until(const uint64_t* flag, uint64_t ep, Ctrl* ctrl,
+                                           uint64_t timeout_ns, int code) {
+  uint64_t t0 = 0;
+  unsigned it = 0;
+  while (dev::ld_acquire_sys(flag) < ep) {
+    if ((++it & 1023u) == 0u) {
+      const uint64_t now = dev::globaltimer_ns();
+      if (t0 == 0) {
+        t0 = now;
+      } else if (now - t0 > timeout_ns) {
+        atomicExch(&ctrl->error_code, code);
+        __trap();  // a peer never arrived: fail loudly instead of hanging the GPU
+      }
+    }
+  }
+}
+
+template <typename T, int W>
+__device__ __forceinline__ void reduce_vec(const uint4 (&x)[W], const float (&r)[W],
+                                           char* const (&dst)[W], size_t off, double (&lsq)[W],
+                                           double& gsq) {
+  using V = dev::Vec<T>;
+  constexpr int E = V::E;
+  float acc[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = 0.0f;
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    float g[E];
+    V::unpack(x[j], g);
+    float sq = 0.0f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      acc[e] = fmaf(r[j], g[e], acc[e]);
+      sq = fmaf(g[e], g[e], sq);
+    }
+    lsq[j] += (double)sq;
+  }
+  float gs = 0.0f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) gs = fmaf(acc[e], acc[e], gs);
+  gsq += (double)gs;
+  const uint4 y = V::pack(acc);
+#pragma unroll
+  for (int j = 0; j < W; ++j) dev::st16(dst[j] + off, y);
+}
+
+template <typename T, int W, int U>
+__global__ void __launch_bounds__(512, 1) twoshot_kernel(const ArArgs a) {
+  using V = dev::Vec<T>;
+  constexpr int E = V::E;
+  __shared__ double red[32 * (W + 1)];
+  __shared__ double s_part[W + 1];
+  __shared__ float s_r[W];
+  __shared__ uint64_t s_ep;
+  __shared__ bool s_last;
+  const int b = blockIdx.x, tid = threadIdx.x;
+
+  if (tid == 0) s_ep = a.ctrl->epoch[b] + 1;
+  __syncthreads();
+  const uint64_t ep = s_ep;
+
+  // ---- 0. entry barrier (+ exchange of r_j and the bucket identity)
+  if (tid < W) {
+    Ctrl* pc = a.pctrl[tid];
+    dev::st_relaxed_sys_f64(&pc->rv[b][a.rank], a.r_me);
+    dev::st_relaxed_sys_u64(&pc->meta[b][a.rank], a.meta);
+    dev::st_release_sys(&pc->entry[b][a.rank], ep);
+    spin_until(&a.ctrl->entry[b][tid], ep, a.ctrl, a.timeout_ns, 1);
+    s_r[tid] = (float)a.ctrl->rv[b][tid];
+    if (a.ctrl->meta[b][tid] != a.meta) {
+      atomicExch(&a.ctrl->error_code, 2);  // ranks disagree on bucket offset/size/dtype/grid
+      __trap();
+    }
+  }
+  __syncthreads();
+
+  float r[W];
+  char* dst[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    r[j] = s_r[j];
+    dst[j] = a.bucket[j];
+  }
+  double lsq[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) lsq[j] = 0.0;
+  double gsq = 0.0;
+
+  // ---- 1+2. reduce-scatter on S_rank, fused norms, push to every peer
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t v = a.shard_lo + (size_t)b * blockDim.x + tid;
+  for (; v + (U - 1) * stride < a.shard_hi; v += U * stride) {
+    uint4 x[U][W];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < W; ++j) x[u][j] = dev::ld16(dst[j] + (v + u * stride) * 16);
+#pragma unroll
+    for (int u = 0; u < U; ++u) reduce_vec<T, W>(x[u], r, dst, (v + u * stride) * 16, lsq, gsq);
+  }
+  for (; v < a.shard_hi; v += stride) {
+    uint4 x[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) x[j] = dev::ld16(dst[j] + v * 16);
+    reduce_vec<T, W>(x, r, dst, v * 16, lsq, gsq);
+  }
+  // ragged tail (< one vector of elements): owned by the last rank, CTA 0
+  if (a.rank == W - 1 && b == 0) {
+    const size_t e = a.nvec * E + tid;
+    if (e < a.n) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        const float g = V::load1(dst[j] + e * sizeof(T));
+        acc = fmaf(r[j], g, acc);
+        lsq[j] += (double)(g * g);
+      }
+      gsq += (double)(acc * acc);
+#pragma unroll
+      for (int j = 0; j < W; ++j) V::store1(dst[j] + e * sizeof(T), acc);
+    }
+  }
+
+  // ---- 3. per-CTA norm partials -> every peer's pad
+  double vals[W + 1];
+#pragma unroll
+  for (int j = 0; j < W; ++j) vals[j] = lsq[j];
+  vals[W] = gsq;
+  dev::block_sum<W + 1>(vals, red);
+  if (tid == 0) {
+#pragma unroll
+    for (int j = 0; j <= W; ++j) s_part[j] = vals[j];
+  }
+  __syncthreads();  // also: every data store of this CTA has been issued
+
+  // ---- 4. exit barrier
+  if (tid < W) {
+    Ctrl* pc = a.pctrl[tid];
+#pragma unroll
+    for (int j = 0; j <= W; ++j) dev::st_relaxed_sys_f64(&pc->part[a.rank][b][j], s_part[j]);
+    __threadfence_system();
+    dev::st_release_sys(&pc->exit_[b][a.rank], ep);
+    spin_until(&a.ctrl->exit_[b][tid], ep, a.ctrl, a.timeout_ns, 3);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    a.ctrl->epoch[b] = ep;
+    __threadfence();
+    s_last = (atomicAdd(&a.ctrl->ticket_ar, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+
+  // ---- 5. fixed-order total over (rank, CTA) -> ctx accumulator
+  for (int j = 0; j <= W; ++j) {
+    double tot = 0.0;
+    for (int src = 0; src < W; ++src) {
+      const double s =
+          dev::block_strided_sum(&a.ctrl->part[src][0][j], gridDim.x, kMaxWorld + 1, red);
+      if (tid == 0) tot += s;
+    }
+    if (tid == 0) a.ctrl->stats[j] += tot;
+  }
+  if (tid == 0) a.ctrl->ticket_ar = 0u;
+}
+
+template <typename T, int W>
+static cudaError_t launch_w(const ArArgs& a, int grid, cudaStream_t st) {
+  constexpr int U = W <= 2 ? 4 : (W <= 4 ? 2 : 1);
+  twoshot_kernel<T, W, U><<<grid, 512, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t dispatch_w(int W, const ArArgs& a, int grid, cudaStream_t st) {
+  switch (W) {
+    case 2: return launch_w<T, 2>(a, grid, st);
+    case 3: return launch_w<T, 3>(a, grid, st);
+    case 4: return launch_w<T, 4>(a, grid, st);
+    case 5: return launch_w<T, 5>(a, grid, st);
+    case 6: return launch_w<T, 6>(a, grid, st);
+    case 7: return launch_w<T, 7>(a, grid, st);
+    case 8: return launch_w<T, 8>(a, grid, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// Launch K3 on the bucket at byte offset `off` of every rank's allocation.
+cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
+                           cudaStream_t st) {
+  const int W = ctx->world;
+  ArArgs a{};
+  for (int j = 0; j < W; ++j) {
+    a.bucket[j] = ctx->peer_base[j] + off;
+    a.pctrl[j] = reinterpret_cast<Ctrl*>(ctx->peer_base[j]);
+  }
+  a.ctrl = ctx->ctrl;
+  const size_t esz = dt == CANNIKIN_F32 ? 4 : 2;
+  a.n = n;
+  a.nvec = n * esz / 16;
+  size_t L = a.nvec / W;
+  L -= L % 64;  // shard boundaries on 1 KiB
+  a.shard_lo = L * (size_t)ctx->rank;
+  a.shard_hi = (ctx->rank == W - 1) ? a.nvec : L * (size_t)(ctx->rank + 1);
+  uint64_t meta = (uint64_t)off * 0x9E3779B97F4A7C15ull;
+  meta ^= (uint64_t)n * 0xC2B2AE3D27D4EB4Full;
+  meta ^= ((uint64_t)ctx->grid_ar << 8) ^ (uint64_t)dt;
+  a.meta = meta;
+  a.timeout_ns = ctx->spin_timeout_ns;
+  a.r_me = r_i;
+  a.rank = ctx->rank;
+  if (dt == CANNIKIN_F32) return dispatch_w<float>(W, a, ctx->grid_ar, st);
+  return dispatch_w<__nv_bfloat16>(W, a, ctx->grid_ar, st);
+}
+
+}  // namespace cannikin

@@ -1,0 +1,222 @@
+// K2: single-GPU fused pass over n emulated ranks (the 1-B200 metric kernel).
+//
+//   out[e]        = sum_{j=0..n-1} r_j in_j[e]          Eq. 9, fp32, rank order
+//   local_sq[j]   = sum_e in_j[e]^2                     |g_j|^2, Eq. 10 input
+//   global_sq     = sum_e acc[e]^2                      |g|^2 from the fp32 accumulator (reading Q2)
+//
+// HBM-bound: (n+1) * N * sizeof(T) algorithmic bytes, ~3 flops per element and rank.  Design:
+// persistent grid of (SMs x occupancy) CTAs of 256 threads, each thread streams 16-byte vectors
+// with n*U independent 128-bit loads in flight, L1 bypassed; norms are accumulated per thread in
+// fp32 over one vector and fp64 beyond; per-CTA partials are reduced by the last CTA to finish
+// (ticket) in a fixed order, so the result is bitwise deterministic for a fixed grid.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "ctx.h"
+#include "device_utils.cuh"
+
+namespace cannikin {
+
+struct LocalArgs {
+  const char* in[kMaxEmu];
+  float r[kMaxEmu];
+  char* out;
+  size_t nvec;     // full 16-byte vectors
+  size_t n;        // elements
+  double* partials;  // [grid][n+1]
+  unsigned* ticket;
+  double* local_sq;  // [n]
+  double* global_sq;
+  int accumulate;
+};
+
+template <typename T, int NR>
+__device__ __forceinline__ void wsum_vec(const uint4 (&x)[NR], const float (&r)[NR], char* dst,
+                                         double (&lsq)[NR], double& gsq) {
+  using V = dev::Vec<T>;
+  constexpr int E = V::E;
+  float acc[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = 0.0f;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    float g[E];
+    V::unpack(x[j], g);
+    float sq = 0.0f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      acc[e] = fmaf(r[j], g[e], acc[e]);
+      sq = fmaf(g[e], g[e], sq);
+    }
+    lsq[j] += (double)sq;
+  }
+  float gs = 0.0f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) gs = fmaf(acc[e], acc[e], gs);
+  gsq += (double)gs;
+  dev::st16(dst, V::pack(acc));
+}
+
+template <typename T, int NR, int U>
+__global__ void __launch_bounds__(256) wsum_local_kernel(const LocalArgs a) {
+  using V = dev::Vec<T>;
+  constexpr int E = V::E;
+  __shared__ double red[32 * (NR + 1)];
+  __shared__ bool s_last;
+
+  float r[NR];
+  const char* in[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    r[j] = a.r[j];
+    in[j] = a.in[j];
+  }
+  double lsq[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) lsq[j] = 0.0;
+  double gsq = 0.0;
+
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; v + (U - 1) * stride < a.nvec; v += U * stride) {
+    uint4 x[U][NR];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < NR; ++j) x[u][j] = dev::ld16(in[j] + (v + u * stride) * 16);
+#pragma unroll
+    for (int u = 0; u < U; ++u) wsum_vec<T, NR>(x[u], r, a.out + (v + u * stride) * 16, lsq, gsq);
+  }
+  for (; v < a.nvec; v += stride) {
+    uint4 x[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) x[j] = dev::ld16(in[j] + v * 16);
+    wsum_vec<T, NR>(x, r, a.out + v * 16, lsq, gsq);
+  }
+  // ragged tail (< one vector of elements) -- scalar, block 0
+  if (blockIdx.x == 0) {
+    const size_t e = a.nvec * E + threadIdx.x;
+    if (e < a.n) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const float g = V::load1(in[j] + e * sizeof(T));
+        acc = fmaf(r[j], g, acc);
+        lsq[j] += (double)(g * g);
+      }
+      gsq += (double)(acc * acc);
+      V::store1(a.out + e * sizeof(T), acc);
+    }
+  }
+
+  double vals[NR + 1];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) vals[j] = lsq[j];
+  vals[NR] = gsq;
+  dev::block_sum<NR + 1>(vals, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j <= NR; ++j) a.partials[(size_t)blockIdx.x * (NR + 1) + j] = vals[j];
+    __threadfence();
+    const unsigned t = atomicAdd(a.ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // last CTA: fixed-order tree over the per-CTA partials (K5)
+  for (int j = 0; j <= NR; ++j) {
+    const double s = dev::block_strided_sum(a.partials + j, gridDim.x, NR + 1, red);
+    if (threadIdx.x == 0) {
+      double* dst = (j < NR) ? (a.local_sq + j) : a.global_sq;
+      *dst = a.accumulate ? (*dst + s) : s;
+    }
+  }
+  if (threadIdx.x == 0) *a.ticket = 0u;
+}
+
+// ------------------------------------------------------------------------------ host launcher
+template <typename T, int NR>
+static cudaError_t launch_t(const LocalArgs& a, int grid, cudaStream_t st) {
+  constexpr int U = NR <= 2 ? 4 : (NR <= 4 ? 2 : 1);
+  wsum_local_kernel<T, NR, U><<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T, int NR>
+static int occupancy_grid(int num_sms) {
+  constexpr int U = NR <= 2 ? 4 : (NR <= 4 ? 2 : 1);
+  static int cached = 0;
+  if (!cached) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wsum_local_kernel<T, NR, U>, 256,
+                                                      0) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    cached = per_sm;
+  }
+  int g = cached * num_sms;
+  return g > kMaxLocalBlocks ? kMaxLocalBlocks : g;
+}
+
+template <typename T>
+static cudaError_t dispatch(int nr, const LocalArgs& a, size_t nvec, int num_sms, int grid_override,
+                            cudaStream_t st) {
+  int grid = 0;
+  switch (nr) {
+#define CANNIKIN_CASE(K)                                                         \
+  case K:                                                                        \
+    grid = grid_override > 0 ? grid_override : occupancy_grid<T, K>(num_sms);    \
+    break;
+    CANNIKIN_CASE(1) CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5)
+    CANNIKIN_CASE(6) CANNIKIN_CASE(7) CANNIKIN_CASE(8) CANNIKIN_CASE(9) CANNIKIN_CASE(10)
+    CANNIKIN_CASE(11) CANNIKIN_CASE(12) CANNIKIN_CASE(13) CANNIKIN_CASE(14) CANNIKIN_CASE(15)
+    CANNIKIN_CASE(16)
+#undef CANNIKIN_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+  // do not launch CTAs that would own no vector (keeps tiny buckets cheap)
+  const size_t need = (nvec + 255) / 256;
+  if ((size_t)grid > need) grid = need < 1 ? 1 : (int)need;
+  if (grid > kMaxLocalBlocks) grid = kMaxLocalBlocks;
+  switch (nr) {
+#define CANNIKIN_CASE(K) \
+  case K:                \
+    return launch_t<T, K>(a, grid, st);
+    CANNIKIN_CASE(1) CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5)
+    CANNIKIN_CASE(6) CANNIKIN_CASE(7) CANNIKIN_CASE(8) CANNIKIN_CASE(9) CANNIKIN_CASE(10)
+    CANNIKIN_CASE(11) CANNIKIN_CASE(12) CANNIKIN_CASE(13) CANNIKIN_CASE(14) CANNIKIN_CASE(15)
+    CANNIKIN_CASE(16)
+#undef CANNIKIN_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+// Launch K2.  Validation is the caller's job (api.cu).
+cudaError_t launch_wsum_local(cannikin_ctx* ctx, const void* const* in, int nr, const double* r,
+                              void* out, size_t n, cannikin_dtype dt, double* d_local_sq,
+                              double* d_global_sq, bool accumulate, int grid_override,
+                              cudaStream_t st) {
+  LocalArgs a{};
+  for (int j = 0; j < nr; ++j) {
+    a.in[j] = static_cast<const char*>(in[j]);
+    a.r[j] = (float)r[j];
+  }
+  a.out = static_cast<char*>(out);
+  const size_t esz = dt == CANNIKIN_F32 ? 4 : 2;
+  a.n = n;
+  a.nvec = n * esz / 16;
+  a.partials = &ctx->ctrl->local_part[0][0];
+  a.ticket = &ctx->ctrl->ticket_local;
+  a.local_sq = d_local_sq;
+  a.global_sq = d_global_sq;
+  a.accumulate = accumulate ? 1 : 0;
+  // partial rows are (nr+1) doubles wide: reinterpret local_part as a flat array
+  if (dt == CANNIKIN_F32) return dispatch<float>(nr, a, a.nvec, ctx->num_sms, grid_override, st);
+  return dispatch<__nv_bfloat16>(nr, a, a.nvec, ctx->num_sms, grid_override, st);
+}
+
+}  // namespace cannikin
