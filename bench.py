@@ -1,0 +1,459 @@
+#!/usr/bin/env python
+"""Benchmark of the Cannikin data-parallel hot path on B200 (one JSON line on rank 0).
+
+A *step* is one pass of the whole hot path over one batch of synthetic gradients:
+  weighted aggregation g = sum_i r_i g_i with the fused norms |g_i|^2, |g|^2   (Eq. 9-10)
+  -> read the norm statistics -> heterogeneous GNS estimate (Theorem 1)
+  -> OptPerf split for the next step (opt_split).
+N = 1 : the ranks are emulated on one GPU (K2, `cannikin_weighted_sum_local`); metric bytes are
+        the kernel's HBM algorithmic bytes (n+1) N s.
+N > 1 : one process per GPU (torchrun); `cannikin_weighted_allreduce` (K3, NVLink two-shot);
+        metric bytes are the NVLink bus bytes of the whole job, n * 2(n-1)/n * N s.
+
+    python bench.py [--gpus N --steps K --warmup W --config c4 --impl {cannikin,reference}]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# ---------------------------------------------------------------------------- workloads
+# Gradient sizes from the paper's Table 4; 355M is BASELINE.json's sweep model.
+CONFIGS = {
+    "c1": {"workload": "c1: 3 emulated heterogeneous ranks, 2^20 fp32 gradient, b={32,64,96}",
+           "N": 1 << 20, "dtype": "f32", "n_emu": 3, "B": 192, "fixed_b": [32, 64, 96]},
+    "c2": {"workload": "c2: ResNet-18/CIFAR-10 gradient, 11,689,512 fp32, unequal b_i",
+           "N": 11_689_512, "dtype": "f32", "n_emu": 2, "B": 64, "fixed_b": [24, 40]},
+    "c3": {"workload": "c3: ResNet-50/ImageNet gradient, 25,557,032 fp32, P100/V100/A100 mix",
+           "N": 25_557_032, "dtype": "f32", "n_emu": 8, "B": 400},
+    "c4": {"workload": "c4: BERT-base SQuAD gradient, 110,000,000 bf16, P100/V100/A100 mix",
+           "N": 110_000_000, "dtype": "bf16", "n_emu": 8, "B": 96},
+    "c5": {"workload": "c5: 355M-param gradient, 354,823,168 fp32, P100/V100/A100 mix",
+           "N": 354_823_168, "dtype": "f32", "n_emu": 8, "B": 400},
+}
+
+# Heterogeneous node models (Eq. 3) with per-sample speed in the ratio of Table 1's
+# FP16 TFLOPS (A100 77.97, V100 31.4, P100 21.2) -- the C3/C4 emulated mix.
+TFLOPS = {"A100": 77.97, "V100": 31.4, "P100": 21.2}
+MIX = ["A100", "A100", "A100", "V100", "V100", "V100", "P100", "P100"]
+COMM = (0.20, 0.010, 0.004)  # gamma, T_o, T_u
+
+
+def node_models(n):
+    out = []
+    for i in range(n):
+        f = TFLOPS["A100"] / TFLOPS[MIX[i % len(MIX)]]
+        out.append((0.0004 * f, 0.004, 0.0008 * f, 0.002))  # q, s, k, m  (seconds)
+    return out
+
+
+def esize(dtype):
+    return 4 if dtype == "f32" else 2
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons DURING the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.lines, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
+                 "100", "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.25)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def ncu_traffic(tag):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(tag)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------- CPU oracle legs
+def oracle_step(gs, r, dtype, b, models, B):
+    """One oracle pass over a bounded sample: Eq. 9 + norms, GNS estimate, split."""
+    from oracle import aggregate as agg
+    from oracle import gns as ogns
+    from oracle import optsplit as osp
+
+    g, ls, gsq = agg.aggregate(gs, r, dtype)
+    if len(b) >= 2:
+        ogns.gns_estimate(ls, gsq, b)
+    osp.int_split_greedy(models, COMM, B)
+    return g
+
+
+def cpu_sample(cfg, n, sample_elems, seed=0):
+    import cannikin_synth as synth
+    from oracle import aggregate as agg
+
+    b = cfg.get("fixed_b") or [max(1, cfg["B"] // n)] * n
+    b = (b * n)[:n]
+    gs = synth.gns_gradients(n, sample_elems, b, seed=seed, dtype=cfg["dtype"])
+    return gs, agg.ratios(b), b
+
+
+def cpu_baseline(cfg, n, seconds=10.0, sample_elems=1 << 22):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    gs, r, b = cpu_sample(cfg, n, sample_elems)
+    models = node_models(n)
+    calls, t0 = 0, time.perf_counter()
+    while True:
+        oracle_step(gs, r, cfg["dtype"], b, models, cfg["B"])
+        calls += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    nbytes = (n + 1) * sample_elems * esize(cfg["dtype"])
+    return {"value": round(nbytes * calls / el / 1e9, 4), "unit": "GB/s", "cores": 1,
+            "kind": "oracle",
+            "sample": f"{calls} oracle passes over {n} ranks x {sample_elems} {cfg['dtype']} "
+                      f"elements (first 2^22 of the workload shape), {el:.1f} s, numpy float64 "
+                      "single-threaded"}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU oracle as it stands, on rank 0 only (others exit 0)."""
+    if rank != 0:
+        return
+    n = cfg["n_emu"] if world == 1 else world
+    sample = 1 << 22
+    gs, r, b = cpu_sample(cfg, n, sample)
+    models = node_models(n)
+    for _ in range(args.warmup):
+        oracle_step(gs, r, cfg["dtype"], b, models, cfg["B"])
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_step(gs, r, cfg["dtype"], b, models, cfg["B"])
+    el = time.perf_counter() - t0
+    nbytes = (n + 1) * sample * esize(cfg["dtype"])
+    val = nbytes * args.steps / el / 1e9
+    line = {"impl": "reference", "metric": "weighted-allreduce+GNS GB/s (% HBM/NVLink roofline)", "value": round(val, 4),
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "emulated_ranks": n,
+                       "sample_elements_per_rank": sample},
+            "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"each step: oracle Eq.9+norms over {n} x {sample} "
+                                       f"{cfg['dtype']} elements, GNS estimate, opt_split"},
+            "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="cannikin", choices=["cannikin", "reference"])
+    ap.add_argument("--n-emulated", type=int, default=0, help="N=1: emulated ranks (0 = config)")
+    ap.add_argument("--bucket-mb", type=float, default=0.0, help="bucket size per rank (0 = whole)")
+    ap.add_argument("--dtype", default=None, choices=[None, "f32", "bf16"])
+    ap.add_argument("--grid", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = dict(CONFIGS[args.config])
+    if args.dtype:
+        cfg["dtype"] = args.dtype
+    if args.n_emulated:
+        cfg["n_emu"] = args.n_emulated
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import numpy as np
+    import torch
+
+    import cannikin_synth as synth
+    import paper_2402_05302_b200 as ck
+    from paper_2402_05302_b200 import torch_api as ta
+
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}[cfg["dtype"]]
+    N, s = cfg["N"], esize(cfg["dtype"])
+    n = cfg["n_emu"] if world == 1 else world
+    models = node_models(n)
+    split = ck.opt_split(models, COMM, cfg["B"]) if "fixed_b" not in cfg else None
+    b = cfg.get("fixed_b") if world == 1 and "fixed_b" in cfg else (split["b"] if split else None)
+    if b is None or len(b) != n:
+        b = ck.opt_split(models, COMM, max(cfg["B"], n))["b"]
+    B = sum(b)
+    r = [x / B for x in b]
+    bucket_elems = N if args.bucket_mb <= 0 else max(1, int(args.bucket_mb * 2**20) // s)
+    bucket_elems -= bucket_elems % 8
+    cuts = list(range(0, N, bucket_elems)) + [N]
+    stream = torch.cuda.current_stream()
+    peaks, peak_kind = measured_peaks()
+
+    def launches_per_step():
+        return len(cuts) - 1
+
+    if world == 1:
+        ctx = ck.Context(world=1, device=local_rank)
+        gs = synth.device_gns_gradients(n, N, b, seed=0, dtype=cfg["dtype"])
+        out = torch.empty(N, dtype=tdt, device="cuda")
+        stats_d = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+        local, glob = stats_d[:n], stats_d[n:]
+        stats_h = torch.empty(n + 1, dtype=torch.float64, pin_memory=True)
+        step_bytes = (n + 1) * N * s
+
+        def hot(kev=None):
+            for bi in range(len(cuts) - 1):
+                a, c = cuts[bi], cuts[bi + 1]
+                if kev is not None:
+                    kev[0].record(stream)
+                ta.weighted_sum_local(ctx, [g[a:c] for g in gs], r, out[a:c], local, glob,
+                                      accumulate=bi > 0)
+                if kev is not None:
+                    kev[1].record(stream)
+                    kev[2].append(kev[0:2])
+                    kev[0:2] = [torch.cuda.Event(enable_timing=True),
+                                torch.cuda.Event(enable_timing=True)]
+
+        def finish_step():
+            stats_h.copy_(stats_d, non_blocking=True)
+            stream.synchronize()
+            st = stats_h.tolist()
+            if n >= 2:
+                ck.gns_estimate(st[:n], st[n], b)
+            ck.opt_split(models, COMM, B)
+    else:
+        ctx = ta.init_distributed_context(heap_bytes=N * s, grid=args.grid)
+        bucket = ta.bucket_tensor(ctx, N, tdt)
+        g0 = synth.device_gns_gradients(n, N, b, seed=0, dtype=cfg["dtype"], ranks=[rank])[0]
+        bucket.copy_(g0)
+        del g0
+        step_bytes = n * 2 * (n - 1) * N * s // n  # whole-job NVLink bus bytes
+
+        def hot(kev=None):
+            for bi in range(len(cuts) - 1):
+                a, c = cuts[bi], cuts[bi + 1]
+                if kev is not None:
+                    kev[0].record(stream)
+                ta.weighted_allreduce(ctx, bucket[a:c], r[rank])
+                if kev is not None:
+                    kev[1].record(stream)
+                    kev[2].append(kev[0:2])
+                    kev[0:2] = [torch.cuda.Event(enable_timing=True),
+                                torch.cuda.Event(enable_timing=True)]
+
+        def finish_step():
+            loc, gsq = ctx.gns_stats(stream)
+            ck.gns_estimate(loc, gsq, b)
+            ck.opt_split(models, COMM, B)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(kev=None):
+        hot(kev)
+        finish_step()
+
+    for _ in range(args.warmup):
+        step()
+    # ---- timed region: K steps, events on the launching stream, max over ranks
+    kev = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), []]
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(kev)
+        t1.record(stream)
+        barrier()
+    ms = t0.elapsed_time(t1)
+    kernel_ms = [a.elapsed_time(c) for a, c in kev[2]]
+    if dist is not None:
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        kk = torch.tensor([statistics.mean(kernel_ms)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(kk, op=dist.ReduceOp.MAX)
+        kmean = float(kk.item())
+    else:
+        kmean = statistics.mean(kernel_ms)
+    ms_step = ms / args.steps
+    value = step_bytes / (ms_step * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (per launch)
+    launch_bytes = step_bytes / launches_per_step()
+    if world == 1:
+        achieved = launch_bytes / (kmean * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+                "peak_kind": peak_kind, "kernel": "wsum_local_kernel (K2)",
+                "kernel_ms": round(kmean, 4),
+                "traffic": ncu_traffic(f"{args.config}_n{n}_{cfg['dtype']}_b{launches_per_step()}")}
+    else:
+        busbw = (N * s / len(cuts[:-1])) / (kmean * 1e-3) * 2 * (n - 1) / n / 1e9
+        roof = {"bound": "nvlink", "achieved": round(busbw, 1), "peak": 770.0, "unit": "GB/s",
+                "frac": round(busbw / 770.0, 4),
+                "peak_kind": "measured peer copy per GPU per direction (B200_PROFILING.md); 900 nominal",
+                "kernel": "twoshot_kernel (K3)", "kernel_ms": round(kmean, 4),
+                "traffic": ncu_traffic(f"{args.config}_w{n}_{cfg['dtype']}")}
+
+    # ---- DDP baseline (equal split, NCCL average) on the same bucket, N > 1
+    ddp = None
+    if world > 1:
+        for _ in range(3):
+            ta.ddp_allreduce_mean(ctx, bucket)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            ta.ddp_allreduce_mean(ctx, bucket)
+        e1.record(stream)
+        barrier()
+        dm = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda", dtype=torch.float64)
+        dist.all_reduce(dm, op=dist.ReduceOp.MAX)
+        ddp = {"ms_per_allreduce": round(float(dm.item()), 4),
+               "note": "ncclAllReduce(avg) of the same bucket, equal-split DDP semantics (Eq. 2)"}
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        if world == 1:
+            host = [torch.empty(N, dtype=tdt, pin_memory=True) for _ in range(n)]
+            for h, g in zip(host, gs):
+                h.copy_(g)
+            h2d = n * N * s
+
+            def e2e_step():
+                for h, g in zip(host, gs):
+                    g.copy_(h, non_blocking=True)
+                step()
+        else:
+            host = torch.empty(N, dtype=tdt, pin_memory=True)
+            host.copy_(bucket)
+            h2d = N * s
+
+            def e2e_step():
+                bucket.copy_(host, non_blocking=True)
+                step()
+        d2h = (n + 1) * 8
+        ek = max(3, min(args.steps, 10))
+        e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ek):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        em = torch.tensor([e0.elapsed_time(e1) / ek], device="cuda", dtype=torch.float64)
+        if dist is not None:
+            dist.all_reduce(em, op=dist.ReduceOp.MAX)
+        em = float(em.item())
+        e2e = {"value": round(step_bytes / (em * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "ms_per_step": round(em, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "steps": ek}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg, n)
+
+    if rank == 0:
+        line = {
+            "metric": "weighted-allreduce+GNS GB/s (% HBM/NVLink roofline)",
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+            "config": {"workload": cfg["workload"], "elements": N, "ranks": n,
+                       "emulated": world == 1, "b": b, "B": B,
+                       "buckets_per_step": launches_per_step(),
+                       "bytes_per_step": step_bytes,
+                       "bytes_model": "(n+1)*N*s HBM" if world == 1 else "n*2(n-1)/n*N*s NVLink",
+                       "l2": f"inputs larger than L2 ({step_bytes / 126e6:.1f}x 126 MB)"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "ddp_baseline": ddp,
+            "gpu_launches": launches_per_step() * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        ctx.close()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

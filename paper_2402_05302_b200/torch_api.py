@@ -1,0 +1,80 @@
+"""torch.Tensor conveniences over the C ABI (argument marshalling only).
+
+PyTorch supplies device memory, streams and process groups; every step of the hot path runs in
+libcannikin.so.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import BF16, F32, Context, get_unique_id
+
+_CODES = {torch.float32: F32, torch.bfloat16: BF16}
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    if dt not in _CODES:
+        raise TypeError(f"cannikin supports float32 and bfloat16 gradients, not {dt}")
+    return _CODES[dt]
+
+
+class _DeviceView:
+    """Expose a raw device pointer owned by a cannikin ctx as a torch tensor (no copy)."""
+
+    def __init__(self, ptr: int, numel: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (numel,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def bucket_tensor(ctx: Context, numel: int, dtype: torch.dtype) -> torch.Tensor:
+    """Allocate a peer-mapped bucket from the ctx heap (collective for world > 1) and view it as a
+    tensor.  The ctx owns the memory; free it with ``free_bucket_tensor``."""
+    esz = torch.empty(0, dtype=dtype).element_size()
+    ptr = ctx.alloc_bucket(max(numel * esz, 1))
+    typestr = {torch.float32: "<f4", torch.bfloat16: "<i2"}[dtype]
+    t = torch.as_tensor(_DeviceView(ptr, numel, typestr), device=f"cuda:{ctx.device}")
+    return t.view(dtype) if dtype == torch.bfloat16 else t
+
+
+def free_bucket_tensor(ctx: Context, t: torch.Tensor):
+    ctx.free_bucket(t.data_ptr())
+
+
+def _cur(stream):
+    return stream if stream is not None else torch.cuda.current_stream()
+
+
+def weighted_allreduce(ctx: Context, bucket: torch.Tensor, r_i: float, stream=None):
+    """In place: bucket <- sum_j r_j g_j over all ranks (Eq. 9), norms accumulated in the ctx."""
+    assert bucket.is_cuda and bucket.is_contiguous()
+    ctx.weighted_allreduce(bucket.data_ptr(), bucket.numel(), dtype_code(bucket.dtype), r_i,
+                           _cur(stream))
+
+
+def weighted_sum_local(ctx: Context, grads, r, out: torch.Tensor, local_sq: torch.Tensor,
+                       global_sq: torch.Tensor, accumulate: bool = False, stream=None):
+    """Emulated ranks on one GPU: out <- sum_j r_j grads[j]; local_sq[j] <- |grads[j]|^2;
+    global_sq <- |out|^2 (float64 device tensors)."""
+    dt = dtype_code(out.dtype)
+    for g in grads:
+        assert g.is_cuda and g.is_contiguous() and g.dtype == out.dtype and g.numel() == out.numel()
+    assert local_sq.dtype == torch.float64 and global_sq.dtype == torch.float64
+    ctx.weighted_sum_local([g.data_ptr() for g in grads], list(r), out.data_ptr(), out.numel(), dt,
+                           local_sq.data_ptr(), global_sq.data_ptr(), accumulate, _cur(stream))
+
+
+def ddp_allreduce_mean(ctx: Context, bucket: torch.Tensor, stream=None):
+    ctx.ddp_allreduce_mean(bucket.data_ptr(), bucket.numel(), dtype_code(bucket.dtype), _cur(stream))
+
+
+def init_distributed_context(heap_bytes: int, grid: int = 0, group=None) -> Context:
+    """Create the ctx of this rank of an initialised torch.distributed group: rank 0 draws the NCCL
+    unique id, which is broadcast over the torch process group (plumbing only)."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    dev = torch.cuda.current_device()
+    return Context(rank=rank, world=world, unique_id=obj[0], device=dev, heap_bytes=heap_bytes,
+                   grid=grid)

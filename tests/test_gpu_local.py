@@ -1,0 +1,220 @@
+"""GPU parity of the single-GPU path (K2 emulated ranks; world-1 weighted_allreduce) against the
+oracle, through the C ABI.  Tolerances (BASELINE.json north_star; readings Q1-Q3 of DESIGN.md §4):
+  g        : max_e |gpu_e - ref_e| / max(sum_i |r_i g_i[e]|, 1e-30) <= 1e-5 (fp32), 1e-2 (bf16)
+  norms    : relative 1e-4
+  GNS      : G, S within 1e-4 of the oracle's scale (Q3)
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import cannikin_synth as synth  # noqa: E402
+import paper_2402_05302_b200 as ck  # noqa: E402
+from paper_2402_05302_b200 import torch_api as ta  # noqa: E402
+from oracle import aggregate as agg  # noqa: E402
+from oracle import gns as ogns  # noqa: E402
+
+TOL = {"f32": 1e-5, "bf16": 1e-2}
+TDT = {"f32": torch.float32, "bf16": torch.bfloat16}
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = ck.Context(world=1, device=0)
+    yield c
+    c.close()
+
+
+def to_dev(a, dtype):
+    if dtype == "bf16":
+        return torch.from_numpy(a.view(np.int16).copy()).cuda().view(torch.bfloat16)
+    return torch.from_numpy(a.copy()).cuda()
+
+
+def from_dev(t, dtype):
+    if dtype == "bf16":
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+def run_local(ctx, gs, r, dtype, out=None, accumulate=False, local=None, glob=None):
+    ins = [to_dev(g, dtype) for g in gs]
+    N = ins[0].numel()
+    if out is None:
+        out = torch.empty(N, dtype=TDT[dtype], device="cuda")
+    if local is None:
+        local = torch.zeros(len(gs), dtype=torch.float64, device="cuda")
+        glob = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ta.weighted_sum_local(ctx, ins, r, out, local, glob, accumulate=accumulate)
+    torch.cuda.synchronize()
+    return out, local, glob, ins
+
+
+def check(gs, r, dtype, out, local, glob):
+    g_ref, ls_ref, gs_ref = agg.aggregate(gs, r, dtype)
+    gs64 = [agg.to_f64(g, dtype) for g in gs]
+    got = agg.to_f64(from_dev(out, dtype), dtype)
+    if got.size:
+        scale = np.maximum(agg.elementwise_scale(gs64, r), 1e-30)
+        err = np.max(np.abs(got - g_ref) / scale)
+        assert err <= TOL[dtype], err
+    ls = local.cpu().numpy()
+    for j in range(len(gs)):
+        assert abs(ls[j] - ls_ref[j]) <= 1e-4 * max(ls_ref[j], 1e-300), (j, ls[j], ls_ref[j])
+    gv = float(glob.cpu()[0])
+    assert abs(gv - gs_ref) <= 1e-4 * max(gs_ref, 1e-300), (gv, gs_ref)
+    return g_ref, ls_ref, gs_ref
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("nr", [1, 2, 3, 5, 8, 16])
+@pytest.mark.parametrize("N", [1, 7, 4099, (1 << 20) + 3])
+def test_parity_sizes_ranks(ctx, dtype, nr, N):
+    b = [int(x) for x in np.random.default_rng(nr * 7 + N).integers(1, 200, size=nr)]
+    gs = synth.gns_gradients(nr, N, b, seed=nr + N, dtype=dtype)
+    r = agg.ratios(b)
+    out, local, glob, _ = run_local(ctx, gs, r, dtype)
+    check(gs, r, dtype, out, local, glob)
+
+
+def test_config1_end_to_end_gns(ctx):
+    """configs[0]: 3 emulated ranks, 2^20 fp32, b = {32, 64, 96}; the GNS estimate through the
+    library from the GPU norms matches the oracle's from its own norms (reading Q3)."""
+    b = [32, 64, 96]
+    gs = synth.gns_gradients(3, 1 << 20, b, seed=0, dtype="f32")
+    r = agg.ratios(b)
+    out, local, glob, _ = run_local(ctx, gs, r, "f32")
+    _, ls_ref, gs_ref = check(gs, r, "f32", out, local, glob)
+    est = ck.gns_estimate(local.cpu().tolist(), float(glob.cpu()[0]), b)
+    ref = ogns.gns_estimate(ls_ref, gs_ref, b)
+    B = sum(b)
+    for i in range(3):
+        scaleG = (B * gs_ref + b[i] * ls_ref[i]) / (B - b[i])
+        scaleS = b[i] * B / (B - b[i]) * (ls_ref[i] + gs_ref)
+        assert abs(est["Gi"][i] - ref["Gi"][i]) <= 1e-4 * scaleG
+        assert abs(est["Si"][i] - ref["Si"][i]) <= 1e-4 * scaleS
+    sG = sum(abs(w) * (B * gs_ref + bb * l) / (B - bb) for w, bb, l in zip(ref["wG"], b, ls_ref))
+    sS = sum(abs(w) * bb * B / (B - bb) * (l + gs_ref) for w, bb, l in zip(ref["wS"], b, ls_ref))
+    assert abs(est["G2"] - ref["G2"]) <= 1e-4 * sG
+    assert abs(est["trS"] - ref["trS"]) <= 1e-4 * sS
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_layered_precision_stress(ctx, dtype):
+    gs = synth.layered_gradients(4, (1 << 18) + 5, seed=3, dtype=dtype)
+    r = agg.ratios([5, 17, 40, 2])
+    out, local, glob, _ = run_local(ctx, gs, r, dtype)
+    check(gs, r, dtype, out, local, glob)
+
+
+def test_special_values(ctx):
+    N = 10007
+    zeros = [np.zeros(N, dtype=np.float32)] * 3
+    out, local, glob, _ = run_local(ctx, zeros, [0.2, 0.3, 0.5], "f32")
+    assert not out.any() and not local.any() and not glob.any()
+    g = synth.gns_gradients(1, N, [4], seed=1)[0]
+    out, local, glob, _ = run_local(ctx, [g, g, g], [0.0, 1.0, 0.0], "f32")
+    assert np.array_equal(out.cpu().numpy(), g)  # one-hot r copies g_1 exactly
+    gs = synth.gns_gradients(3, N, [1, 1, 1], seed=2)
+    out, local, glob, _ = run_local(ctx, gs, [1 / 3] * 3, "f32")
+    check(gs, [1 / 3] * 3, "f32", out, local, glob)  # equal b: plain mean
+
+
+def test_empty_bucket(ctx):
+    out, local, glob, _ = run_local(ctx, [np.zeros(0, np.float32)] * 2, [0.5, 0.5], "f32")
+    assert not local.any() and not glob.any()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_deterministic_bitwise(ctx, dtype):
+    gs = synth.gns_gradients(5, (1 << 20) + 11, [3, 9, 27, 81, 1], seed=9, dtype=dtype)
+    r = agg.ratios([3, 9, 27, 81, 1])
+    o1, l1, g1, _ = run_local(ctx, gs, r, dtype)
+    o2, l2, g2, _ = run_local(ctx, gs, r, dtype)
+    assert torch.equal(o1.view(torch.int16) if dtype == "bf16" else o1,
+                       o2.view(torch.int16) if dtype == "bf16" else o2)
+    assert torch.equal(l1, l2) and torch.equal(g1, g2)
+
+
+def test_in_place_and_accumulate(ctx):
+    """out may alias an input; ACCUMULATE sums stats over buckets (multi-bucket gradient)."""
+    N = 3 * 65536 + 8
+    b = [10, 20, 30]
+    gs = synth.gns_gradients(3, N, b, seed=4)
+    r = agg.ratios(b)
+    ins = [to_dev(g, "f32") for g in gs]
+    local = torch.zeros(3, dtype=torch.float64, device="cuda")
+    glob = torch.zeros(1, dtype=torch.float64, device="cuda")
+    cuts = [0, 65536, 2 * 65536 + 4, N]
+    for a, c in zip(cuts[:-1], cuts[1:]):
+        ta.weighted_sum_local(ctx, [x[a:c] for x in ins], r, ins[0][a:c], local, glob,
+                              accumulate=True)
+    torch.cuda.synchronize()
+    check(gs, r, "f32", ins[0], local, glob)
+
+
+def test_world1_allreduce_and_stats(ctx):
+    N = 123457
+    g = synth.gns_gradients(1, N, [8], seed=6)[0]
+    t = to_dev(g, "f32")
+    ta.weighted_allreduce(ctx, t, 1.0)
+    loc, glob = ctx.gns_stats()
+    ref = agg.sq_norm(agg.to_f64(g, "f32"))
+    assert np.array_equal(t.cpu().numpy(), g)
+    assert math.isclose(loc[0], ref, rel_tol=1e-6) and math.isclose(glob, ref, rel_tol=1e-6)
+    assert ctx.gns_stats() == ([0.0], 0.0)   # reset after read
+
+
+def test_errors(ctx):
+    x = torch.zeros(1024, device="cuda")
+    loc = torch.zeros(17, dtype=torch.float64, device="cuda")
+    glob = torch.zeros(1, dtype=torch.float64, device="cuda")
+    with pytest.raises(ck.CannikinError) as e:
+        ctx.weighted_sum_local([x.data_ptr()] * 17, [1 / 17] * 17, x.data_ptr(), 1024, ck.F32,
+                               loc.data_ptr(), glob.data_ptr())
+    assert e.value.name == "UNSUPPORTED"
+    with pytest.raises(ck.CannikinError) as e:
+        ctx.weighted_sum_local([x.data_ptr() + 4], [1.0], x.data_ptr(), 1000, ck.F32,
+                               loc.data_ptr(), glob.data_ptr())
+    assert e.value.name == "INVALID"
+    with pytest.raises(ck.CannikinError) as e:
+        ctx.weighted_allreduce(x.data_ptr(), 1024, 7, 1.0)
+    assert e.value.name == "UNSUPPORTED"
+
+
+@pytest.mark.parametrize("nr", [8])
+def test_full_size_c4_sampled(ctx, nr):
+    """configs[3] at full size in the bench launch configuration: 110M bf16, 8 emulated ranks.
+    Sampled elements vs the oracle one by one; the norms vs the oracle over the whole vectors."""
+    N = 110_000_000
+    b = [37, 29, 21, 12, 9, 8, 3, 1]
+    gs = synth.device_gns_gradients(nr, N, b, seed=0, dtype="bf16")
+    r = agg.ratios(b)
+    out = torch.empty(N, dtype=torch.bfloat16, device="cuda")
+    local = torch.zeros(nr, dtype=torch.float64, device="cuda")
+    glob = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ta.weighted_sum_local(ctx, gs, r, out, local, glob)
+    torch.cuda.synchronize()
+    idx = torch.from_numpy(np.random.default_rng(0).choice(N, 200_000, replace=False)).cuda()
+    samp = [from_dev(g[idx], "bf16") for g in gs]
+    ref = agg.weighted_sum([agg.to_f64(s, "bf16") for s in samp], r)
+    got = agg.to_f64(from_dev(out[idx], "bf16"), "bf16")
+    scale = np.maximum(agg.elementwise_scale([agg.to_f64(s, "bf16") for s in samp], r), 1e-30)
+    assert np.max(np.abs(got - ref) / scale) <= 1e-2
+    ls = local.cpu().numpy()
+    chunk = 10_000_000
+    gsum = 0.0
+    lsum = np.zeros(nr)
+    for a in range(0, N, chunk):
+        parts = [agg.to_f64(from_dev(g[a:a + chunk], "bf16"), "bf16") for g in gs]
+        for j in range(nr):
+            lsum[j] += agg.sq_norm(parts[j])
+        gsum += agg.sq_norm(agg.weighted_sum(parts, r))
+    assert np.allclose(ls, lsum, rtol=1e-4)
+    assert abs(float(glob.cpu()[0]) - gsum) <= 1e-4 * gsum
