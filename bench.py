@@ -218,6 +218,7 @@ def main():
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of a CUDA graph")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -259,41 +260,28 @@ def main():
     bucket_elems = N if args.bucket_mb <= 0 else max(1, int(args.bucket_mb * 2**20) // s)
     bucket_elems -= bucket_elems % 8
     cuts = list(range(0, N, bucket_elems)) + [N]
-    stream = torch.cuda.current_stream()
     peaks, peak_kind = measured_peaks()
 
     def launches_per_step():
         return len(cuts) - 1
 
+    stats_h = torch.empty(n + 1, dtype=torch.float64, pin_memory=True)
+    stats_d = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+    nb = len(cuts) - 1
     if world == 1:
         ctx = ck.Context(world=1, device=local_rank)
         gs = synth.device_gns_gradients(n, N, b, seed=0, dtype=cfg["dtype"])
         out = torch.empty(N, dtype=tdt, device="cuda")
-        stats_d = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
         local, glob = stats_d[:n], stats_d[n:]
-        stats_h = torch.empty(n + 1, dtype=torch.float64, pin_memory=True)
         step_bytes = (n + 1) * N * s
 
-        def hot(kev=None):
-            for bi in range(len(cuts) - 1):
-                a, c = cuts[bi], cuts[bi + 1]
-                if kev is not None:
-                    kev[0].record(stream)
-                ta.weighted_sum_local(ctx, [g[a:c] for g in gs], r, out[a:c], local, glob,
-                                      accumulate=bi > 0)
-                if kev is not None:
-                    kev[1].record(stream)
-                    kev[2].append(kev[0:2])
-                    kev[0:2] = [torch.cuda.Event(enable_timing=True),
-                                torch.cuda.Event(enable_timing=True)]
+        def launch(bi):
+            a, c = cuts[bi], cuts[bi + 1]
+            ta.weighted_sum_local(ctx, [g[a:c] for g in gs], r, out[a:c], local, glob,
+                                  accumulate=bi > 0)
 
-        def finish_step():
+        def read_stats():
             stats_h.copy_(stats_d, non_blocking=True)
-            stream.synchronize()
-            st = stats_h.tolist()
-            if n >= 2:
-                ck.gns_estimate(st[:n], st[n], b)
-            ck.opt_split(models, COMM, B)
     else:
         ctx = ta.init_distributed_context(heap_bytes=N * s, grid=args.grid)
         bucket = ta.bucket_tensor(ctx, N, tdt)
@@ -302,47 +290,74 @@ def main():
         del g0
         step_bytes = n * 2 * (n - 1) * N * s // n  # whole-job NVLink bus bytes
 
-        def hot(kev=None):
-            for bi in range(len(cuts) - 1):
-                a, c = cuts[bi], cuts[bi + 1]
-                if kev is not None:
-                    kev[0].record(stream)
-                ta.weighted_allreduce(ctx, bucket[a:c], r[rank])
-                if kev is not None:
-                    kev[1].record(stream)
-                    kev[2].append(kev[0:2])
-                    kev[0:2] = [torch.cuda.Event(enable_timing=True),
-                                torch.cuda.Event(enable_timing=True)]
+        def launch(bi):
+            a, c = cuts[bi], cuts[bi + 1]
+            ta.weighted_allreduce(ctx, bucket[a:c], r[rank])
 
-        def finish_step():
-            loc, gsq = ctx.gns_stats(stream)
-            ck.gns_estimate(loc, gsq, b)
-            ck.opt_split(models, COMM, B)
+        def read_stats():
+            ctx.gns_stats_async(stats_d.data_ptr(), torch.cuda.current_stream())
+            stats_h.copy_(stats_d, non_blocking=True)
+
+    # per-kernel timing events on the launching stream (external: recordable inside a graph)
+    evs = [(torch.cuda.Event(enable_timing=True, external=True),
+            torch.cuda.Event(enable_timing=True, external=True)) for _ in range(nb)]
+
+    def device_part():
+        for bi in range(nb):
+            evs[bi][0].record()
+            launch(bi)
+            evs[bi][1].record()
+        read_stats()
+
+    def host_part():
+        torch.cuda.current_stream().synchronize()
+        st = stats_h.tolist()
+        if n >= 2:
+            ck.gns_estimate(st[:n], st[n], b)
+        ck.opt_split(models, COMM, B)
+
+    graph = None
+    device_part()
+    host_part()
+    if not args.no_graph:
+        # the device half of a step is one CUDA graph (kernels + stats readback): no per-kernel
+        # host launch latency; the host half (GNS estimate, opt_split) runs after each replay
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            device_part()
+        torch.cuda.synchronize()
+
+    kernel_ms = []
+
+    def step(record=False):
+        if graph is not None:
+            graph.replay()
+        else:
+            device_part()
+        host_part()
+        if record:
+            kernel_ms.extend(a.elapsed_time(c) for a, c in evs)
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    def step(kev=None):
-        hot(kev)
-        finish_step()
-
     for _ in range(args.warmup):
         step()
     # ---- timed region: K steps, events on the launching stream, max over ranks
-    kev = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), []]
+    stream = torch.cuda.current_stream()
     with ClockSampler(local_rank) as clk:
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
         for _ in range(args.steps):
-            step(kev)
+            step(record=True)
         t1.record(stream)
         barrier()
     ms = t0.elapsed_time(t1)
-    kernel_ms = [a.elapsed_time(c) for a, c in kev[2]]
     if dist is not None:
         tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -401,7 +416,7 @@ def main():
             def e2e_step():
                 for h, g in zip(host, gs):
                     g.copy_(h, non_blocking=True)
-                step()
+                eager_step()
         else:
             host = torch.empty(N, dtype=tdt, pin_memory=True)
             host.copy_(bucket)
@@ -409,7 +424,13 @@ def main():
 
             def e2e_step():
                 bucket.copy_(host, non_blocking=True)
-                step()
+                eager_step()
+        def eager_step():  # the plain public-API calls a user makes, no graph
+            for bi in range(nb):
+                launch(bi)
+            read_stats()
+            host_part()
+
         d2h = (n + 1) * 8
         ek = max(3, min(args.steps, 10))
         e2e_step()
@@ -443,7 +464,11 @@ def main():
                        "buckets_per_step": launches_per_step(),
                        "bytes_per_step": step_bytes,
                        "bytes_model": "(n+1)*N*s HBM" if world == 1 else "n*2(n-1)/n*N*s NVLink",
-                       "l2": f"inputs larger than L2 ({step_bytes / 126e6:.1f}x 126 MB)"},
+                       "l2": (f"inputs larger than L2 ({step_bytes / 126e6:.1f}x 126 MB), no flush"
+                              if step_bytes > 2 * 126e6 else
+                              "working set fits in L2 (not flushed): latency-bound case, "
+                              "not a roofline claim"),
+                       "cuda_graph": graph is not None},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "ddp_baseline": ddp,
             "gpu_launches": launches_per_step() * args.steps,
             "clocks": clk.summary(),

@@ -1,0 +1,106 @@
+"""Per-rank worker for tests/test_gpu_multi.py (launched by torchrun, one process per GPU).
+
+Every rank draws ALL ranks' inputs of record on the host from the shared seeded generator (small
+sizes), loads its own into a bucket, runs cannikin_weighted_allreduce through the C ABI, and
+writes its output bits and norm statistics to <outdir>/rank<r>_<case>.npz for the parent test to
+compare against the oracle and across ranks.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import cannikin_synth as synth  # noqa: E402
+import paper_2402_05302_b200 as ck  # noqa: E402
+from paper_2402_05302_b200 import torch_api as ta  # noqa: E402
+
+CASES = [  # (name, N, dtype, seed)
+    ("tiny1", 1, "f32", 1),
+    ("odd7", 7, "bf16", 2),
+    ("small", 4099, "f32", 3),
+    ("mid_f32", (1 << 20) + 3, "f32", 4),
+    ("mid_bf16", (1 << 20) + 5, "bf16", 5),
+    ("big_bf16", 3_000_011, "bf16", 6),
+    ("resnet18", 11_689_512, "f32", 7),
+]
+
+
+def b_for(world, seed):
+    rng = np.random.default_rng(100 + seed)
+    return [int(x) for x in rng.integers(1, 97, size=world)]
+
+
+def to_dev(a, dtype):
+    if dtype == "bf16":
+        return torch.from_numpy(a.view(np.int16).copy()).cuda().view(torch.bfloat16)
+    return torch.from_numpy(a.copy()).cuda()
+
+
+def from_dev(t, dtype):
+    if dtype == "bf16":
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--grid", type=int, default=0)
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    lr = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(lr)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+    maxN = max(c[1] for c in CASES)
+    ctx = ta.init_distributed_context(heap_bytes=maxN * 4 + 4096, grid=args.grid)
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}
+    for name, N, dtype, seed in CASES:
+        b = b_for(world, seed)
+        B = sum(b)
+        gs = synth.gns_gradients(world, N, b, seed=seed, dtype=dtype)
+        # (1) zero-copy bucket in the symmetric heap
+        bucket = ta.bucket_tensor(ctx, N, tdt[dtype])
+        bucket.copy_(to_dev(gs[rank], dtype))
+        ta.weighted_allreduce(ctx, bucket, b[rank] / B)
+        loc, glob = ctx.gns_stats()
+        out1 = from_dev(bucket, dtype)
+        # (2) again (determinism, flag epochs advance)
+        bucket.copy_(to_dev(gs[rank], dtype))
+        ta.weighted_allreduce(ctx, bucket, b[rank] / B)
+        loc2, glob2 = ctx.gns_stats()
+        out2 = from_dev(bucket, dtype)
+        ta.free_bucket_tensor(ctx, bucket)
+        # (3) ordinary (non-peer-mapped) torch tensor: staged through the heap scratch
+        t = to_dev(gs[rank], dtype)
+        ta.weighted_allreduce(ctx, t, b[rank] / B)
+        loc3, glob3 = ctx.gns_stats()
+        out3 = from_dev(t, dtype)
+        # (4) the same gradient as 3 buckets of different sizes; stats accumulate over buckets
+        t = to_dev(gs[rank], dtype)
+        cuts = sorted({0, N // 3 - (N // 3) % 8, (2 * N) // 3 - ((2 * N) // 3) % 8, N})
+        for a, c in zip(cuts[:-1], cuts[1:]):
+            ta.weighted_allreduce(ctx, t[a:c], b[rank] / B)
+        loc4, glob4 = ctx.gns_stats()
+        out4 = from_dev(t, dtype)
+        np.savez(os.path.join(args.out, f"rank{rank}_{name}.npz"), out1=out1, out2=out2,
+                 out3=out3, out4=out4, loc=np.array(loc), glob=glob, loc2=np.array(loc2),
+                 glob2=glob2, loc3=np.array(loc3), glob3=glob3, loc4=np.array(loc4), glob4=glob4,
+                 b=np.array(b))
+    # DDP baseline semantics: mean of the ranks' buffers
+    x = torch.full((1000,), float(rank + 1), device="cuda")
+    ta.ddp_allreduce_mean(ctx, x)
+    torch.cuda.synchronize()
+    np.save(os.path.join(args.out, f"rank{rank}_ddp.npy"), x.cpu().numpy())
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

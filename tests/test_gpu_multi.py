@@ -1,0 +1,80 @@
+"""Multi-GPU parity of cannikin_weighted_allreduce (two-shot NVLink kernel) against the oracle,
+bitwise identity across ranks, run-to-run determinism, staging path, multi-bucket stats.
+Runs tests/mp_allreduce_worker.py under torchrun on every visible GPU (2..8)."""
+import os
+import socket
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import cannikin_synth as synth  # noqa: E402
+from oracle import aggregate as agg  # noqa: E402
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import mp_allreduce_worker as W  # noqa: E402
+
+TOL = {"f32": 1e-5, "bf16": 1e-2}
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def results():
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(torch.cuda.device_count(), 8)
+    d = tempfile.mkdtemp()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           os.path.join(os.path.dirname(__file__), "mp_allreduce_worker.py"), "--out", d]
+    env = dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    return world, d
+
+
+@pytest.mark.parametrize("case", W.CASES, ids=[c[0] for c in W.CASES])
+def test_parity_and_identity(results, case):
+    world, d = results
+    name, N, dtype, seed = case
+    ranks = [dict(np.load(os.path.join(d, f"rank{r}_{name}.npz"))) for r in range(world)]
+    b = [int(x) for x in ranks[0]["b"]]
+    gs = synth.gns_gradients(world, N, b, seed=seed, dtype=dtype)
+    r = agg.ratios(b)
+    g_ref, ls_ref, gsq_ref = agg.aggregate(gs, r, dtype)
+    scale = np.maximum(agg.elementwise_scale([agg.to_f64(g, dtype) for g in gs], r), 1e-30)
+    for k in ("out1", "out2", "out3", "out4"):
+        got = agg.to_f64(ranks[0][k], dtype)
+        err = np.max(np.abs(got - g_ref) / scale) if N else 0.0
+        assert err <= TOL[dtype], (k, err)
+        for q in range(1, world):  # bitwise identical on every rank
+            assert np.array_equal(ranks[q][k], ranks[0][k]), (k, q)
+    # the two zero-copy runs are bitwise identical (determinism)
+    assert np.array_equal(ranks[0]["out1"], ranks[0]["out2"])
+    for sfx in ("", "2", "3", "4"):
+        loc, glob = ranks[0]["loc" + sfx], float(ranks[0]["glob" + sfx])
+        assert np.allclose(loc, ls_ref, rtol=1e-4, atol=0), (sfx, loc, ls_ref)
+        assert abs(glob - gsq_ref) <= 1e-4 * max(gsq_ref, 1e-300), (sfx, glob, gsq_ref)
+        for q in range(1, world):
+            assert np.array_equal(ranks[q]["loc" + sfx], loc)
+            assert float(ranks[q]["glob" + sfx]) == glob
+    assert np.array_equal(ranks[0]["loc"], ranks[0]["loc2"])
+    assert float(ranks[0]["glob"]) == float(ranks[0]["glob2"])
+
+
+def test_ddp_baseline_mean(results):
+    world, d = results
+    x = np.load(os.path.join(d, "rank0_ddp.npy"))
+    assert np.allclose(x, (world + 1) / 2)
