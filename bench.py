@@ -126,7 +126,8 @@ def ncu_traffic(tag):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
-        return d.get(tag)
+        v = d.get(tag)
+        return float(v) if isinstance(v, (int, float)) else None
     except (OSError, ValueError):
         return None
 
@@ -265,23 +266,26 @@ def main():
     def launches_per_step():
         return len(cuts) - 1
 
-    stats_h = torch.empty(n + 1, dtype=torch.float64, pin_memory=True)
-    stats_d = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+    # two statistics buffers: the host half of step t (GNS estimate, split) runs while the GPU
+    # already executes step t+1 -- the paper consumes B_noise and r_opt per epoch, not per step
+    NBUF = 2
+    stats_h = [torch.empty(n + 1, dtype=torch.float64, pin_memory=True) for _ in range(NBUF)]
+    stats_d = [torch.zeros(n + 1, dtype=torch.float64, device="cuda") for _ in range(NBUF)]
+    ready = [torch.cuda.Event() for _ in range(NBUF)]
     nb = len(cuts) - 1
     if world == 1:
         ctx = ck.Context(world=1, device=local_rank)
         gs = synth.device_gns_gradients(n, N, b, seed=0, dtype=cfg["dtype"])
         out = torch.empty(N, dtype=tdt, device="cuda")
-        local, glob = stats_d[:n], stats_d[n:]
         step_bytes = (n + 1) * N * s
 
-        def launch(bi):
+        def launch(bi, k):
             a, c = cuts[bi], cuts[bi + 1]
-            ta.weighted_sum_local(ctx, [g[a:c] for g in gs], r, out[a:c], local, glob,
-                                  accumulate=bi > 0)
+            ta.weighted_sum_local(ctx, [g[a:c] for g in gs], r, out[a:c], stats_d[k][:n],
+                                  stats_d[k][n:], accumulate=bi > 0)
 
-        def read_stats():
-            stats_h.copy_(stats_d, non_blocking=True)
+        def read_stats(k):
+            stats_h[k].copy_(stats_d[k], non_blocking=True)
     else:
         ctx = ta.init_distributed_context(heap_bytes=N * s, grid=args.grid)
         bucket = ta.bucket_tensor(ctx, N, tdt)
@@ -290,62 +294,72 @@ def main():
         del g0
         step_bytes = n * 2 * (n - 1) * N * s // n  # whole-job NVLink bus bytes
 
-        def launch(bi):
+        def launch(bi, k):
             a, c = cuts[bi], cuts[bi + 1]
             ta.weighted_allreduce(ctx, bucket[a:c], r[rank])
 
-        def read_stats():
-            ctx.gns_stats_async(stats_d.data_ptr(), torch.cuda.current_stream())
-            stats_h.copy_(stats_d, non_blocking=True)
+        def read_stats(k):
+            ctx.gns_stats_async(stats_d[k].data_ptr(), torch.cuda.current_stream())
+            stats_h[k].copy_(stats_d[k], non_blocking=True)
 
     # per-kernel timing events on the launching stream (external: recordable inside a graph)
-    evs = [(torch.cuda.Event(enable_timing=True, external=True),
-            torch.cuda.Event(enable_timing=True, external=True)) for _ in range(nb)]
+    evs = [[(torch.cuda.Event(enable_timing=True, external=True),
+             torch.cuda.Event(enable_timing=True, external=True)) for _ in range(nb)]
+           for _ in range(NBUF)]
 
-    def device_part():
+    def device_part(k):
         for bi in range(nb):
-            evs[bi][0].record()
-            launch(bi)
-            evs[bi][1].record()
-        read_stats()
-
-    def host_part():
-        torch.cuda.current_stream().synchronize()
-        st = stats_h.tolist()
-        if n >= 2:
-            ck.gns_estimate(st[:n], st[n], b)
-        ck.opt_split(models, COMM, B)
-
-    graph = None
-    device_part()
-    host_part()
-    if not args.no_graph:
-        # the device half of a step is one CUDA graph (kernels + stats readback): no per-kernel
-        # host launch latency; the host half (GNS estimate, opt_split) runs after each replay
-        torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            device_part()
-        torch.cuda.synchronize()
+            evs[k][bi][0].record()
+            launch(bi, k)
+            evs[k][bi][1].record()
+        read_stats(k)
 
     kernel_ms = []
 
-    def step(record=False):
-        if graph is not None:
-            graph.replay()
-        else:
-            device_part()
-        host_part()
+    def host_part(k, record=False):
+        ready[k].synchronize()
+        st = stats_h[k].tolist()
+        if n >= 2:
+            ck.gns_estimate(st[:n], st[n], b)
+        ck.opt_split(models, COMM, B)
         if record:
-            kernel_ms.extend(a.elapsed_time(c) for a, c in evs)
+            kernel_ms.extend(a.elapsed_time(c) for a, c in evs[k])
+
+    graphs = None
+    for k in range(NBUF):
+        device_part(k)
+        ready[k].record()
+        host_part(k)
+    if not args.no_graph:
+        # the device half of a step is one CUDA graph (kernels + stats readback): no per-kernel
+        # host launch latency
+        torch.cuda.synchronize()
+        graphs = []
+        for k in range(NBUF):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                device_part(k)
+            graphs.append(g)
+        torch.cuda.synchronize()
+
+    def run_steps(count, record=False):
+        for t in range(count):
+            k = t % NBUF
+            if graphs is not None:
+                graphs[k].replay()
+            else:
+                device_part(k)
+            ready[k].record()
+            if t > 0:
+                host_part((t - 1) % NBUF, record)
+        host_part((count - 1) % NBUF, record)
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        step()
+    run_steps(args.warmup)
     # ---- timed region: K steps, events on the launching stream, max over ranks
     stream = torch.cuda.current_stream()
     with ClockSampler(local_rank) as clk:
@@ -353,8 +367,7 @@ def main():
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        for _ in range(args.steps):
-            step(record=True)
+        run_steps(args.steps, record=True)
         t1.record(stream)
         barrier()
     ms = t0.elapsed_time(t1)
@@ -425,11 +438,12 @@ def main():
             def e2e_step():
                 bucket.copy_(host, non_blocking=True)
                 eager_step()
-        def eager_step():  # the plain public-API calls a user makes, no graph
+        def eager_step():  # the plain public-API calls a user makes, no graph, no overlap
             for bi in range(nb):
-                launch(bi)
-            read_stats()
-            host_part()
+                launch(bi, 0)
+            read_stats(0)
+            ready[0].record()
+            host_part(0)
 
         d2h = (n + 1) * 8
         ek = max(3, min(args.steps, 10))
@@ -468,7 +482,8 @@ def main():
                               if step_bytes > 2 * 126e6 else
                               "working set fits in L2 (not flushed): latency-bound case, "
                               "not a roofline claim"),
-                       "cuda_graph": graph is not None},
+                       "cuda_graph": graphs is not None,
+                       "host_overlap": "host half of step t overlaps device half of step t+1"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "ddp_baseline": ddp,
             "gpu_launches": launches_per_step() * args.steps,
             "clocks": clk.summary(),
