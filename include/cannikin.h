@@ -135,8 +135,13 @@ cannikin_status cannikin_gns_stats_async(cannikin_ctx* ctx, double* d_out, void*
  *   d_local_sq  : device pointer, n_ranks doubles: |in[j]|^2
  *   d_global_sq : device pointer, 1 double: |out|^2 taken from the fp32 accumulator (reading Q2)
  *   flags & CANNIKIN_ACCUMULATE: add to d_local_sq/d_global_sq instead of overwriting (multi-bucket)
+ *   flags & CANNIKIN_LOCAL_LDG / CANNIKIN_LOCAL_TMA: force the 128-bit-load or the TMA-bulk-staged
+ *         kernel variant (identical output bits; norms equal up to fp64 summation grouping);
+ *         default: the faster one
  * 1 <= n_ranks <= CANNIKIN_MAX_EMULATED.  Errors: INVALID, UNSUPPORTED, CUDA. */
 #define CANNIKIN_ACCUMULATE 1u
+#define CANNIKIN_LOCAL_LDG 2u
+#define CANNIKIN_LOCAL_TMA 4u
 cannikin_status cannikin_weighted_sum_local(cannikin_ctx* ctx, const void* const* in, int n_ranks,
                                             const double* r, void* out, size_t n, cannikin_dtype dt,
                                             double* d_local_sq, double* d_global_sq, unsigned flags,

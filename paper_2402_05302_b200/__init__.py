@@ -27,6 +27,8 @@ __all__ = [
 
 F32, BF16 = 0, 1
 ACCUMULATE = 1
+LOCAL_LDG = 2
+LOCAL_TMA = 4
 ROUND_PAPER = 1
 GNS_G_NONPOSITIVE = 1
 MAX_WORLD = 8
@@ -180,11 +182,16 @@ class Context:
         _check(lib().cannikin_gns_stats_async(self._h, d_out, _stream(stream)))
 
     def weighted_sum_local(self, in_ptrs, r, out_ptr: int, n: int, dtype: int, d_local_sq: int,
-                           d_global_sq: int, accumulate: bool = False, stream=None):
+                           d_global_sq: int, accumulate: bool = False, stream=None,
+                           variant: str | None = None):
+        """variant: None (library default), "ldg" or "tma": same per-element arithmetic (identical
+        output bits); the fp64 norm partials differ only in summation grouping."""
         arr = (ctypes.c_void_p * len(in_ptrs))(*in_ptrs)
+        flags = (ACCUMULATE if accumulate else 0) | {None: 0, "ldg": LOCAL_LDG,
+                                                     "tma": LOCAL_TMA}[variant]
         _check(lib().cannikin_weighted_sum_local(self._h, arr, len(in_ptrs), _dbl(r), out_ptr, n,
-                                                 dtype, d_local_sq, d_global_sq,
-                                                 ACCUMULATE if accumulate else 0, _stream(stream)))
+                                                 dtype, d_local_sq, d_global_sq, flags,
+                                                 _stream(stream)))
 
     def ddp_allreduce_mean(self, ptr: int, n: int, dtype: int, stream=None):
         _check(lib().cannikin_ddp_allreduce_mean(self._h, ptr, n, dtype, _stream(stream)))

@@ -12,14 +12,7 @@
 
 using cannikin::fail;
 
-namespace cannikin {
-cudaError_t launch_wsum_local(cannikin_ctx* ctx, const void* const* in, int nr, const double* r,
-                              void* out, size_t n, cannikin_dtype dt, double* d_local_sq,
-                              double* d_global_sq, bool accumulate, int grid_override,
-                              cudaStream_t st);
-cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
-                           cudaStream_t st);
-}  // namespace cannikin
+#include "kernels.h"
 
 #define CK_CUDA(expr)                                                                     \
   do {                                                                                    \
@@ -85,6 +78,8 @@ extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world
   if (ce != cudaSuccess) { destroy_partial(ctx); CK_CUDA(ce); }
   ctx->grid_ar = grid > 0 ? grid : ctx->num_sms;
   if (ctx->grid_ar > cannikin::kMaxArBlocks) ctx->grid_ar = cannikin::kMaxArBlocks;
+  if (const char* t = std::getenv("CANNIKIN_K2_IMPL")) ctx->local_tma = std::strcmp(t, "tma") == 0;
+  if (const char* t = std::getenv("CANNIKIN_LOCAL_GRID")) ctx->grid_local = std::atoi(t);
   if (const char* t = std::getenv("CANNIKIN_SPIN_TIMEOUT_MS"))
     ctx->spin_timeout_ns = (uint64_t)std::strtoull(t, nullptr, 10) * 1000000ull;
   ctx->heap_bytes = align_up(heap_bytes, 256);
@@ -295,8 +290,16 @@ extern "C" cannikin_status cannikin_weighted_sum_local(cannikin_ctx* ctx, const 
   if (reinterpret_cast<uintptr_t>(out) % 16)
     return fail(CANNIKIN_ERR_INVALID, "weighted_sum_local: out not 16-byte aligned");
   CK_CUDA(cudaSetDevice(ctx->device));
-  CK_CUDA(cannikin::launch_wsum_local(ctx, in, n_ranks, r, out, n, dt, d_local_sq, d_global_sq,
-                                      (flags & CANNIKIN_ACCUMULATE) != 0, 0, S(stream)));
+  const bool acc = (flags & CANNIKIN_ACCUMULATE) != 0;
+  bool use_tma = ctx->local_tma;
+  if (flags & CANNIKIN_LOCAL_LDG) use_tma = false;
+  if (flags & CANNIKIN_LOCAL_TMA) use_tma = true;
+  if (use_tma)
+    CK_CUDA(cannikin::launch_wsum_local_tma(ctx, in, n_ranks, r, out, n, dt, d_local_sq,
+                                            d_global_sq, acc, S(stream)));
+  else
+    CK_CUDA(cannikin::launch_wsum_local(ctx, in, n_ranks, r, out, n, dt, d_local_sq, d_global_sq,
+                                        acc, ctx->grid_local, S(stream)));
   ctx->last_launches = 1;
   return CANNIKIN_OK;
 }

@@ -38,6 +38,8 @@ struct Ctrl {
 struct cannikin_ctx {
   int rank = 0, world = 1, device = 0;
   int grid_ar = 148;
+  int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2
+  bool local_tma = false;   // default variant of K2 (CANNIKIN_K2_IMPL=tma|ldg)
   int num_sms = 148;
   size_t heap_bytes = 0;
   // local allocation = [Ctrl | user heap (heap_bytes) | scratch (heap_bytes)]

@@ -1,0 +1,35 @@
+// Internal declarations shared by the kernel translation units and api.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "ctx.h"
+
+namespace cannikin {
+
+// Arguments of the emulated-rank kernels (K2, both variants).
+struct LocalArgs {
+  const char* in[kMaxEmu];
+  float r[kMaxEmu];
+  char* out;
+  size_t nvec;       // full 16-byte vectors
+  size_t n;          // elements
+  double* partials;  // [grid][n+1]
+  unsigned* ticket;
+  double* local_sq;  // [n]
+  double* global_sq;
+  int accumulate;
+};
+
+cudaError_t launch_wsum_local(cannikin_ctx* ctx, const void* const* in, int nr, const double* r,
+                              void* out, size_t n, cannikin_dtype dt, double* d_local_sq,
+                              double* d_global_sq, bool accumulate, int grid_override,
+                              cudaStream_t st);
+cudaError_t launch_wsum_local_tma(cannikin_ctx* ctx, const void* const* in, int nr,
+                                  const double* r, void* out, size_t n, cannikin_dtype dt,
+                                  double* d_local_sq, double* d_global_sq, bool accumulate,
+                                  cudaStream_t st);
+cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
+                           cudaStream_t st);
+
+}  // namespace cannikin

@@ -23,6 +23,7 @@
 #include "common.h"
 #include "ctx.h"
 #include "device_utils.cuh"
+#include "kernels.h"
 
 namespace cannikin {
 

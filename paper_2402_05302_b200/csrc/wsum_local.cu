@@ -15,21 +15,10 @@
 #include "common.h"
 #include "ctx.h"
 #include "device_utils.cuh"
+#include "kernels.h"
 
 namespace cannikin {
 
-struct LocalArgs {
-  const char* in[kMaxEmu];
-  float r[kMaxEmu];
-  char* out;
-  size_t nvec;     // full 16-byte vectors
-  size_t n;        // elements
-  double* partials;  // [grid][n+1]
-  unsigned* ticket;
-  double* local_sq;  // [n]
-  double* global_sq;
-  int accumulate;
-};
 
 template <typename T, int NR>
 __device__ __forceinline__ void wsum_vec(const uint4 (&x)[NR], const float (&r)[NR], char* dst,

@@ -52,7 +52,8 @@ def weighted_allreduce(ctx: Context, bucket: torch.Tensor, r_i: float, stream=No
 
 
 def weighted_sum_local(ctx: Context, grads, r, out: torch.Tensor, local_sq: torch.Tensor,
-                       global_sq: torch.Tensor, accumulate: bool = False, stream=None):
+                       global_sq: torch.Tensor, accumulate: bool = False, stream=None,
+                       variant=None):
     """Emulated ranks on one GPU: out <- sum_j r_j grads[j]; local_sq[j] <- |grads[j]|^2;
     global_sq <- |out|^2 (float64 device tensors)."""
     dt = dtype_code(out.dtype)
@@ -60,7 +61,8 @@ def weighted_sum_local(ctx: Context, grads, r, out: torch.Tensor, local_sq: torc
         assert g.is_cuda and g.is_contiguous() and g.dtype == out.dtype and g.numel() == out.numel()
     assert local_sq.dtype == torch.float64 and global_sq.dtype == torch.float64
     ctx.weighted_sum_local([g.data_ptr() for g in grads], list(r), out.data_ptr(), out.numel(), dt,
-                           local_sq.data_ptr(), global_sq.data_ptr(), accumulate, _cur(stream))
+                           local_sq.data_ptr(), global_sq.data_ptr(), accumulate, _cur(stream),
+                           variant)
 
 
 def ddp_allreduce_mean(ctx: Context, bucket: torch.Tensor, stream=None):

@@ -43,7 +43,7 @@ def from_dev(t, dtype):
     return t.cpu().numpy()
 
 
-def run_local(ctx, gs, r, dtype, out=None, accumulate=False, local=None, glob=None):
+def run_local(ctx, gs, r, dtype, out=None, accumulate=False, local=None, glob=None, variant=None):
     ins = [to_dev(g, dtype) for g in gs]
     N = ins[0].numel()
     if out is None:
@@ -51,7 +51,7 @@ def run_local(ctx, gs, r, dtype, out=None, accumulate=False, local=None, glob=No
     if local is None:
         local = torch.zeros(len(gs), dtype=torch.float64, device="cuda")
         glob = torch.zeros(1, dtype=torch.float64, device="cuda")
-    ta.weighted_sum_local(ctx, ins, r, out, local, glob, accumulate=accumulate)
+    ta.weighted_sum_local(ctx, ins, r, out, local, glob, accumulate=accumulate, variant=variant)
     torch.cuda.synchronize()
     return out, local, glob, ins
 
@@ -72,15 +72,28 @@ def check(gs, r, dtype, out, local, glob):
     return g_ref, ls_ref, gs_ref
 
 
+@pytest.mark.parametrize("variant", ["ldg", "tma"])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("nr", [1, 2, 3, 5, 8, 16])
 @pytest.mark.parametrize("N", [1, 7, 4099, (1 << 20) + 3])
-def test_parity_sizes_ranks(ctx, dtype, nr, N):
+def test_parity_sizes_ranks(ctx, dtype, nr, N, variant):
     b = [int(x) for x in np.random.default_rng(nr * 7 + N).integers(1, 200, size=nr)]
     gs = synth.gns_gradients(nr, N, b, seed=nr + N, dtype=dtype)
     r = agg.ratios(b)
-    out, local, glob, _ = run_local(ctx, gs, r, dtype)
+    out, local, glob, _ = run_local(ctx, gs, r, dtype, variant=variant)
     check(gs, r, dtype, out, local, glob)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_variants_identical_output_bits(ctx, dtype):
+    b = [7, 1, 30, 12, 5]
+    gs = synth.gns_gradients(5, 3_000_017, b, seed=12, dtype=dtype)
+    r = agg.ratios(b)
+    o1, l1, g1, _ = run_local(ctx, gs, r, dtype, variant="ldg")
+    o2, l2, g2, _ = run_local(ctx, gs, r, dtype, variant="tma")
+    v = (lambda t: t.view(torch.int16)) if dtype == "bf16" else (lambda t: t)
+    assert torch.equal(v(o1), v(o2))
+    assert torch.allclose(l1, l2, rtol=1e-12) and torch.allclose(g1, g2, rtol=1e-12)
 
 
 def test_config1_end_to_end_gns(ctx):
@@ -131,18 +144,20 @@ def test_empty_bucket(ctx):
     assert not local.any() and not glob.any()
 
 
+@pytest.mark.parametrize("variant", ["ldg", "tma"])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_deterministic_bitwise(ctx, dtype):
+def test_deterministic_bitwise(ctx, dtype, variant):
     gs = synth.gns_gradients(5, (1 << 20) + 11, [3, 9, 27, 81, 1], seed=9, dtype=dtype)
     r = agg.ratios([3, 9, 27, 81, 1])
-    o1, l1, g1, _ = run_local(ctx, gs, r, dtype)
-    o2, l2, g2, _ = run_local(ctx, gs, r, dtype)
+    o1, l1, g1, _ = run_local(ctx, gs, r, dtype, variant=variant)
+    o2, l2, g2, _ = run_local(ctx, gs, r, dtype, variant=variant)
     assert torch.equal(o1.view(torch.int16) if dtype == "bf16" else o1,
                        o2.view(torch.int16) if dtype == "bf16" else o2)
     assert torch.equal(l1, l2) and torch.equal(g1, g2)
 
 
-def test_in_place_and_accumulate(ctx):
+@pytest.mark.parametrize("variant", ["ldg", "tma"])
+def test_in_place_and_accumulate(ctx, variant):
     """out may alias an input; ACCUMULATE sums stats over buckets (multi-bucket gradient)."""
     N = 3 * 65536 + 8
     b = [10, 20, 30]
@@ -154,7 +169,7 @@ def test_in_place_and_accumulate(ctx):
     cuts = [0, 65536, 2 * 65536 + 4, N]
     for a, c in zip(cuts[:-1], cuts[1:]):
         ta.weighted_sum_local(ctx, [x[a:c] for x in ins], r, ins[0][a:c], local, glob,
-                              accumulate=True)
+                              accumulate=True, variant=variant)
     torch.cuda.synchronize()
     check(gs, r, "f32", ins[0], local, glob)
 
@@ -188,8 +203,9 @@ def test_errors(ctx):
     assert e.value.name == "UNSUPPORTED"
 
 
+@pytest.mark.parametrize("variant", ["ldg", "tma"])
 @pytest.mark.parametrize("nr", [8])
-def test_full_size_c4_sampled(ctx, nr):
+def test_full_size_c4_sampled(ctx, nr, variant):
     """configs[3] at full size in the bench launch configuration: 110M bf16, 8 emulated ranks.
     Sampled elements vs the oracle one by one; the norms vs the oracle over the whole vectors."""
     N = 110_000_000
@@ -199,7 +215,7 @@ def test_full_size_c4_sampled(ctx, nr):
     out = torch.empty(N, dtype=torch.bfloat16, device="cuda")
     local = torch.zeros(nr, dtype=torch.float64, device="cuda")
     glob = torch.zeros(1, dtype=torch.float64, device="cuda")
-    ta.weighted_sum_local(ctx, gs, r, out, local, glob)
+    ta.weighted_sum_local(ctx, gs, r, out, local, glob, variant=variant)
     torch.cuda.synchronize()
     idx = torch.from_numpy(np.random.default_rng(0).choice(N, 200_000, replace=False)).cuda()
     samp = [from_dev(g[idx], "bf16") for g in gs]
