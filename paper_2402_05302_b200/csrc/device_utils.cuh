@@ -122,6 +122,23 @@ __device__ __forceinline__ double block_strided_sum(const double* base, int coun
   return v[0];
 }
 
+// NV column sums of a row-major table base[i*row_stride + j] (i = 0..count-1, j = 0..NV-1) in ONE
+// pass over the block: thread t accumulates rows t, t+T, t+2T, ... for all columns (independent
+// loads, pipelined), then one butterfly/warp-order reduction.  Fixed order => deterministic.
+// Result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_table_sum(const double* base, int count, int row_stride,
+                                                double (&out)[NV], double* smem) {
+#pragma unroll
+  for (int j = 0; j < NV; ++j) out[j] = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    const double* row = base + (size_t)i * row_stride;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) out[j] += __ldcg(row + j);
+  }
+  block_sum<NV>(out, smem);
+}
+
 // ------------------------------------------------------------------ system-scope flags
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

@@ -195,16 +195,24 @@ __global__ void __launch_bounds__(512, 1) twoshot_kernel(const ArArgs a) {
   __threadfence();
 
   // ---- 5. fixed-order total over (rank, CTA) -> ctx accumulator
-  for (int j = 0; j <= W; ++j) {
-    double tot = 0.0;
-    for (int src = 0; src < W; ++src) {
-      const double s =
-          dev::block_strided_sum(&a.ctrl->part[src][0][j], gridDim.x, kMaxWorld + 1, red);
-      if (tid == 0) tot += s;
-    }
-    if (tid == 0) a.ctrl->stats[j] += tot;
+  // one pass: thread t sums rows (src, cta) = i, i + T, ... of the W x G partial table in
+  // ascending order for all W+1 columns, then the fixed block tree
+  double tot[W + 1];
+#pragma unroll
+  for (int j = 0; j <= W; ++j) tot[j] = 0.0;
+  const int G = gridDim.x;
+  for (int i = tid; i < W * G; i += blockDim.x) {
+    const int src = i / G, cta = i - src * G;
+    const double* row = &a.ctrl->part[src][cta][0];
+#pragma unroll
+    for (int j = 0; j <= W; ++j) tot[j] += __ldcg(row + j);
   }
-  if (tid == 0) a.ctrl->ticket_ar = 0u;
+  dev::block_sum<W + 1>(tot, red);
+  if (tid == 0) {
+#pragma unroll
+    for (int j = 0; j <= W; ++j) a.ctrl->stats[j] += tot[j];
+    a.ctrl->ticket_ar = 0u;
+  }
 }
 
 template <typename T, int W>

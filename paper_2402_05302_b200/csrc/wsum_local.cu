@@ -115,27 +115,27 @@ __global__ void __launch_bounds__(256) wsum_local_kernel(const LocalArgs a) {
   if (!s_last) return;
   __threadfence();
   // last CTA: fixed-order tree over the per-CTA partials (K5)
-  for (int j = 0; j <= NR; ++j) {
-    const double s = dev::block_strided_sum(a.partials + j, gridDim.x, NR + 1, red);
-    if (threadIdx.x == 0) {
+  double tot[NR + 1];
+  dev::block_table_sum<NR + 1>(a.partials, gridDim.x, NR + 1, tot, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j <= NR; ++j) {
       double* dst = (j < NR) ? (a.local_sq + j) : a.global_sq;
-      *dst = a.accumulate ? (*dst + s) : s;
+      *dst = a.accumulate ? (*dst + tot[j]) : tot[j];
     }
+    *a.ticket = 0u;
   }
-  if (threadIdx.x == 0) *a.ticket = 0u;
 }
 
 // ------------------------------------------------------------------------------ host launcher
-template <typename T, int NR>
-static cudaError_t launch_t(const LocalArgs& a, int grid, cudaStream_t st) {
-  constexpr int U = NR <= 2 ? 4 : (NR <= 4 ? 2 : 1);
-  wsum_local_kernel<T, NR, U><<<grid, 256, 0, st>>>(a);
-  return cudaGetLastError();
+// Loads in flight per thread = NR * U; the default keeps NR * U ~ 4-8 (U_alt = 2 U for sweeps).
+template <int NR>
+constexpr int u_default() {
+  return NR <= 2 ? 4 : (NR <= 4 ? 2 : 1);
 }
 
-template <typename T, int NR>
+template <typename T, int NR, int U>
 static int occupancy_grid(int num_sms) {
-  constexpr int U = NR <= 2 ? 4 : (NR <= 4 ? 2 : 1);
   static int cached = 0;
   if (!cached) {
     int per_sm = 0;
@@ -149,31 +149,25 @@ static int occupancy_grid(int num_sms) {
   return g > kMaxLocalBlocks ? kMaxLocalBlocks : g;
 }
 
-template <typename T>
-static cudaError_t dispatch(int nr, const LocalArgs& a, size_t nvec, int num_sms, int grid_override,
-                            cudaStream_t st) {
-  int grid = 0;
-  switch (nr) {
-#define CANNIKIN_CASE(K)                                                         \
-  case K:                                                                        \
-    grid = grid_override > 0 ? grid_override : occupancy_grid<T, K>(num_sms);    \
-    break;
-    CANNIKIN_CASE(1) CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5)
-    CANNIKIN_CASE(6) CANNIKIN_CASE(7) CANNIKIN_CASE(8) CANNIKIN_CASE(9) CANNIKIN_CASE(10)
-    CANNIKIN_CASE(11) CANNIKIN_CASE(12) CANNIKIN_CASE(13) CANNIKIN_CASE(14) CANNIKIN_CASE(15)
-    CANNIKIN_CASE(16)
-#undef CANNIKIN_CASE
-    default:
-      return cudaErrorInvalidValue;
-  }
+template <typename T, int NR, int U>
+static cudaError_t launch_u(const LocalArgs& a, int num_sms, int grid_override, cudaStream_t st) {
+  int grid = grid_override > 0 ? grid_override : occupancy_grid<T, NR, U>(num_sms);
   // do not launch CTAs that would own no vector (keeps tiny buckets cheap)
-  const size_t need = (nvec + 255) / 256;
+  const size_t need = (a.nvec + 255) / 256;
   if ((size_t)grid > need) grid = need < 1 ? 1 : (int)need;
   if (grid > kMaxLocalBlocks) grid = kMaxLocalBlocks;
+  wsum_local_kernel<T, NR, U><<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t dispatch(int nr, const LocalArgs& a, int num_sms, int grid_override, bool alt_u,
+                            cudaStream_t st) {
   switch (nr) {
-#define CANNIKIN_CASE(K) \
-  case K:                \
-    return launch_t<T, K>(a, grid, st);
+#define CANNIKIN_CASE(K)                                                                   \
+  case K:                                                                                  \
+    return alt_u ? launch_u<T, K, 2 * u_default<K>()>(a, num_sms, grid_override, st)       \
+                 : launch_u<T, K, u_default<K>()>(a, num_sms, grid_override, st);
     CANNIKIN_CASE(1) CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5)
     CANNIKIN_CASE(6) CANNIKIN_CASE(7) CANNIKIN_CASE(8) CANNIKIN_CASE(9) CANNIKIN_CASE(10)
     CANNIKIN_CASE(11) CANNIKIN_CASE(12) CANNIKIN_CASE(13) CANNIKIN_CASE(14) CANNIKIN_CASE(15)
@@ -204,8 +198,9 @@ cudaError_t launch_wsum_local(cannikin_ctx* ctx, const void* const* in, int nr, 
   a.global_sq = d_global_sq;
   a.accumulate = accumulate ? 1 : 0;
   // partial rows are (nr+1) doubles wide: reinterpret local_part as a flat array
-  if (dt == CANNIKIN_F32) return dispatch<float>(nr, a, a.nvec, ctx->num_sms, grid_override, st);
-  return dispatch<__nv_bfloat16>(nr, a, a.nvec, ctx->num_sms, grid_override, st);
+  if (dt == CANNIKIN_F32)
+    return dispatch<float>(nr, a, ctx->num_sms, grid_override, ctx->local_alt_u, st);
+  return dispatch<__nv_bfloat16>(nr, a, ctx->num_sms, grid_override, ctx->local_alt_u, st);
 }
 
 }  // namespace cannikin

@@ -191,14 +191,16 @@ __global__ void __launch_bounds__(tma::kThreads, 1)
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int j = 0; j <= NR; ++j) {
-    const double sum = dev::block_strided_sum(a.partials + j, gridDim.x, NR + 1, red);
-    if (threadIdx.x == 0) {
+  double tot[NR + 1];
+  dev::block_table_sum<NR + 1>(a.partials, gridDim.x, NR + 1, tot, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j <= NR; ++j) {
       double* dst = (j < NR) ? (a.local_sq + j) : a.global_sq;
-      *dst = a.accumulate ? (*dst + sum) : sum;
+      *dst = a.accumulate ? (*dst + tot[j]) : tot[j];
     }
+    *a.ticket = 0u;
   }
-  if (threadIdx.x == 0) *a.ticket = 0u;
 }
 
 // ------------------------------------------------------------------------------ host launcher
