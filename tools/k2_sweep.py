@@ -21,7 +21,8 @@ from paper_2402_05302_b200 import torch_api as ta  # noqa: E402
 SHAPES = [("c4", 8, 110_000_000, "bf16"), ("c5", 8, 354_823_168, "f32"), ("c3", 8, 25_557_032, "f32"),
           ("c2", 2, 11_689_512, "f32"), ("c1-big", 3, 1 << 26, "f32"), ("c4x3", 3, 110_000_000, "bf16"),
           ("c4f32", 8, 110_000_000, "f32"), ("c5bf16", 8, 354_823_168, "bf16"),
-          ("c4x2", 8, 220_000_000, "bf16")]
+          ("c4x2", 8, 220_000_000, "bf16"), ("c4q", 8, 27_500_000, "bf16"),
+          ("c4h", 8, 55_000_000, "bf16")]
 
 
 def main():
@@ -30,6 +31,7 @@ def main():
     ap.add_argument("--shapes", default="c4,c5,c3,c2,c1-big,c4x3")
     ap.add_argument("--grids", default="0,148,296,444,592,740,888")
     ap.add_argument("--altu-grids", default="0")
+    ap.add_argument("--tma", type=int, default=1)
     args = ap.parse_args()
     torch.cuda.set_device(0)
     want = args.shapes.split(",")
@@ -42,12 +44,14 @@ def main():
         out = torch.empty_like(gs[0])
         st = torch.zeros(nr + 1, dtype=torch.float64, device="cuda")
         nbytes = (nr + 1) * N * (4 if dt == "f32" else 2)
-        variants = [("tma", None, 0)] + [("ldg", int(g), 0) for g in args.grids.split(",")]
-        variants += [("ldg", int(g), 1) for g in args.altu_grids.split(",") if g]
-        for var, grid, altu in variants:
+        variants = [("tma", None, 0, 1)] if args.tma else []
+        variants += [("ldg", int(g), 0, dyn) for g in args.grids.split(",") for dyn in (1, 0)]
+        variants += [("ldg", int(g), 1, 1) for g in args.altu_grids.split(",") if g]
+        for var, grid, altu, dyn in variants:
             if grid is not None:
                 os.environ["CANNIKIN_LOCAL_GRID"] = str(grid)
             os.environ["CANNIKIN_K2_ALT_U"] = str(altu)
+            os.environ["CANNIKIN_K2_DYN"] = str(dyn)
             ctx = ck.Context(world=1, device=0)
             for _ in range(3):
                 ta.weighted_sum_local(ctx, gs, r, out, st[:nr], st[nr:], variant=var)
@@ -67,7 +71,7 @@ def main():
                 times += [a.elapsed_time(c) for a, c in evs]
             t = statistics.median(times)
             print(json.dumps({"shape": name, "ranks": nr, "N": N, "dtype": dt, "variant": var,
-                              "grid": grid, "alt_u": altu, "ms": round(t, 4),
+                              "grid": grid, "alt_u": altu, "dyn": dyn, "ms": round(t, 4),
                               "GBps": round(nbytes / (t * 1e-3) / 1e9, 1)}), flush=True)
             del g
             ctx.close()
