@@ -13,7 +13,6 @@ namespace cannikin {
 constexpr int kMaxWorld = CANNIKIN_MAX_WORLD;
 constexpr int kMaxArBlocks = 256;      // grid cap of the two-shot kernel
 constexpr int kMaxLocalBlocks = 2048;  // grid cap of the emulated-rank kernel
-constexpr int kMaxLocalChunks = 4096;  // partial-table rows of the emulated-rank kernel
 constexpr int kMaxEmu = CANNIKIN_MAX_EMULATED;
 
 // Control region of one rank.  Fields marked [peer] are written by peers over NVLink; fields
@@ -28,10 +27,9 @@ struct Ctrl {
   uint64_t epoch[kMaxArBlocks];                              // [local] per-block epoch counter
   unsigned ticket_ar;                                        // [local] last-block-done ticket
   unsigned ticket_local;
-  unsigned chunk_counter;                                    // [local] K2 dynamic chunk counter
   int error_code;                                            // [local] protocol error (trap reason)
   double stats[kMaxWorld + 1];                               // [local] accumulated |g_j|^2, |g|^2
-  double local_part[kMaxLocalChunks][kMaxEmu + 1];           // [local] emulated-kernel partials
+  double local_part[kMaxLocalBlocks][kMaxEmu + 1];           // [local] emulated-kernel partials
 };
 
 }  // namespace cannikin
@@ -42,7 +40,6 @@ struct cannikin_ctx {
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2
   bool local_tma = false;   // default variant of K2 (CANNIKIN_K2_IMPL=tma|ldg)
   bool local_alt_u = false; // CANNIKIN_K2_ALT_U=1: twice the loads in flight per thread
-  bool local_dyn = true;    // CANNIKIN_K2_DYN=0: static round-robin chunks
   int num_sms = 148;
   size_t heap_bytes = 0;
   // local allocation = [Ctrl | user heap (heap_bytes) | scratch (heap_bytes)]

@@ -14,11 +14,8 @@ struct LocalArgs {
   char* out;
   size_t nvec;       // full 16-byte vectors
   size_t n;          // elements
-  double* partials;  // [chunks or grid][n+1]
+  double* partials;  // [grid][n+1]
   unsigned* ticket;
-  unsigned* counter;  // dynamic chunk counter (LDG variant)
-  size_t chunk;       // vectors per chunk (LDG variant)
-  int dyn;            // 1: chunks handed out by atomic counter, 0: static round robin
   double* local_sq;  // [n]
   double* global_sq;
   int accumulate;

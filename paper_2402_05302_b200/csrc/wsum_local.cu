@@ -5,11 +5,10 @@
 //   global_sq     = sum_e acc[e]^2                      |g|^2 from the fp32 accumulator (reading Q2)
 //
 // HBM-bound: (n+1) * N * sizeof(T) algorithmic bytes, ~3 flops per element and rank.  Design:
-// grid of (SMs x occupancy) CTAs of 256 threads pulling chunks of the vector range (dynamic,
-// atomic counter); each thread streams 16-byte vectors with n*U independent 128-bit loads in
-// flight, L1 bypassed; norms are accumulated per thread in fp32 over one vector and fp64 beyond;
-// per-chunk partials are reduced by the last CTA to finish (ticket) in chunk order, so the result
-// is bitwise deterministic and independent of the grid.
+// persistent grid of (SMs x occupancy) CTAs of 256 threads, each thread streams 16-byte vectors
+// with n*U independent 128-bit loads in flight, L1 bypassed; norms are accumulated per thread in
+// fp32 over one vector and fp64 beyond; per-CTA partials are reduced by the last CTA to finish
+// (ticket) in a fixed order, so the result is bitwise deterministic for a fixed grid.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -48,17 +47,11 @@ __device__ __forceinline__ void wsum_vec(const uint4 (&x)[NR], const float (&r)[
   dev::st16(dst, V::pack(acc));
 }
 
-// Work is split into chunks of `a.chunk` vectors (a multiple of 256 U).  Inside a chunk the thread
-// -> vector mapping is fixed (thread t takes vectors t, t+256, ...), and the chunk's n+1 partial
-// sums are written to row c of the partial table, so the result does not depend on which CTA
-// processed the chunk: chunks can be handed out dynamically (atomic counter, no tail imbalance
-// between CTAs) and the statistics stay bitwise deterministic for any grid.
 template <typename T, int NR, int U>
 __global__ void __launch_bounds__(256) wsum_local_kernel(const LocalArgs a) {
   using V = dev::Vec<T>;
   constexpr int E = V::E;
   __shared__ double red[32 * (NR + 1)];
-  __shared__ unsigned s_chunk[2];
   __shared__ bool s_last;
 
   float r[NR];
@@ -68,72 +61,31 @@ __global__ void __launch_bounds__(256) wsum_local_kernel(const LocalArgs a) {
     r[j] = a.r[j];
     in[j] = a.in[j];
   }
-  const unsigned nchunks = (unsigned)((a.nvec + a.chunk - 1) / a.chunk);
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    s_chunk[0] = a.dyn ? atomicAdd(a.counter, 1u) : blockIdx.x;
-    s_chunk[1] = a.dyn ? atomicAdd(a.counter, 1u) : blockIdx.x + gridDim.x;
+  double lsq[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) lsq[j] = 0.0;
+  double gsq = 0.0;
+
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; v + (U - 1) * stride < a.nvec; v += U * stride) {
+    uint4 x[U][NR];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < NR; ++j) x[u][j] = dev::ld16(in[j] + (v + u * stride) * 16);
+#pragma unroll
+    for (int u = 0; u < U; ++u) wsum_vec<T, NR>(x[u], r, a.out + (v + u * stride) * 16, lsq, gsq);
   }
-  __syncthreads();
-  for (unsigned k = 0;; ++k) {
-    const unsigned c = s_chunk[k & 1];
-    if (c >= nchunks) break;
-    double lsq[NR];
+  for (; v < a.nvec; v += stride) {
+    uint4 x[NR];
 #pragma unroll
-    for (int j = 0; j < NR; ++j) lsq[j] = 0.0;
-    double gsq = 0.0;
-    const size_t v0 = (size_t)c * a.chunk;
-    const size_t v1 = (v0 + a.chunk < a.nvec) ? v0 + a.chunk : a.nvec;
-    size_t v = v0 + tid;
-    for (; v + (U - 1) * 256 < v1; v += U * 256) {
-      uint4 x[U][NR];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int j = 0; j < NR; ++j) x[u][j] = dev::ld16(in[j] + (v + u * 256) * 16);
-#pragma unroll
-      for (int u = 0; u < U; ++u) wsum_vec<T, NR>(x[u], r, a.out + (v + u * 256) * 16, lsq, gsq);
-    }
-    for (; v < v1; v += 256) {
-      uint4 x[NR];
-#pragma unroll
-      for (int j = 0; j < NR; ++j) x[j] = dev::ld16(in[j] + v * 16);
-      wsum_vec<T, NR>(x, r, a.out + v * 16, lsq, gsq);
-    }
-    // ragged tail (< one vector of elements) belongs to the last chunk
-    if (c == nchunks - 1) {
-      const size_t e = a.nvec * E + tid;
-      if (e < a.n) {
-        float acc = 0.0f;
-#pragma unroll
-        for (int j = 0; j < NR; ++j) {
-          const float g = V::load1(in[j] + e * sizeof(T));
-          acc = fmaf(r[j], g, acc);
-          lsq[j] += (double)(g * g);
-        }
-        gsq += (double)(acc * acc);
-        V::store1(a.out + e * sizeof(T), acc);
-      }
-    }
-    double vals[NR + 1];
-#pragma unroll
-    for (int j = 0; j < NR; ++j) vals[j] = lsq[j];
-    vals[NR] = gsq;
-    dev::block_sum<NR + 1>(vals, red);  // ends with __syncthreads: s_chunk[k&1] is free again
-    if (tid == 0) {
-#pragma unroll
-      for (int j = 0; j <= NR; ++j) a.partials[(size_t)c * (NR + 1) + j] = vals[j];
-      s_chunk[k & 1] = a.dyn ? atomicAdd(a.counter, 1u) : c + 2 * gridDim.x;
-    }
-    __syncthreads();
+    for (int j = 0; j < NR; ++j) x[j] = dev::ld16(in[j] + v * 16);
+    wsum_vec<T, NR>(x, r, a.out + v * 16, lsq, gsq);
   }
-  // n == 0 or fewer vectors than one element-vector: the tail alone (no chunk)
-  if (nchunks == 0 && blockIdx.x == 0) {
-    double lsq[NR];
-#pragma unroll
-    for (int j = 0; j < NR; ++j) lsq[j] = 0.0;
-    double gsq = 0.0;
-    const size_t e = tid;
+  // ragged tail (< one vector of elements) -- scalar, block 0
+  if (blockIdx.x == 0) {
+    const size_t e = a.nvec * E + threadIdx.x;
     if (e < a.n) {
       float acc = 0.0f;
 #pragma unroll
@@ -145,35 +97,33 @@ __global__ void __launch_bounds__(256) wsum_local_kernel(const LocalArgs a) {
       gsq += (double)(acc * acc);
       V::store1(a.out + e * sizeof(T), acc);
     }
-    double vals[NR + 1];
-#pragma unroll
-    for (int j = 0; j < NR; ++j) vals[j] = lsq[j];
-    vals[NR] = gsq;
-    dev::block_sum<NR + 1>(vals, red);
-    if (tid == 0) {
-#pragma unroll
-      for (int j = 0; j <= NR; ++j) a.partials[j] = vals[j];
-    }
   }
 
-  if (tid == 0) {
+  double vals[NR + 1];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) vals[j] = lsq[j];
+  vals[NR] = gsq;
+  dev::block_sum<NR + 1>(vals, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j <= NR; ++j) a.partials[(size_t)blockIdx.x * (NR + 1) + j] = vals[j];
     __threadfence();
-    s_last = (atomicAdd(a.ticket, 1u) == gridDim.x - 1);
+    const unsigned t = atomicAdd(a.ticket, 1u);
+    s_last = (t == gridDim.x - 1);
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // last CTA: fixed-order sum over the per-chunk partial rows (K5)
+  // last CTA: fixed-order tree over the per-CTA partials (K5)
   double tot[NR + 1];
-  dev::block_table_sum<NR + 1>(a.partials, nchunks > 0 ? (int)nchunks : 1, NR + 1, tot, red);
-  if (tid == 0) {
+  dev::block_table_sum<NR + 1>(a.partials, gridDim.x, NR + 1, tot, red);
+  if (threadIdx.x == 0) {
 #pragma unroll
     for (int j = 0; j <= NR; ++j) {
       double* dst = (j < NR) ? (a.local_sq + j) : a.global_sq;
       *dst = a.accumulate ? (*dst + tot[j]) : tot[j];
     }
     *a.ticket = 0u;
-    *a.counter = 0u;
   }
 }
 
@@ -200,16 +150,12 @@ static int occupancy_grid(int num_sms) {
 }
 
 template <typename T, int NR, int U>
-static cudaError_t launch_u(LocalArgs a, int num_sms, int grid_override, cudaStream_t st) {
-  // chunk = a multiple of 256 U vectors, at least 4 per thread, at most kMaxLocalChunks chunks
-  const size_t unit = 256 * (size_t)U;
-  size_t chunk = unit * 4;
-  const size_t need_chunk = (a.nvec + kMaxLocalChunks - 1) / kMaxLocalChunks;
-  if (need_chunk > chunk) chunk = (need_chunk + unit - 1) / unit * unit;
-  a.chunk = chunk;
-  const size_t nchunks = (a.nvec + chunk - 1) / chunk;
+static cudaError_t launch_u(const LocalArgs& a, int num_sms, int grid_override, cudaStream_t st) {
   int grid = grid_override > 0 ? grid_override : occupancy_grid<T, NR, U>(num_sms);
-  if ((size_t)grid > nchunks) grid = nchunks < 1 ? 1 : (int)nchunks;
+  // do not launch CTAs that would own no vector (keeps tiny buckets cheap)
+  const size_t need = (a.nvec + 255) / 256;
+  if ((size_t)grid > need) grid = need < 1 ? 1 : (int)need;
+  if (grid > kMaxLocalBlocks) grid = kMaxLocalBlocks;
   wsum_local_kernel<T, NR, U><<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
@@ -248,8 +194,6 @@ cudaError_t launch_wsum_local(cannikin_ctx* ctx, const void* const* in, int nr, 
   a.nvec = n * esz / 16;
   a.partials = &ctx->ctrl->local_part[0][0];
   a.ticket = &ctx->ctrl->ticket_local;
-  a.counter = &ctx->ctrl->chunk_counter;
-  a.dyn = ctx->local_dyn ? 1 : 0;
   a.local_sq = d_local_sq;
   a.global_sq = d_global_sq;
   a.accumulate = accumulate ? 1 : 0;
