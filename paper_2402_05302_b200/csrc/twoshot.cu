@@ -253,15 +253,21 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
   L -= L % 64;  // shard boundaries on 1 KiB
   a.shard_lo = L * (size_t)ctx->rank;
   a.shard_hi = (ctx->rank == W - 1) ? a.nvec : L * (size_t)(ctx->rank + 1);
+  // small buckets use fewer CTAs (>= ~2 vectors per thread): fewer flags to exchange and a smaller
+  // final reduction.  A function of (n, W, grid) only, so every rank picks the same grid.
+  int grid = ctx->grid_ar;
+  const size_t per_cta = 512 * 2;
+  const size_t want = (L + per_cta - 1) / per_cta;
+  if (want < (size_t)grid) grid = want < 1 ? 1 : (int)want;
   uint64_t meta = (uint64_t)off * 0x9E3779B97F4A7C15ull;
   meta ^= (uint64_t)n * 0xC2B2AE3D27D4EB4Full;
-  meta ^= ((uint64_t)ctx->grid_ar << 8) ^ (uint64_t)dt;
+  meta ^= ((uint64_t)grid << 8) ^ (uint64_t)dt;
   a.meta = meta;
   a.timeout_ns = ctx->spin_timeout_ns;
   a.r_me = r_i;
   a.rank = ctx->rank;
-  if (dt == CANNIKIN_F32) return dispatch_w<float>(W, a, ctx->grid_ar, st);
-  return dispatch_w<__nv_bfloat16>(W, a, ctx->grid_ar, st);
+  if (dt == CANNIKIN_F32) return dispatch_w<float>(W, a, grid, st);
+  return dispatch_w<__nv_bfloat16>(W, a, grid, st);
 }
 
 }  // namespace cannikin
