@@ -44,7 +44,8 @@ CONFIGS = {
 # Heterogeneous node models (Eq. 3) with per-sample speed in the ratio of Table 1's
 # FP16 TFLOPS (A100 77.97, V100 31.4, P100 21.2) -- the C3/C4 emulated mix.
 TFLOPS = {"A100": 77.97, "V100": 31.4, "P100": 21.2}
-MIX = ["A100", "A100", "A100", "V100", "V100", "V100", "P100", "P100"]
+# cyclic so that every prefix is heterogeneous; the 8-rank mix is C3's 3 A100 / 3 V100 / 2 P100
+MIX = ["A100", "V100", "P100", "A100", "V100", "P100", "A100", "V100"]
 COMM = (0.20, 0.010, 0.004)  # gamma, T_o, T_u
 
 
@@ -54,6 +55,112 @@ def node_models(n):
         f = TFLOPS["A100"] / TFLOPS[MIX[i % len(MIX)]]
         out.append((0.0004 * f, 0.004, 0.0008 * f, 0.002))  # q, s, k, m  (seconds)
     return out
+
+
+def hetero_models(n):
+    """Per-node (q, s, k, m) in seconds for the step-time comparison: an A100-class node spends
+    0.04 ms/sample forward and 0.08 ms/sample backward (+0.3 / 0.2 ms fixed); slower nodes scale
+    the per-sample terms by Table 1's TFLOPS ratio."""
+    out = []
+    for i in range(n):
+        f = TFLOPS["A100"] / TFLOPS[MIX[i % len(MIX)]]
+        out.append((0.04e-3 * f, 0.3e-3, 0.08e-3 * f, 0.2e-3))
+    return out
+
+
+def hetero_step_compare(ctx, bucket, N, s, rank, world, B, steps, dist, ta, ck, torch):
+    """Step time of Cannikin (opt_split b_i + the fused weighted all-reduce, K3) against
+    equal-split DDP (b_i = B/n + NCCL average) on ranks made heterogeneous by emulated compute
+    (K7, the Eq. 3 model of each rank).  Backprop is split into NB chunks; bucket j is reduced on a
+    comm stream as soon as chunk j is done (the bucketed overlap of §3.2.3), so
+    gamma = 1/NB.  T_o and T_u are measured from the comm kernels themselves."""
+    NB = 9
+    be = (N // NB) - (N // NB) % 8
+    cuts = [i * be for i in range(NB)] + [N]
+    cs = torch.cuda.current_stream()
+    ms = torch.cuda.Stream()
+    models = hetero_models(world)
+
+    def time_comm(op, reps=10):
+        for _ in range(2):
+            for j in range(NB):
+                op(j)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(ms):
+            e0.record(ms)
+            for _ in range(reps):
+                for j in range(NB):
+                    op(j)
+            e1.record(ms)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / reps / NB * 1e-3], device="cuda",
+                         dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    stats = torch.zeros(world + 1, dtype=torch.float64, device="cuda")
+
+    def ours_op(j, r):
+        ta.weighted_allreduce(ctx, bucket[cuts[j]:cuts[j + 1]], r, stream=ms)
+
+    def ddp_op(j):
+        ta.ddp_allreduce_mean(ctx, bucket[cuts[j]:cuts[j + 1]], stream=ms)
+
+    t_ours = time_comm(lambda j: ours_op(j, 1.0 / world))
+    ctx.gns_stats(ms)
+    t_nccl = time_comm(ddp_op)
+    comm_ours = (1.0 / NB, (NB - 1) * t_ours, t_ours)
+    comm_nccl = (1.0 / NB, (NB - 1) * t_nccl, t_nccl)
+    sp = ck.opt_split(models, comm_ours, B)
+    b_c = sp["b"]
+    b_d = [B // world + (1 if i < B % world else 0) for i in range(world)]
+    pred_ddp = max(ck.node_time(models[i], comm_nccl, b_d[i]) for i in range(world))
+    evs = [torch.cuda.Event() for _ in range(NB)]
+
+    def step(b_i, op):
+        q, s0, k, m = models[rank]
+        ck.emulate_compute(q * b_i + s0, cs)
+        for j in range(NB):
+            ck.emulate_compute((k * b_i + m) / NB, cs)
+            evs[j].record(cs)
+            ms.wait_event(evs[j])
+            op(j)
+        cs.wait_stream(ms)
+
+    def run(b_vec, op, with_stats):
+        for _ in range(3):
+            step(b_vec[rank], op)
+            if with_stats:
+                ctx.gns_stats_async(stats.data_ptr(), cs)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cs)
+        for _ in range(steps):
+            step(b_vec[rank], op)
+            if with_stats:
+                ctx.gns_stats_async(stats.data_ptr(), cs)
+        e1.record(cs)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / steps], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    Bsum = sum(b_c)
+    ms_c = run(b_c, lambda j: ours_op(j, b_c[rank] / Bsum), True)
+    ms_d = run(b_d, ddp_op, False)
+    return {"cannikin_ms": round(ms_c, 4), "ddp_ms": round(ms_d, 4),
+            "saving": round(1.0 - ms_c / ms_d, 4),
+            "predicted_cannikin_ms": round(sp["T_int"] * 1e3, 4),
+            "predicted_ddp_ms": round(pred_ddp * 1e3, 4),
+            "prediction_error": round(abs(sp["T_int"] * 1e3 - ms_c) / ms_c, 4),
+            "b_cannikin": b_c, "b_ddp": b_d, "buckets": NB,
+            "bucket_comm_ms": {"cannikin_k3": round(t_ours * 1e3, 4), "nccl": round(t_nccl * 1e3, 4)},
+            "mix": [MIX[i % len(MIX)] for i in range(world)],
+            "note": "compute emulated per rank from the Eq. 3 model (K7); comm kernels real; "
+                    "gamma = 1/buckets; max over ranks"}
 
 
 def esize(dtype):
@@ -220,6 +327,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of a CUDA graph")
+    ap.add_argument("--no-hetero", action="store_true", help="skip the step-time-vs-DDP comparison")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -417,6 +525,11 @@ def main():
         ddp = {"ms_per_allreduce": round(float(dm.item()), 4),
                "note": "ncclAllReduce(avg) of the same bucket, equal-split DDP semantics (Eq. 2)"}
 
+    hetero = None
+    if world > 1 and not args.no_hetero:
+        hetero = hetero_step_compare(ctx, bucket, N, s, rank, world, max(B, world), args.steps,
+                                     dist, ta, ck, torch)
+
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -485,6 +598,7 @@ def main():
                        "cuda_graph": graphs is not None,
                        "host_overlap": "host half of step t overlaps device half of step t+1"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "ddp_baseline": ddp,
+            "step_vs_ddp": hetero,
             "gpu_launches": launches_per_step() * args.steps,
             "clocks": clk.summary(),
         }

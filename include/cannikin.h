@@ -152,6 +152,11 @@ cannikin_status cannikin_weighted_sum_local(cannikin_ctx* ctx, const void* const
 cannikin_status cannikin_ddp_allreduce_mean(cannikin_ctx* ctx, void* bucket, size_t n,
                                             cannikin_dtype dt, void* stream);
 
+/* Bench utility (not part of the method): enqueue a synthetic "compute" kernel that occupies one
+ * warp for `seconds` (0..60) of device time, to emulate a node's compute time t_i(b) (Eq. 3,
+ * P:158-165) on homogeneous GPUs, as Cluster C's dummy load does.  Errors: DOMAIN, CUDA. */
+cannikin_status cannikin_emulate_compute(double seconds, void* stream);
+
 /* Number of CUDA kernels the last hot-path call on this ctx enqueued (for launch accounting). */
 int cannikin_last_launch_count(cannikin_ctx* ctx);
 

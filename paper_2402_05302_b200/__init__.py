@@ -89,6 +89,7 @@ SIGNATURES = {
     "cannikin_weighted_sum_local": (_I, [_P, ctypes.POINTER(_P), _I, _DP, _P, _Z, _I, _P, _P, _U, _P]),
     "cannikin_ddp_allreduce_mean": (_I, [_P, _P, _Z, _I, _P]),
     "cannikin_last_launch_count": (_I, [_P]),
+    "cannikin_emulate_compute": (_I, [_D, _P]),
     "cannikin_gns_estimate": (_I, [_DP, _D, _LP, _I, ctypes.POINTER(_GnsResult)]),
     "cannikin_node_time": (_D, [ctypes.POINTER(_NodeModel), ctypes.POINTER(_CommModel), _D]),
     "cannikin_opt_split": (_I, [ctypes.POINTER(_NodeModel), _I, ctypes.POINTER(_CommModel), _L, _LP,
@@ -198,6 +199,11 @@ class Context:
 
     def last_launch_count(self) -> int:
         return int(lib().cannikin_last_launch_count(self._h))
+
+
+def emulate_compute(seconds: float, stream=None):
+    """Bench utility: synthetic compute of `seconds` device time on `stream` (K7)."""
+    _check(lib().cannikin_emulate_compute(float(seconds), _stream(stream)))
 
 
 def get_unique_id() -> bytes:

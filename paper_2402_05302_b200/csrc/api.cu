@@ -320,3 +320,10 @@ extern "C" cannikin_status cannikin_ddp_allreduce_mean(cannikin_ctx* ctx, void* 
 }
 
 extern "C" int cannikin_last_launch_count(cannikin_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+extern "C" cannikin_status cannikin_emulate_compute(double seconds, void* stream) {
+  if (!(seconds >= 0.0) || seconds > 60.0)
+    return fail(CANNIKIN_ERR_DOMAIN, "emulate_compute: %g s outside [0, 60]", seconds);
+  CK_CUDA(cannikin::launch_emulate(seconds, S(stream)));
+  return CANNIKIN_OK;
+}
