@@ -37,6 +37,8 @@ struct Ctrl {
 struct cannikin_ctx {
   int rank = 0, world = 1, device = 0;
   int grid_ar = 148;
+  int ar_threads = 512;     // CTA size of the two-shot kernel (CANNIKIN_AR_THREADS=256|512)
+  bool ar_alt_u = false;    // CANNIKIN_AR_ALT_U=1: twice the vectors in flight per thread
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2
   bool local_tma = false;   // default variant of K2 (CANNIKIN_K2_IMPL=tma|ldg)
   bool local_alt_u = false; // CANNIKIN_K2_ALT_U=1: twice the loads in flight per thread

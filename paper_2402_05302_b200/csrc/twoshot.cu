@@ -86,8 +86,8 @@ __device__ __forceinline__ void reduce_vec(const uint4 (&x)[W], const float (&r)
   for (int j = 0; j < W; ++j) dev::st16(dst[j] + off, y);
 }
 
-template <typename T, int W, int U>
-__global__ void __launch_bounds__(512, 1) twoshot_kernel(const ArArgs a) {
+template <typename T, int W, int U, int NT>
+__global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
   using V = dev::Vec<T>;
   constexpr int E = V::E;
   __shared__ double red[32 * (W + 1)];
@@ -215,23 +215,35 @@ __global__ void __launch_bounds__(512, 1) twoshot_kernel(const ArArgs a) {
   }
 }
 
+template <int W>
+constexpr int u_default_ar() {
+  return W <= 2 ? 4 : (W <= 4 ? 2 : 1);
+}
+
 template <typename T, int W>
-static cudaError_t launch_w(const ArArgs& a, int grid, cudaStream_t st) {
-  constexpr int U = W <= 2 ? 4 : (W <= 4 ? 2 : 1);
-  twoshot_kernel<T, W, U><<<grid, 512, 0, st>>>(a);
+static cudaError_t launch_w(const ArArgs& a, int grid, int threads, bool alt_u, cudaStream_t st) {
+  constexpr int U = u_default_ar<W>();
+  if (threads == 256) {
+    if (alt_u) twoshot_kernel<T, W, 2 * U, 256><<<grid, 256, 0, st>>>(a);
+    else twoshot_kernel<T, W, U, 256><<<grid, 256, 0, st>>>(a);
+  } else {
+    if (alt_u) twoshot_kernel<T, W, 2 * U, 512><<<grid, 512, 0, st>>>(a);
+    else twoshot_kernel<T, W, U, 512><<<grid, 512, 0, st>>>(a);
+  }
   return cudaGetLastError();
 }
 
 template <typename T>
-static cudaError_t dispatch_w(int W, const ArArgs& a, int grid, cudaStream_t st) {
+static cudaError_t dispatch_w(int W, const ArArgs& a, int grid, int threads, bool alt_u,
+                              cudaStream_t st) {
   switch (W) {
-    case 2: return launch_w<T, 2>(a, grid, st);
-    case 3: return launch_w<T, 3>(a, grid, st);
-    case 4: return launch_w<T, 4>(a, grid, st);
-    case 5: return launch_w<T, 5>(a, grid, st);
-    case 6: return launch_w<T, 6>(a, grid, st);
-    case 7: return launch_w<T, 7>(a, grid, st);
-    case 8: return launch_w<T, 8>(a, grid, st);
+    case 2: return launch_w<T, 2>(a, grid, threads, alt_u, st);
+    case 3: return launch_w<T, 3>(a, grid, threads, alt_u, st);
+    case 4: return launch_w<T, 4>(a, grid, threads, alt_u, st);
+    case 5: return launch_w<T, 5>(a, grid, threads, alt_u, st);
+    case 6: return launch_w<T, 6>(a, grid, threads, alt_u, st);
+    case 7: return launch_w<T, 7>(a, grid, threads, alt_u, st);
+    case 8: return launch_w<T, 8>(a, grid, threads, alt_u, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -256,7 +268,7 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
   // small buckets use fewer CTAs (>= ~2 vectors per thread): fewer flags to exchange and a smaller
   // final reduction.  A function of (n, W, grid) only, so every rank picks the same grid.
   int grid = ctx->grid_ar;
-  const size_t per_cta = 512 * 2;
+  const size_t per_cta = (size_t)ctx->ar_threads * 2;
   const size_t want = (L + per_cta - 1) / per_cta;
   if (want < (size_t)grid) grid = want < 1 ? 1 : (int)want;
   uint64_t meta = (uint64_t)off * 0x9E3779B97F4A7C15ull;
@@ -266,8 +278,8 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
   a.timeout_ns = ctx->spin_timeout_ns;
   a.r_me = r_i;
   a.rank = ctx->rank;
-  if (dt == CANNIKIN_F32) return dispatch_w<float>(W, a, grid, st);
-  return dispatch_w<__nv_bfloat16>(W, a, grid, st);
+  if (dt == CANNIKIN_F32) return dispatch_w<float>(W, a, grid, ctx->ar_threads, ctx->ar_alt_u, st);
+  return dispatch_w<__nv_bfloat16>(W, a, grid, ctx->ar_threads, ctx->ar_alt_u, st);
 }
 
 }  // namespace cannikin

@@ -47,7 +47,8 @@ def timed(fn, reps):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dtype", default="f32")
-    ap.add_argument("--grids", default="148")
+    ap.add_argument("--grids", default="0")
+    ap.add_argument("--variants", default="512:0", help="threads:alt_u list")
     ap.add_argument("--sizes-mb", default="1,4,16,64,256,1024")
     ap.add_argument("--total", type=int, default=TOTAL)
     args = ap.parse_args()
@@ -60,7 +61,11 @@ def main():
     N = args.total
     b = list(range(1, world + 1))
     r = b[rank] / sum(b)
-    for grid in [int(x) for x in args.grids.split(",")]:
+    combos = [(int(g), v) for g in args.grids.split(",") for v in args.variants.split(",")]
+    for grid, var in combos:
+        thr, altu = var.split(":")
+        os.environ["CANNIKIN_AR_THREADS"] = thr
+        os.environ["CANNIKIN_AR_ALT_U"] = altu
         ctx = ta.init_distributed_context(heap_bytes=N * s, grid=grid)
         bucket = ta.bucket_tensor(ctx, N, tdt)
         bucket.copy_(synth.device_gns_gradients(world, N, b, seed=0, dtype=args.dtype,
@@ -86,7 +91,7 @@ def main():
             t_nccl = timed(nccl, reps)
             bus = lambda t: N * s / (t * 1e-3) * 2 * (world - 1) / world / 1e9  # noqa: E731
             if rank == 0:
-                print(json.dumps({"world": world, "dtype": args.dtype, "grid": grid,
+                print(json.dumps({"world": world, "dtype": args.dtype, "grid": grid, "variant": var,
                                   "bucket_MB": mb, "buckets": nb, "total_MB": round(N * s / 2**20),
                                   "ours_ms": round(t_ours, 4), "nccl_ms": round(t_nccl, 4),
                                   "ours_busbw": round(bus(t_ours), 1),
