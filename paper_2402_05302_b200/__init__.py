@@ -90,6 +90,7 @@ SIGNATURES = {
     "cannikin_ddp_allreduce_mean": (_I, [_P, _P, _Z, _I, _P]),
     "cannikin_last_launch_count": (_I, [_P]),
     "cannikin_emulate_compute": (_I, [_D, _P]),
+    "cannikin_trace": (_I, [_P, ctypes.POINTER(ctypes.c_uint64), _I, _IP]),
     "cannikin_gns_estimate": (_I, [_DP, _D, _LP, _I, ctypes.POINTER(_GnsResult)]),
     "cannikin_node_time": (_D, [ctypes.POINTER(_NodeModel), ctypes.POINTER(_CommModel), _D]),
     "cannikin_opt_split": (_I, [ctypes.POINTER(_NodeModel), _I, ctypes.POINTER(_CommModel), _L, _LP,
@@ -196,6 +197,14 @@ class Context:
 
     def ddp_allreduce_mean(self, ptr: int, n: int, dtype: int, stream=None):
         _check(lib().cannikin_ddp_allreduce_mean(self._h, ptr, n, dtype, _stream(stream)))
+
+    def trace(self, max_ctas: int = 256):
+        """Per-CTA timeline (ns) of the last two-shot kernel: list of [start, entry, data, exit,
+        end] (end only set on the last CTA to finish)."""
+        buf = (ctypes.c_uint64 * (5 * max_ctas))()
+        n = ctypes.c_int()
+        _check(lib().cannikin_trace(self._h, buf, max_ctas, ctypes.byref(n)))
+        return [list(buf[5 * i:5 * i + 5]) for i in range(n.value)]
 
     def last_launch_count(self) -> int:
         return int(lib().cannikin_last_launch_count(self._h))

@@ -330,3 +330,16 @@ extern "C" cannikin_status cannikin_emulate_compute(double seconds, void* stream
   CK_CUDA(cannikin::launch_emulate(seconds, S(stream)));
   return CANNIKIN_OK;
 }
+
+extern "C" cannikin_status cannikin_trace(cannikin_ctx* ctx, uint64_t* out, int max_ctas,
+                                          int* n_ctas) {
+  if (!ctx || !out || !n_ctas || max_ctas < 1) return fail(CANNIKIN_ERR_INVALID, "trace: bad arguments");
+  CK_CUDA(cudaSetDevice(ctx->device));
+  CK_CUDA(cudaDeviceSynchronize());
+  int g = 0;
+  CK_CUDA(cudaMemcpy(&g, &ctx->ctrl->trace_grid, sizeof g, cudaMemcpyDeviceToHost));
+  if (g > max_ctas) g = max_ctas;
+  *n_ctas = g;
+  if (g > 0) CK_CUDA(cudaMemcpy(out, ctx->ctrl->trace, sizeof(uint64_t) * 5 * g, cudaMemcpyDeviceToHost));
+  return CANNIKIN_OK;
+}

@@ -29,6 +29,8 @@ struct Ctrl {
   unsigned ticket_local;
   int error_code;                                            // [local] protocol error (trap reason)
   double stats[kMaxWorld + 1];                               // [local] accumulated |g_j|^2, |g|^2
+  uint64_t trace[kMaxArBlocks][5];                           // [local] K3 per-CTA timeline (ns)
+  int trace_grid;                                            // [local] CTAs of the last K3 call
   double local_part[kMaxLocalBlocks][kMaxEmu + 1];           // [local] emulated-kernel partials
 };
 

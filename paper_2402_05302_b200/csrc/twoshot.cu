@@ -97,7 +97,10 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
   __shared__ bool s_last;
   const int b = blockIdx.x, tid = threadIdx.x;
 
-  if (tid == 0) s_ep = a.ctrl->epoch[b] + 1;
+  if (tid == 0) {
+    s_ep = a.ctrl->epoch[b] + 1;
+    a.ctrl->trace[b][0] = dev::globaltimer_ns();
+  }
   __syncthreads();
   const uint64_t ep = s_ep;
 
@@ -115,6 +118,7 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
     }
   }
   __syncthreads();
+  if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
 
   float r[W];
   char* dst[W];
@@ -172,6 +176,7 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
   if (tid == 0) {
 #pragma unroll
     for (int j = 0; j <= W; ++j) s_part[j] = vals[j];
+    a.ctrl->trace[b][2] = dev::globaltimer_ns();
   }
   __syncthreads();  // also: every data store of this CTA has been issued
 
@@ -187,6 +192,7 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
   __syncthreads();
   if (tid == 0) {
     a.ctrl->epoch[b] = ep;
+    a.ctrl->trace[b][3] = dev::globaltimer_ns();
     __threadfence();
     s_last = (atomicAdd(&a.ctrl->ticket_ar, 1u) == gridDim.x - 1);
   }
@@ -212,6 +218,8 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
 #pragma unroll
     for (int j = 0; j <= W; ++j) a.ctrl->stats[j] += tot[j];
     a.ctrl->ticket_ar = 0u;
+    a.ctrl->trace[b][4] = dev::globaltimer_ns();
+    a.ctrl->trace_grid = G;
   }
 }
 

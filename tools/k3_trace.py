@@ -1,0 +1,61 @@
+#!/usr/bin/env python
+"""Per-phase device timeline of the two-shot kernel (K3) from its built-in %globaltimer trace.
+    torchrun --nproc-per-node N tools/k3_trace.py
+Prints, per bucket size and rank: event-timed kernel time and the CTA-median / max of
+entry-barrier wait, data phase, exit-barrier wait, final reduction (microseconds)."""
+import json
+import os
+import statistics
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2402_05302_b200 import torch_api as ta  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank))))
+    N = 64 << 20
+    ctx = ta.init_distributed_context(heap_bytes=N * 4)
+    bucket = ta.bucket_tensor(ctx, N, torch.float32)
+    bucket.normal_()
+    for mb in [0.004, 0.0625, 1, 4, 16, 64, 256]:
+        n = max(8, int(mb * 2**20) // 4)
+        for _ in range(5):
+            ta.weighted_allreduce(ctx, bucket[:n], 1.0 / world)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ta.weighted_allreduce(ctx, bucket[:n], 1.0 / world)
+        e1.record()
+        torch.cuda.synchronize()
+        tr = ctx.trace()
+        t0 = min(t[0] for t in tr)
+        ph = lambda k: [(t[k + 1] - t[k]) / 1e3 for t in tr]  # noqa: E731
+        start_spread = (max(t[0] for t in tr) - t0) / 1e3
+        last = max(tr, key=lambda t: t[4])
+        out = {"rank": rank, "bucket_MB": mb, "ctas": len(tr), "event_us": round(e0.elapsed_time(e1) * 1e3, 1),
+               "start_spread_us": round(start_spread, 2),
+               "entry_med": round(statistics.median(ph(0)), 2), "entry_max": round(max(ph(0)), 2),
+               "data_med": round(statistics.median(ph(1)), 2), "data_max": round(max(ph(1)), 2),
+               "exit_med": round(statistics.median(ph(2)), 2), "exit_max": round(max(ph(2)), 2),
+               "final_us": round((last[4] - last[3]) / 1e3, 2),
+               "span_us": round((last[4] - t0) / 1e3, 2)}
+        objs = [None] * world
+        dist.all_gather_object(objs, out)
+        if rank == 0:
+            for o in objs:
+                print(json.dumps(o), flush=True)
+        ctx.gns_stats()
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
