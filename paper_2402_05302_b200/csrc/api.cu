@@ -76,10 +76,9 @@ extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world
   ctx->device = device;
   cudaError_t ce = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (ce != cudaSuccess) { destroy_partial(ctx); CK_CUDA(ce); }
-  if (const char* t = std::getenv("CANNIKIN_AR_THREADS")) ctx->ar_threads = std::atoi(t) == 256 ? 256 : 512;
-  if (const char* t = std::getenv("CANNIKIN_AR_ALT_U")) ctx->ar_alt_u = std::atoi(t) != 0;
-  // default: every CTA of the two-shot kernel co-resident (it spins on peers' CTAs)
-  ctx->grid_ar = grid > 0 ? grid : ctx->num_sms * (ctx->ar_threads == 256 ? 2 : 1);
+  if (const char* t = std::getenv("CANNIKIN_AR_DYN")) ctx->ar_dyn = std::atoi(t) != 0;
+  // default: one CTA per SM, all co-resident (the two-shot kernel spins on peers' CTAs)
+  ctx->grid_ar = grid > 0 ? grid : ctx->num_sms;
   if (ctx->grid_ar > cannikin::kMaxArBlocks) ctx->grid_ar = cannikin::kMaxArBlocks;
   if (const char* t = std::getenv("CANNIKIN_K2_IMPL")) ctx->local_tma = std::strcmp(t, "tma") == 0;
   if (const char* t = std::getenv("CANNIKIN_LOCAL_GRID")) ctx->grid_local = std::atoi(t);

@@ -12,6 +12,7 @@ namespace cannikin {
 
 constexpr int kMaxWorld = CANNIKIN_MAX_WORLD;
 constexpr int kMaxArBlocks = 256;      // grid cap of the two-shot kernel
+constexpr int kMaxArChunks = 2048;     // partial-table rows per source rank (dynamic two-shot)
 constexpr int kMaxLocalBlocks = 2048;  // grid cap of the emulated-rank kernel
 constexpr int kMaxEmu = CANNIKIN_MAX_EMULATED;
 
@@ -23,10 +24,11 @@ struct Ctrl {
   uint64_t exit_[kMaxArBlocks][kMaxWorld];                   // [peer] "shard pushed" epoch
   double rv[kMaxArBlocks][kMaxWorld];                        // [peer] r_src for this bucket
   uint64_t meta[kMaxArBlocks][kMaxWorld];                    // [peer] (heap offset, n) check word
-  double part[kMaxWorld][kMaxArBlocks][kMaxWorld + 1];       // [peer] norm partials [src][blk][j]
+  double part[kMaxWorld][kMaxArChunks][kMaxWorld + 1];       // [peer] norm partials [src][row][j]
   uint64_t epoch[kMaxArBlocks];                              // [local] per-block epoch counter
   unsigned ticket_ar;                                        // [local] last-block-done ticket
   unsigned ticket_local;
+  unsigned ar_counter;                                       // [local] dynamic two-shot chunk counter
   int error_code;                                            // [local] protocol error (trap reason)
   double stats[kMaxWorld + 1];                               // [local] accumulated |g_j|^2, |g|^2
   uint64_t trace[kMaxArBlocks][5];                           // [local] K3 per-CTA timeline (ns)
@@ -39,8 +41,7 @@ struct Ctrl {
 struct cannikin_ctx {
   int rank = 0, world = 1, device = 0;
   int grid_ar = 148;
-  int ar_threads = 512;     // CTA size of the two-shot kernel (CANNIKIN_AR_THREADS=256|512)
-  bool ar_alt_u = false;    // CANNIKIN_AR_ALT_U=1: twice the vectors in flight per thread
+  bool ar_dyn = false;      // CANNIKIN_AR_DYN=1: dynamic chunk scheduling in the two-shot kernel
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2
   bool local_tma = false;   // default variant of K2 (CANNIKIN_K2_IMPL=tma|ldg)
   bool local_alt_u = false; // CANNIKIN_K2_ALT_U=1: twice the loads in flight per thread

@@ -35,9 +35,14 @@ struct ArArgs {
   size_t shard_lo, shard_hi;  // this rank's vector range
   uint64_t meta;            // identity of (offset, n, dtype, grid): must agree on every rank
   uint64_t timeout_ns;
+  size_t chunk;             // dynamic variant: vectors per chunk
+  size_t shard_len;         // vectors of shards 0..W-2 (the last shard: shard_len_last)
+  size_t shard_len_last;
   double r_me;
   int rank;
 };
+
+constexpr int kArThreads = 512;
 
 __device__ __forceinline__ void spin_until(const uint64_t* flag, uint64_t ep, Ctrl* ctrl,
                                            uint64_t timeout_ns, int code) {
@@ -223,35 +228,186 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
   }
 }
 
+
+// Dynamic variant of K3: identical protocol and arithmetic; the shard is cut into chunks that CTAs
+// claim from a per-rank counter, and every chunk's W+1 norm partials form one row of the peers'
+// partial tables (written by the W "flag" threads), so the statistics do not depend on which CTA
+// did which chunk.  The exit barrier still pairs CTA b with CTA b of every peer: when all CTAs of
+// this rank have passed it, every peer CTA -- hence every peer chunk and row -- is complete.
+template <typename T, int W, int U>
+__global__ void __launch_bounds__(kArThreads, 1) twoshot_dyn_kernel(const ArArgs a) {
+  using V = dev::Vec<T>;
+  constexpr int E = V::E;
+  constexpr int NT = kArThreads;
+  __shared__ double red[32 * (W + 1)];
+  __shared__ double s_part[W + 1];
+  __shared__ float s_r[W];
+  __shared__ uint64_t s_ep;
+  __shared__ unsigned s_chunk[2];
+  __shared__ bool s_last;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const bool has_tail = a.n > a.nvec * E;
+  auto nchunks_of = [&](int src) -> unsigned {
+    const size_t len = (src == W - 1) ? a.shard_len_last : a.shard_len;
+    unsigned c = (unsigned)((len + a.chunk - 1) / a.chunk);
+    if (src == W - 1 && c == 0 && has_tail) c = 1;
+    return c;
+  };
+  const unsigned my_chunks = nchunks_of(a.rank);
+
+  if (tid == 0) {
+    s_ep = a.ctrl->epoch[b] + 1;
+    a.ctrl->trace[b][0] = dev::globaltimer_ns();
+    s_chunk[0] = atomicAdd(&a.ctrl->ar_counter, 1u);
+    s_chunk[1] = atomicAdd(&a.ctrl->ar_counter, 1u);
+  }
+  __syncthreads();
+  const uint64_t ep = s_ep;
+  if (tid < W) {
+    Ctrl* pc = a.pctrl[tid];
+    dev::st_relaxed_sys_f64(&pc->rv[b][a.rank], a.r_me);
+    dev::st_relaxed_sys_u64(&pc->meta[b][a.rank], a.meta);
+    dev::st_release_sys(&pc->entry[b][a.rank], ep);
+    spin_until(&a.ctrl->entry[b][tid], ep, a.ctrl, a.timeout_ns, 1);
+    s_r[tid] = (float)a.ctrl->rv[b][tid];
+    if (a.ctrl->meta[b][tid] != a.meta) {
+      atomicExch(&a.ctrl->error_code, 2);
+      __trap();
+    }
+  }
+  __syncthreads();
+  if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
+
+  float r[W];
+  char* dst[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    r[j] = s_r[j];
+    dst[j] = a.bucket[j];
+  }
+  for (unsigned k = 0;; ++k) {
+    const unsigned c = s_chunk[k & 1];
+    if (c >= my_chunks) break;
+    double lsq[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) lsq[j] = 0.0;
+    double gsq = 0.0;
+    const size_t v0 = a.shard_lo + (size_t)c * a.chunk;
+    const size_t v1 = (v0 + a.chunk < a.shard_hi) ? v0 + a.chunk : a.shard_hi;
+    size_t v = v0 + tid;
+    for (; v + (U - 1) * NT < v1; v += U * NT) {
+      uint4 x[U][W];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < W; ++j) x[u][j] = dev::ld16(dst[j] + (v + u * NT) * 16);
+#pragma unroll
+      for (int u = 0; u < U; ++u) reduce_vec<T, W>(x[u], r, dst, (v + u * NT) * 16, lsq, gsq);
+    }
+    for (; v < v1; v += NT) {
+      uint4 x[W];
+#pragma unroll
+      for (int j = 0; j < W; ++j) x[j] = dev::ld16(dst[j] + v * 16);
+      reduce_vec<T, W>(x, r, dst, v * 16, lsq, gsq);
+    }
+    if (a.rank == W - 1 && c == my_chunks - 1 && has_tail) {
+      const size_t e = a.nvec * E + tid;
+      if (e < a.n) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          const float g = V::load1(dst[j] + e * sizeof(T));
+          acc = fmaf(r[j], g, acc);
+          lsq[j] += (double)(g * g);
+        }
+        gsq += (double)(acc * acc);
+#pragma unroll
+        for (int j = 0; j < W; ++j) V::store1(dst[j] + e * sizeof(T), acc);
+      }
+    }
+    double vals[W + 1];
+#pragma unroll
+    for (int j = 0; j < W; ++j) vals[j] = lsq[j];
+    vals[W] = gsq;
+    dev::block_sum<W + 1>(vals, red);
+    if (tid == 0) {
+#pragma unroll
+      for (int j = 0; j <= W; ++j) s_part[j] = vals[j];
+      s_chunk[k & 1] = atomicAdd(&a.ctrl->ar_counter, 1u);
+    }
+    __syncthreads();
+    if (tid < W) {
+      Ctrl* pc = a.pctrl[tid];
+#pragma unroll
+      for (int j = 0; j <= W; ++j) dev::st_relaxed_sys_f64(&pc->part[a.rank][c][j], s_part[j]);
+    }
+  }
+  if (tid == 0) a.ctrl->trace[b][2] = dev::globaltimer_ns();
+  __syncthreads();  // every data and partial store of this CTA has been issued
+
+  if (tid < W) {
+    __threadfence_system();
+    dev::st_release_sys(&a.pctrl[tid]->exit_[b][a.rank], ep);
+    spin_until(&a.ctrl->exit_[b][tid], ep, a.ctrl, a.timeout_ns, 3);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    a.ctrl->epoch[b] = ep;
+    a.ctrl->trace[b][3] = dev::globaltimer_ns();
+    __threadfence();
+    s_last = (atomicAdd(&a.ctrl->ticket_ar, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // fixed order: rank 0's chunk rows, then rank 1's, ...; thread t takes rows t, t+NT, ...
+  double tot[W + 1];
+#pragma unroll
+  for (int j = 0; j <= W; ++j) tot[j] = 0.0;
+  unsigned base = 0;
+  for (int src = 0; src < W; ++src) {
+    const unsigned nc = nchunks_of(src);
+    for (unsigned i = tid; i < nc; i += NT) {
+      const double* row = &a.ctrl->part[src][i][0];
+#pragma unroll
+      for (int j = 0; j <= W; ++j) tot[j] += __ldcg(row + j);
+    }
+    base += nc;
+  }
+  dev::block_sum<W + 1>(tot, red);
+  if (tid == 0) {
+#pragma unroll
+    for (int j = 0; j <= W; ++j) a.ctrl->stats[j] += tot[j];
+    a.ctrl->ticket_ar = 0u;
+    a.ctrl->ar_counter = 0u;
+    a.ctrl->trace[b][4] = dev::globaltimer_ns();
+    a.ctrl->trace_grid = gridDim.x;
+  }
+}
+
 template <int W>
 constexpr int u_default_ar() {
   return W <= 2 ? 4 : (W <= 4 ? 2 : 1);
 }
 
 template <typename T, int W>
-static cudaError_t launch_w(const ArArgs& a, int grid, int threads, bool alt_u, cudaStream_t st) {
+static cudaError_t launch_w(const ArArgs& a, int grid, bool dyn, cudaStream_t st) {
   constexpr int U = u_default_ar<W>();
-  if (threads == 256) {
-    if (alt_u) twoshot_kernel<T, W, 2 * U, 256><<<grid, 256, 0, st>>>(a);
-    else twoshot_kernel<T, W, U, 256><<<grid, 256, 0, st>>>(a);
-  } else {
-    if (alt_u) twoshot_kernel<T, W, 2 * U, 512><<<grid, 512, 0, st>>>(a);
-    else twoshot_kernel<T, W, U, 512><<<grid, 512, 0, st>>>(a);
-  }
+  if (dyn) twoshot_dyn_kernel<T, W, U><<<grid, kArThreads, 0, st>>>(a);
+  else twoshot_kernel<T, W, U, kArThreads><<<grid, kArThreads, 0, st>>>(a);
   return cudaGetLastError();
 }
 
 template <typename T>
-static cudaError_t dispatch_w(int W, const ArArgs& a, int grid, int threads, bool alt_u,
-                              cudaStream_t st) {
+static cudaError_t dispatch_w(int W, const ArArgs& a, int grid, bool dyn, cudaStream_t st) {
   switch (W) {
-    case 2: return launch_w<T, 2>(a, grid, threads, alt_u, st);
-    case 3: return launch_w<T, 3>(a, grid, threads, alt_u, st);
-    case 4: return launch_w<T, 4>(a, grid, threads, alt_u, st);
-    case 5: return launch_w<T, 5>(a, grid, threads, alt_u, st);
-    case 6: return launch_w<T, 6>(a, grid, threads, alt_u, st);
-    case 7: return launch_w<T, 7>(a, grid, threads, alt_u, st);
-    case 8: return launch_w<T, 8>(a, grid, threads, alt_u, st);
+    case 2: return launch_w<T, 2>(a, grid, dyn, st);
+    case 3: return launch_w<T, 3>(a, grid, dyn, st);
+    case 4: return launch_w<T, 4>(a, grid, dyn, st);
+    case 5: return launch_w<T, 5>(a, grid, dyn, st);
+    case 6: return launch_w<T, 6>(a, grid, dyn, st);
+    case 7: return launch_w<T, 7>(a, grid, dyn, st);
+    case 8: return launch_w<T, 8>(a, grid, dyn, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -276,18 +432,28 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
   // small buckets use fewer CTAs (>= ~2 vectors per thread): fewer flags to exchange and a smaller
   // final reduction.  A function of (n, W, grid) only, so every rank picks the same grid.
   int grid = ctx->grid_ar;
-  const size_t per_cta = (size_t)ctx->ar_threads * 2;
+  const size_t per_cta = (size_t)kArThreads * 2;
   const size_t want = (L + per_cta - 1) / per_cta;
   if (want < (size_t)grid) grid = want < 1 ? 1 : (int)want;
   uint64_t meta = (uint64_t)off * 0x9E3779B97F4A7C15ull;
   meta ^= (uint64_t)n * 0xC2B2AE3D27D4EB4Full;
   meta ^= ((uint64_t)grid << 8) ^ (uint64_t)dt;
-  a.meta = meta;
   a.timeout_ns = ctx->spin_timeout_ns;
   a.r_me = r_i;
   a.rank = ctx->rank;
-  if (dt == CANNIKIN_F32) return dispatch_w<float>(W, a, grid, ctx->ar_threads, ctx->ar_alt_u, st);
-  return dispatch_w<__nv_bfloat16>(W, a, grid, ctx->ar_threads, ctx->ar_alt_u, st);
+  // dynamic variant: chunks of the shard handed out by a per-rank atomic counter (balances the
+  // per-CTA NVLink bandwidth spread); per-chunk partial rows keep the statistics deterministic
+  const bool dyn = ctx->ar_dyn;
+  size_t chunk = (size_t)kArThreads * 4 * 4;
+  const size_t need = (L + kMaxArChunks - 2) / (kMaxArChunks - 1);
+  if (need > chunk) chunk = (need + kArThreads - 1) / kArThreads * kArThreads;
+  a.chunk = chunk;
+  a.shard_len_last = a.nvec - L * (size_t)(W - 1);
+  a.shard_len = L;
+  if (dyn) meta ^= (uint64_t)chunk * 0x94D049BB133111EBull;
+  a.meta = meta;
+  if (dt == CANNIKIN_F32) return dispatch_w<float>(W, a, grid, dyn, st);
+  return dispatch_w<__nv_bfloat16>(W, a, grid, dyn, st);
 }
 
 }  // namespace cannikin

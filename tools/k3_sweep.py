@@ -48,7 +48,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--grids", default="0")
-    ap.add_argument("--variants", default="512:0", help="threads:alt_u list")
+    ap.add_argument("--variants", default="0", help="CANNIKIN_AR_DYN values")
     ap.add_argument("--sizes-mb", default="1,4,16,64,256,1024")
     ap.add_argument("--total", type=int, default=TOTAL)
     args = ap.parse_args()
@@ -63,9 +63,7 @@ def main():
     r = b[rank] / sum(b)
     combos = [(int(g), v) for g in args.grids.split(",") for v in args.variants.split(",")]
     for grid, var in combos:
-        thr, altu = var.split(":")
-        os.environ["CANNIKIN_AR_THREADS"] = thr
-        os.environ["CANNIKIN_AR_ALT_U"] = altu
+        os.environ["CANNIKIN_AR_DYN"] = var
         ctx = ta.init_distributed_context(heap_bytes=N * s, grid=grid)
         bucket = ta.bucket_tensor(ctx, N, tdt)
         bucket.copy_(synth.device_gns_gradients(world, N, b, seed=0, dtype=args.dtype,

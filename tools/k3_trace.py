@@ -20,6 +20,7 @@ def main():
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
     dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank))))
     N = 64 << 20
+    dyn = os.environ.get("CANNIKIN_AR_DYN", "0")
     ctx = ta.init_distributed_context(heap_bytes=N * 4)
     bucket = ta.bucket_tensor(ctx, N, torch.float32)
     bucket.normal_()
@@ -39,7 +40,7 @@ def main():
         ph = lambda k: [(t[k + 1] - t[k]) / 1e3 for t in tr]  # noqa: E731
         start_spread = (max(t[0] for t in tr) - t0) / 1e3
         last = max(tr, key=lambda t: t[4])
-        out = {"rank": rank, "bucket_MB": mb, "ctas": len(tr), "event_us": round(e0.elapsed_time(e1) * 1e3, 1),
+        out = {"rank": rank, "dyn": dyn, "bucket_MB": mb, "ctas": len(tr), "event_us": round(e0.elapsed_time(e1) * 1e3, 1),
                "start_spread_us": round(start_spread, 2),
                "entry_med": round(statistics.median(ph(0)), 2), "entry_max": round(max(ph(0)), 2),
                "data_med": round(statistics.median(ph(1)), 2), "data_max": round(max(ph(1)), 2),
