@@ -444,9 +444,13 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
   // dynamic variant: chunks of the shard handed out by a per-rank atomic counter (balances the
   // per-CTA NVLink bandwidth spread); per-chunk partial rows keep the statistics deterministic
   const bool dyn = ctx->ar_dyn;
-  size_t chunk = (size_t)kArThreads * 4 * 4;
+  // ~4 chunks per CTA, between one vector per thread and 16 per thread, <= kMaxArChunks-1 chunks
+  size_t chunk = (L + (size_t)grid * 4 - 1) / ((size_t)grid * 4);
+  if (chunk > (size_t)kArThreads * 16) chunk = (size_t)kArThreads * 16;
   const size_t need = (L + kMaxArChunks - 2) / (kMaxArChunks - 1);
-  if (need > chunk) chunk = (need + kArThreads - 1) / kArThreads * kArThreads;
+  if (need > chunk) chunk = need;
+  chunk = (chunk + kArThreads - 1) / kArThreads * kArThreads;
+  if (chunk < (size_t)kArThreads) chunk = kArThreads;
   a.chunk = chunk;
   a.shard_len_last = a.nvec - L * (size_t)(W - 1);
   a.shard_len = L;
