@@ -20,10 +20,9 @@ constexpr int kMaxEmu = CANNIKIN_MAX_EMULATED;
 // marked [local] only by this rank's own kernels.  Flags carry monotonically increasing epochs
 // (never reset), so back-to-back buckets need no re-initialisation (no reset races).
 struct Ctrl {
-  uint64_t entry[kMaxArBlocks][kMaxWorld];                   // [peer] "bucket ready" epoch
   uint64_t exit_[kMaxArBlocks][kMaxWorld];                   // [peer] "shard pushed" epoch
-  double rv[kMaxArBlocks][kMaxWorld];                        // [peer] r_src for this bucket
-  uint64_t meta[kMaxArBlocks][kMaxWorld];                    // [peer] (heap offset, n) check word
+  uint64_t rv_word[kMaxArBlocks][kMaxWorld];                 // [peer] entry: (float r_src, epoch32)
+  uint64_t meta_word[kMaxArBlocks][kMaxWorld];               // [peer] entry: (bucket hash32, epoch32)
   double part[kMaxWorld][kMaxArChunks][kMaxWorld + 1];       // [peer] norm partials [src][row][j]
   uint64_t epoch[kMaxArBlocks];                              // [local] per-block epoch counter
   unsigned ticket_ar;                                        // [local] last-block-done ticket
@@ -41,7 +40,7 @@ struct Ctrl {
 struct cannikin_ctx {
   int rank = 0, world = 1, device = 0;
   int grid_ar = 148;
-  bool ar_dyn = false;      // CANNIKIN_AR_DYN=1: dynamic chunk scheduling in the two-shot kernel
+  int ar_dyn = -1;          // CANNIKIN_AR_DYN=0|1 forces static/dynamic chunks; -1 = by size
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2
   bool local_tma = false;   // default variant of K2 (CANNIKIN_K2_IMPL=tma|ldg)
   bool local_alt_u = false; // CANNIKIN_K2_ALT_U=1: twice the loads in flight per thread

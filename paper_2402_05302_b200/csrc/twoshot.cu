@@ -61,6 +61,56 @@ __device__ __forceinline__ void spin_until(const uint64_t* flag, uint64_t ep, Ct
   }
 }
 
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Spin until the low 32 bits of *word (an epoch tag) reach e32 (wrap-safe); returns the word.
+__device__ __forceinline__ uint64_t spin_word(const uint64_t* word, uint32_t e32, Ctrl* ctrl,
+                                              uint64_t timeout_ns, int code) {
+  uint64_t t0 = 0;
+  unsigned it = 0;
+  uint64_t w;
+  while ((int32_t)((uint32_t)(w = ld_relaxed_sys(word)) - e32) < 0) {
+    if ((++it & 1023u) == 0u) {
+      const uint64_t now = dev::globaltimer_ns();
+      if (t0 == 0) {
+        t0 = now;
+      } else if (now - t0 > timeout_ns) {
+        atomicExch(&ctrl->error_code, code);
+        __trap();
+      }
+    }
+  }
+  return w;
+}
+
+// Entry barrier, executed by thread `tid` < W of CTA b for peer tid.  Each 64-bit word carries its
+// own 32-bit epoch tag (r_rank or the bucket-identity hash in the high half), so the two words
+// need no mutual ordering and no fence: the bucket contents were written by earlier kernels and
+// are complete (in the owner's L2, the point of coherence for NVLink loads) at their kernel
+// boundary.  The waiter reads r_tid and checks that every rank reduces the same bucket.
+template <int W>
+__device__ __forceinline__ void entry_barrier_thread(const ArArgs& a, int b, uint64_t ep,
+                                                     float* s_r) {
+  const int tid = threadIdx.x;
+  const uint32_t e32 = (uint32_t)ep;
+  const uint32_t m32 = (uint32_t)(a.meta ^ (a.meta >> 32));
+  Ctrl* pc = a.pctrl[tid];
+  dev::st_relaxed_sys_u64(&pc->rv_word[b][a.rank],
+                          ((uint64_t)__float_as_uint((float)a.r_me) << 32) | e32);
+  dev::st_relaxed_sys_u64(&pc->meta_word[b][a.rank], ((uint64_t)m32 << 32) | e32);
+  const uint64_t wr = spin_word(&a.ctrl->rv_word[b][tid], e32, a.ctrl, a.timeout_ns, 1);
+  const uint64_t wm = spin_word(&a.ctrl->meta_word[b][tid], e32, a.ctrl, a.timeout_ns, 1);
+  s_r[tid] = __uint_as_float((uint32_t)(wr >> 32));
+  if ((uint32_t)(wm >> 32) != m32) {
+    atomicExch(&a.ctrl->error_code, 2);  // ranks disagree on bucket offset/size/dtype/grid
+    __trap();
+  }
+}
+
 template <typename T, int W>
 __device__ __forceinline__ void reduce_vec(const uint4 (&x)[W], const float (&r)[W],
                                            char* const (&dst)[W], size_t off, double (&lsq)[W],
@@ -110,18 +160,7 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
   const uint64_t ep = s_ep;
 
   // ---- 0. entry barrier (+ exchange of r_j and the bucket identity)
-  if (tid < W) {
-    Ctrl* pc = a.pctrl[tid];
-    dev::st_relaxed_sys_f64(&pc->rv[b][a.rank], a.r_me);
-    dev::st_relaxed_sys_u64(&pc->meta[b][a.rank], a.meta);
-    dev::st_release_sys(&pc->entry[b][a.rank], ep);
-    spin_until(&a.ctrl->entry[b][tid], ep, a.ctrl, a.timeout_ns, 1);
-    s_r[tid] = (float)a.ctrl->rv[b][tid];
-    if (a.ctrl->meta[b][tid] != a.meta) {
-      atomicExch(&a.ctrl->error_code, 2);  // ranks disagree on bucket offset/size/dtype/grid
-      __trap();
-    }
-  }
+  if (tid < W) entry_barrier_thread<W>(a, b, ep, s_r);
   __syncthreads();
   if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
 
@@ -263,18 +302,7 @@ __global__ void __launch_bounds__(kArThreads, 1) twoshot_dyn_kernel(const ArArgs
   }
   __syncthreads();
   const uint64_t ep = s_ep;
-  if (tid < W) {
-    Ctrl* pc = a.pctrl[tid];
-    dev::st_relaxed_sys_f64(&pc->rv[b][a.rank], a.r_me);
-    dev::st_relaxed_sys_u64(&pc->meta[b][a.rank], a.meta);
-    dev::st_release_sys(&pc->entry[b][a.rank], ep);
-    spin_until(&a.ctrl->entry[b][tid], ep, a.ctrl, a.timeout_ns, 1);
-    s_r[tid] = (float)a.ctrl->rv[b][tid];
-    if (a.ctrl->meta[b][tid] != a.meta) {
-      atomicExch(&a.ctrl->error_code, 2);
-      __trap();
-    }
-  }
+  if (tid < W) entry_barrier_thread<W>(a, b, ep, s_r);
   __syncthreads();
   if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
 
@@ -443,7 +471,8 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
   a.rank = ctx->rank;
   // dynamic variant: chunks of the shard handed out by a per-rank atomic counter (balances the
   // per-CTA NVLink bandwidth spread); per-chunk partial rows keep the statistics deterministic
-  const bool dyn = ctx->ar_dyn;
+  // auto: dynamic chunks pay off for large shards (measured crossover ~32-128 MiB per shard)
+  const bool dyn = ctx->ar_dyn < 0 ? (L * 16 >= (64ull << 20)) : (ctx->ar_dyn != 0);
   // ~4 chunks per CTA, between one vector per thread and 16 per thread, <= kMaxArChunks-1 chunks
   size_t chunk = (L + (size_t)grid * 4 - 1) / ((size_t)grid * 4);
   if (chunk > (size_t)kArThreads * 16) chunk = (size_t)kArThreads * 16;
