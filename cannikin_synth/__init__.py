@@ -152,3 +152,37 @@ def device_gns_gradients(n: int, N: int, b, *, G2: float = 1.0, trS: float = 100
         out.append((G + sd * eps).to(tdt))
         del eps
     return out
+
+
+def simulate_iteration(nodes, comm, b, rng: np.random.Generator, cv: float = 0.0,
+                       gamma_sd=None):
+    """Noisy timing telemetry of one iteration of a cluster with TRUE models (q, s, k, m) and comm
+    model (gamma, T_o, T_u), for the measured-model loop tests (inputs only, no estimator):
+      a_i, P_i   = Eq. 3 times x lognormal noise with coefficient of variation cv (mean 1)
+      gamma_i    = gamma + N(0, gamma_sd[i])    (node-specific measurement noise, fig:overlapratio)
+      T_o_i, T_u_i = T_o, T_u + the time node i waits for the slowest node to reach the first
+                   bucket ("each node reports different T_i ... because of the
+                   wait-for-synchronization time"); the slowest node waits 0.
+    Returns a list of dicts, one per node."""
+    gamma, t_o, t_u = comm
+    n = len(nodes)
+    if gamma_sd is None:
+        gamma_sd = [0.0] * n
+
+    def ln():
+        if cv <= 0.0:
+            return 1.0
+        s2 = np.log(1.0 + cv * cv)
+        return float(np.exp(rng.normal(-0.5 * s2, np.sqrt(s2))))
+
+    a = [(nodes[i][0] * b[i] + nodes[i][1]) * ln() for i in range(n)]
+    P = [(nodes[i][2] * b[i] + nodes[i][3]) * ln() for i in range(n)]
+    start = [a[i] + gamma * P[i] for i in range(n)]
+    last = max(start)
+    out = []
+    for i in range(n):
+        wait = last - start[i]
+        out.append({"a": a[i], "P": P[i],
+                    "gamma": gamma + (float(rng.normal(0.0, gamma_sd[i])) if gamma_sd[i] > 0 else 0.0),
+                    "t_o": t_o + wait, "t_u": t_u + wait})
+    return out

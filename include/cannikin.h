@@ -235,6 +235,47 @@ cannikin_status cannikin_opt_split(const cannikin_node_model* nodes, int n,
 cannikin_status cannikin_warmup_split(const double* t_sample, int n, int64_t B, double* b_real_out,
                                       int64_t* b_out);
 
+/* ------------------------------------------------------------------------------------------
+ * Measured-model loop (host): learn the Eq. 3 models and the comm model
+ * from timing observations and plan each epoch's split (§4.5; Eq. 8 P:317-324;
+ * "OptPerf as early as the third epoch" P:538).
+ * ------------------------------------------------------------------------------------------ */
+
+/* Least-squares line y = slope * x + intercept through count >= 2 points (exact for two points:
+ * "solving linear equations").  Errors: INVALID (NULL), SINGULAR (count < 2 or all x
+ * equal), DOMAIN (non-finite). */
+cannikin_status cannikin_fit_linear(const double* x, const double* y, int count, double* slope,
+                                    double* intercept);
+
+/* Eq. 12 inverse-variance weighting: sum_i (x_i / v_i) / sum_i (1 / v_i).  Nodes with
+ * v_i == 0 dominate: the result is then their plain mean.  Errors: INVALID, DOMAIN (v_i < 0). */
+cannikin_status cannikin_ivw(const double* estimate, const double* variance, int n, double* out);
+
+typedef struct cannikin_analyzer cannikin_analyzer; /* opaque; host only, not thread-safe */
+cannikin_status cannikin_analyzer_create(int n, cannikin_analyzer** out);
+cannikin_status cannikin_analyzer_destroy(cannikin_analyzer* an);
+/* Record iteration `iter` of `node` at local batch b: a = data loading + forward + update
+ * time, P = backprop time (Eq. 3), gamma = its measured first-bucket share of backprop (Eq. 4),
+ * t_o / t_u = its measured sync times of the overlapped buckets / the last bucket.
+ * Errors: INVALID (node, b < 1), DOMAIN (negative or non-finite time). */
+cannikin_status cannikin_analyzer_observe(cannikin_analyzer* an, int node, int64_t iter, int64_t b,
+                                          double a, double P, double gamma, double t_o,
+                                          double t_u);
+/* Learned models: per node least-squares (q,s,k,m) over all its observations (negative fits
+ * clamped to the model domain), gamma by Eq. 12 over the nodes' observations, T_o and T_u as
+ * the per-iteration minimum over nodes averaged over the iterations all nodes reported
+ * (fallback: min over nodes of each node's mean).  Errors: SINGULAR (a node with < 2 distinct b). */
+cannikin_status cannikin_analyzer_models(cannikin_analyzer* an, cannikin_node_model* nodes_out,
+                                         cannikin_comm_model* comm_out);
+/* Plan the next epoch for total batch B (B >= n; cap[n] optional):
+ *   phase 0 (no observations): even split, extra samples to the lowest ranks;
+ *   phase 1 (some node has seen one batch size only): Eq. 8 from each node's per-sample compute
+ *           time (a+P)/b at its latest batch size, at least one sample per node;
+ *   phase 2: cannikin_opt_split on the learned models; *t_pred = its Eq. 7 prediction (NaN in
+ *           phases 0-1).  Errors: INVALID, INFEASIBLE, and those of opt_split. */
+cannikin_status cannikin_analyzer_plan(cannikin_analyzer* an, int64_t B, const int64_t* cap,
+                                       int64_t* b_out, double* t_pred, int* phase_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,13 @@ SIGNATURES = {
     "cannikin_opt_split": (_I, [ctypes.POINTER(_NodeModel), _I, ctypes.POINTER(_CommModel), _L, _LP,
                                 _LP, _U, _LP, _DP, _DP, _IP]),
     "cannikin_warmup_split": (_I, [_DP, _I, _L, _DP, _LP]),
+    "cannikin_fit_linear": (_I, [_DP, _DP, _I, _DP, _DP]),
+    "cannikin_ivw": (_I, [_DP, _DP, _I, _DP]),
+    "cannikin_analyzer_create": (_I, [_I, ctypes.POINTER(_P)]),
+    "cannikin_analyzer_destroy": (_I, [_P]),
+    "cannikin_analyzer_observe": (_I, [_P, _I, _L, _L, _D, _D, _D, _D, _D]),
+    "cannikin_analyzer_models": (_I, [_P, ctypes.POINTER(_NodeModel), ctypes.POINTER(_CommModel)]),
+    "cannikin_analyzer_plan": (_I, [_P, _L, _LP, _LP, _DP, _IP]),
 }
 
 
@@ -263,3 +270,52 @@ def warmup_split(t_sample, B: int):
     b = (ctypes.c_int64 * n)()
     _check(lib().cannikin_warmup_split(_dbl(t_sample), n, int(B), br, b))
     return list(b), list(br)
+
+
+# ----------------------------------------------------------------------------- measured-model loop
+def fit_linear(x, y):
+    sl, ic = ctypes.c_double(), ctypes.c_double()
+    _check(lib().cannikin_fit_linear(_dbl(x), _dbl(y), len(x), ctypes.byref(sl), ctypes.byref(ic)))
+    return sl.value, ic.value
+
+
+def ivw(estimates, variances) -> float:
+    out = ctypes.c_double()
+    _check(lib().cannikin_ivw(_dbl(estimates), _dbl(variances), len(estimates), ctypes.byref(out)))
+    return out.value
+
+
+class Analyzer:
+    """The paper's analyzer/optimizer loop: observe timings, plan each epoch."""
+
+    def __init__(self, n: int):
+        h = ctypes.c_void_p()
+        _check(lib().cannikin_analyzer_create(n, ctypes.byref(h)))
+        self._h, self.n = h, n
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib().cannikin_analyzer_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def observe(self, node: int, it: int, b: int, a: float, P: float, gamma: float, t_o: float,
+                t_u: float):
+        _check(lib().cannikin_analyzer_observe(self._h, node, int(it), int(b), float(a), float(P),
+                                               float(gamma), float(t_o), float(t_u)))
+
+    def models(self):
+        nodes = (_NodeModel * self.n)()
+        cm = _CommModel()
+        _check(lib().cannikin_analyzer_models(self._h, nodes, ctypes.byref(cm)))
+        return [(x.q, x.s, x.k, x.m) for x in nodes], (cm.gamma, cm.t_o, cm.t_u)
+
+    def plan(self, B: int, cap=None):
+        b = (ctypes.c_int64 * self.n)()
+        t = ctypes.c_double()
+        ph = ctypes.c_int()
+        _check(lib().cannikin_analyzer_plan(self._h, int(B), _i64(cap) if cap is not None else None,
+                                            b, ctypes.byref(t), ctypes.byref(ph)))
+        return {"b": list(b), "T_pred": t.value, "phase": ph.value}
