@@ -276,6 +276,40 @@ cannikin_status cannikin_analyzer_models(cannikin_analyzer* an, cannikin_node_mo
 cannikin_status cannikin_analyzer_plan(cannikin_analyzer* an, int64_t B, const int64_t* cap,
                                        int64_t* b_out, double* t_pred, int* phase_out);
 
+/* ------------------------------------------------------------------------------------------
+ * Adaptive total batch size (host): goodput = throughput x statistical
+ * efficiency, the efficiency modelled by the GNS.
+ * ------------------------------------------------------------------------------------------ */
+
+/* Exponential moving average of the aggregated G and S (separately: the ratio estimator is
+ * biased).  Set decay in [0,1) and count = 0 before the first update.  A snapshot with
+ * G2 <= 0 is skipped (reading Q26).  B_noise = trS / G2 of the average. */
+typedef struct { double G2, trS, decay; int count; } cannikin_gns_ema;
+cannikin_status cannikin_gns_ema_update(cannikin_gns_ema* ema, double G2, double trS);
+
+/* Statistical efficiency of total batch B relative to the initial batch B0 for noise scale
+ * B_noise, in Pollux's form (B_noise + B0) / (B_noise + B) (reading Q27; the paper defers to
+ * Pollux). */
+double cannikin_efficiency(int64_t B, int64_t B0, double B_noise);
+
+/* Among candidates[n_cand] pick the total batch with the largest goodput B/T(B) * efficiency,
+ * T(B) = OptPerf (Eq. 7 at the integer opt_split).  Outputs (optional) T_out[n_cand],
+ * goodput_out[n_cand].  Ties -> the first candidate.  Errors: INVALID, and those of opt_split. */
+cannikin_status cannikin_choose_batch(const cannikin_node_model* nodes, int n,
+                                      const cannikin_comm_model* cm, const int64_t* candidates,
+                                      int n_cand, int64_t B0, double B_noise, int64_t* B_out,
+                                      double* T_out, double* goodput_out);
+
+/* The paper's strategy with the analyzer's learned models: OptPerf_init for every candidate the
+ * first time (or when the candidate list changes), then each epoch only the chosen candidate is
+ * re-solved with the updated models and its cache entry updated; if its overlap pattern (labels)
+ * changed, every candidate is re-solved.  Returns B, its split b_out[n], the
+ * predicted batch time and whether a full recompute happened.  Errors: as analyzer_models. */
+cannikin_status cannikin_analyzer_choose_batch(cannikin_analyzer* an, const int64_t* candidates,
+                                               int n_cand, int64_t B0, double B_noise,
+                                               int64_t* B_out, int64_t* b_out, double* t_pred,
+                                               int* full_recompute);
+
 #ifdef __cplusplus
 }
 #endif

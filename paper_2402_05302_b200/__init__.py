@@ -68,6 +68,11 @@ class _CommModel(ctypes.Structure):
     _fields_ = [("gamma", ctypes.c_double), ("t_o", ctypes.c_double), ("t_u", ctypes.c_double)]
 
 
+class _GnsEma(ctypes.Structure):
+    _fields_ = [("G2", ctypes.c_double), ("trS", ctypes.c_double), ("decay", ctypes.c_double),
+                ("count", ctypes.c_int)]
+
+
 _LIB = None
 
 # Every symbol include/cannikin.h declares, with (restype, argtypes).
@@ -103,6 +108,11 @@ SIGNATURES = {
     "cannikin_analyzer_observe": (_I, [_P, _I, _L, _L, _D, _D, _D, _D, _D]),
     "cannikin_analyzer_models": (_I, [_P, ctypes.POINTER(_NodeModel), ctypes.POINTER(_CommModel)]),
     "cannikin_analyzer_plan": (_I, [_P, _L, _LP, _LP, _DP, _IP]),
+    "cannikin_gns_ema_update": (_I, [ctypes.POINTER(_GnsEma), _D, _D]),
+    "cannikin_efficiency": (_D, [_L, _L, _D]),
+    "cannikin_choose_batch": (_I, [ctypes.POINTER(_NodeModel), _I, ctypes.POINTER(_CommModel), _LP,
+                                   _I, _L, _D, _LP, _DP, _DP]),
+    "cannikin_analyzer_choose_batch": (_I, [_P, _LP, _I, _L, _D, _LP, _LP, _DP, _IP]),
 }
 
 
@@ -312,6 +322,17 @@ class Analyzer:
         _check(lib().cannikin_analyzer_models(self._h, nodes, ctypes.byref(cm)))
         return [(x.q, x.s, x.k, x.m) for x in nodes], (cm.gamma, cm.t_o, cm.t_u)
 
+    def choose_batch(self, candidates, B0: int, B_noise: float):
+        """Goodput-optimal total batch with the OptPerf_init cache."""
+        Bo = ctypes.c_int64()
+        b = (ctypes.c_int64 * self.n)()
+        t = ctypes.c_double()
+        full = ctypes.c_int()
+        _check(lib().cannikin_analyzer_choose_batch(self._h, _i64(candidates), len(candidates),
+                                                    int(B0), float(B_noise), ctypes.byref(Bo), b,
+                                                    ctypes.byref(t), ctypes.byref(full)))
+        return {"B": Bo.value, "b": list(b), "T_pred": t.value, "full_recompute": bool(full.value)}
+
     def plan(self, B: int, cap=None):
         b = (ctypes.c_int64 * self.n)()
         t = ctypes.c_double()
@@ -319,3 +340,37 @@ class Analyzer:
         _check(lib().cannikin_analyzer_plan(self._h, int(B), _i64(cap) if cap is not None else None,
                                             b, ctypes.byref(t), ctypes.byref(ph)))
         return {"b": list(b), "T_pred": t.value, "phase": ph.value}
+
+
+# ----------------------------------------------------------------------------- adaptive batch
+class GnsEma:
+    """EMA of the aggregated G and S (separately), B_noise = S / G of the averages."""
+
+    def __init__(self, decay: float = 0.9):
+        self._s = _GnsEma(0.0, 0.0, float(decay), 0)
+
+    def update(self, G2: float, trS: float):
+        _check(lib().cannikin_gns_ema_update(ctypes.byref(self._s), float(G2), float(trS)))
+
+    @property
+    def count(self) -> int:
+        return self._s.count
+
+    @property
+    def B_noise(self) -> float:
+        return self._s.trS / self._s.G2 if self._s.count else float("nan")
+
+
+def efficiency(B: int, B0: int, B_noise: float) -> float:
+    return lib().cannikin_efficiency(int(B), int(B0), float(B_noise))
+
+
+def choose_batch(nodes, comm, candidates, B0: int, B_noise: float):
+    arr, cm = _models(nodes, comm)
+    k = len(candidates)
+    Bo = ctypes.c_int64()
+    T = (ctypes.c_double * k)()
+    G = (ctypes.c_double * k)()
+    _check(lib().cannikin_choose_batch(arr, len(nodes), ctypes.byref(cm), _i64(candidates), k,
+                                       int(B0), float(B_noise), ctypes.byref(Bo), T, G))
+    return {"B": Bo.value, "T": list(T), "goodput": list(G)}

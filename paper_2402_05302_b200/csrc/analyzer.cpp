@@ -75,10 +75,18 @@ struct Obs {
 };
 }  // namespace
 
+struct OptPerfInitCache {
+  std::vector<int64_t> cand;
+  std::vector<double> T;
+  std::vector<std::vector<int>> labels;
+  bool valid = false;
+};
+
 struct cannikin_analyzer {
   int n = 0;
   int epoch = 0;  // number of plans issued
   std::vector<std::vector<Obs>> obs;
+  OptPerfInitCache cache;
 };
 
 extern "C" cannikin_status cannikin_analyzer_create(int n, cannikin_analyzer** out) {
@@ -285,5 +293,123 @@ extern "C" cannikin_status cannikin_analyzer_plan(cannikin_analyzer* an, int64_t
   an->epoch++;
   if (t_pred) *t_pred = pred;
   if (phase_out) *phase_out = phase;
+  return CANNIKIN_OK;
+}
+
+// ============================================================================================
+// Adaptive total batch size: goodput = throughput x statistical efficiency
+// (Pollux), B_noise from the heterogeneous GNS smoothed by an EMA of G and S
+// separately (the ratio estimator is biased), OptPerf_init cache per candidate.
+// ============================================================================================
+
+extern "C" cannikin_status cannikin_gns_ema_update(cannikin_gns_ema* ema, double G2, double trS) {
+  if (!ema || !(ema->decay >= 0.0) || !(ema->decay < 1.0))
+    return fail(CANNIKIN_ERR_INVALID, "gns_ema_update: decay must be in [0, 1)");
+  if (!std::isfinite(G2) || !std::isfinite(trS)) return fail(CANNIKIN_ERR_DOMAIN, "gns_ema_update: non-finite");
+  if (!(G2 > 0.0)) return CANNIKIN_OK;  // a non-positive G snapshot is left out (reading Q26)
+  if (ema->count == 0) {
+    ema->G2 = G2;
+    ema->trS = trS;
+  } else {
+    ema->G2 = ema->decay * ema->G2 + (1.0 - ema->decay) * G2;
+    ema->trS = ema->decay * ema->trS + (1.0 - ema->decay) * trS;
+  }
+  ema->count++;
+  return CANNIKIN_OK;
+}
+
+extern "C" double cannikin_efficiency(int64_t B, int64_t B0, double B_noise) {
+  // Pollux's statistical efficiency relative to the initial batch B0 (reading Q27)
+  return (B_noise + (double)B0) / (B_noise + (double)B);
+}
+
+extern "C" cannikin_status cannikin_choose_batch(const cannikin_node_model* nodes, int n,
+                                                 const cannikin_comm_model* cm,
+                                                 const int64_t* candidates, int n_cand, int64_t B0,
+                                                 double B_noise, int64_t* B_out,
+                                                 double* T_out, double* goodput_out) {
+  if (!nodes || !cm || !candidates || n_cand < 1 || !B_out || B0 < 1 || !(B_noise >= 0.0))
+    return fail(CANNIKIN_ERR_INVALID, "choose_batch: bad arguments");
+  double best = -1.0;
+  std::vector<int64_t> b(n);
+  for (int c = 0; c < n_cand; ++c) {
+    double t[2];
+    cannikin_status st =
+        cannikin_opt_split(nodes, n, cm, candidates[c], nullptr, nullptr, 0, b.data(), nullptr, t,
+                           nullptr);
+    if (st != CANNIKIN_OK) return st;
+    const double g = (double)candidates[c] / t[1] * cannikin_efficiency(candidates[c], B0, B_noise);
+    if (T_out) T_out[c] = t[1];
+    if (goodput_out) goodput_out[c] = g;
+    if (g > best) {  // ties: the first (smallest) candidate
+      best = g;
+      *B_out = candidates[c];
+    }
+  }
+  return CANNIKIN_OK;
+}
+
+extern "C" cannikin_status cannikin_analyzer_choose_batch(cannikin_analyzer* an,
+                                                          const int64_t* candidates, int n_cand,
+                                                          int64_t B0, double B_noise,
+                                                          int64_t* B_out, int64_t* b_out,
+                                                          double* t_pred, int* full_recompute) {
+  if (!an || !candidates || n_cand < 1 || !B_out || !b_out)
+    return fail(CANNIKIN_ERR_INVALID, "analyzer_choose_batch: bad arguments");
+  const int n = an->n;
+  std::vector<cannikin_node_model> nodes(n);
+  cannikin_comm_model cm;
+  cannikin_status st = cannikin_analyzer_models(an, nodes.data(), &cm);
+  if (st != CANNIKIN_OK) return st;
+  auto& C = an->cache;
+  bool same_cands = C.valid && (int)C.cand.size() == n_cand;
+  for (int c = 0; same_cands && c < n_cand; ++c) same_cands = C.cand[c] == candidates[c];
+  std::vector<int64_t> bb(n);
+  std::vector<int> lab(n);
+  auto solve = [&](int c, double* T, std::vector<int>* labels) -> cannikin_status {
+    double t[2];
+    cannikin_status s2 = cannikin_opt_split(nodes.data(), n, &cm, candidates[c], nullptr, nullptr,
+                                            0, bb.data(), nullptr, t, lab.data());
+    if (s2 != CANNIKIN_OK) return s2;
+    *T = t[1];
+    if (labels) *labels = lab;
+    return CANNIKIN_OK;
+  };
+  int recompute = 0;
+  if (!same_cands) {  // OptPerf_init for every candidate
+    C.cand.assign(candidates, candidates + n_cand);
+    C.T.assign(n_cand, 0.0);
+    C.labels.assign(n_cand, std::vector<int>(n));
+    for (int c = 0; c < n_cand; ++c)
+      if ((st = solve(c, &C.T[c], &C.labels[c])) != CANNIKIN_OK) return st;
+    C.valid = true;
+    recompute = 1;
+  }
+  for (int round = 0; round < 2; ++round) {
+    int best = 0;
+    double bestg = -1.0;
+    for (int c = 0; c < n_cand; ++c) {
+      const double g = (double)candidates[c] / C.T[c] * cannikin_efficiency(candidates[c], B0, B_noise);
+      if (g > bestg) { bestg = g; best = c; }
+    }
+    // OptPerf of the chosen candidate from the updated models
+    double T;
+    std::vector<int> labels;
+    if ((st = solve(best, &T, &labels)) != CANNIKIN_OK) return st;
+    if (labels != C.labels[best] && round == 0) {
+      // overlap pattern changed: start over for every candidate
+      for (int c = 0; c < n_cand; ++c)
+        if ((st = solve(c, &C.T[c], &C.labels[c])) != CANNIKIN_OK) return st;
+      recompute = 1;
+      continue;
+    }
+    C.T[best] = T;  // update OptPerf_init for this candidate
+    C.labels[best] = labels;
+    *B_out = candidates[best];
+    for (int i = 0; i < n; ++i) b_out[i] = bb[i];
+    if (t_pred) *t_pred = T;
+    break;
+  }
+  if (full_recompute) *full_recompute = recompute;
   return CANNIKIN_OK;
 }

@@ -1,0 +1,84 @@
+"""Pins for oracle/goodput.py (adaptive total batch, NEXT-2) and its library twin."""
+import math
+
+import numpy as np
+import pytest
+
+import cannikin_synth as synth
+import paper_2402_05302_b200 as ck
+from oracle import goodput as ogp
+from oracle import learn
+from oracle import optsplit as osp
+
+CANDS = [16, 32, 64, 96, 128, 192, 256, 384, 512]
+
+
+def test_efficiency_closed_forms():
+    assert ogp.efficiency(32, 32, 123.0) == 1.0                       # B = B0
+    assert math.isclose(ogp.efficiency(512, 32, 1e15), 1.0, rel_tol=1e-12)  # noise dominates
+    assert math.isclose(ogp.efficiency(512, 32, 0.0), 32 / 512)       # no noise: B0 / B
+    assert math.isclose(ck.efficiency(100, 32, 50.0), ogp.efficiency(100, 32, 50.0), rel_tol=1e-15)
+
+
+def test_choice_limits():
+    """B_noise = 0: goodput = B0 / T(B), T increasing -> the smallest candidate; B_noise -> inf:
+    goodput = throughput -> the candidate with the largest B / T(B)."""
+    rng = np.random.default_rng(1)
+    nodes, comm = synth.random_cluster(rng, 4)
+    assert ogp.choose_batch(nodes, comm, CANDS, 32, 0.0) == CANDS[0]
+    thr = [B / osp.int_split_greedy(nodes, comm, B)[1] for B in CANDS]
+    assert ogp.choose_batch(nodes, comm, CANDS, 32, 1e15) == CANDS[int(np.argmax(thr))]
+
+
+def test_choice_grows_with_noise_scale():
+    """fig:gns: as the GNS grows during training, the chosen total batch grows."""
+    rng = np.random.default_rng(2)
+    nodes, comm = synth.random_cluster(rng, 4)
+    picks = [ogp.choose_batch(nodes, comm, CANDS, 16, bn) for bn in (1, 10, 100, 1000, 1e5)]
+    assert picks == sorted(picks) and picks[0] < picks[-1]
+
+
+def test_ema_separately_not_ratio():
+    e = ogp.Ema(0.5)
+    e.update(1.0, 100.0)
+    e.update(3.0, 100.0)
+    assert e.B_noise == 100.0 / 2.0                 # not mean(100, 33.3)
+    e.update(-1.0, 5.0)                             # non-positive G skipped (reading Q26)
+    assert e.count == 2
+    le = ck.GnsEma(0.5)
+    for G, S in [(1.0, 100.0), (3.0, 100.0), (-1.0, 5.0)]:
+        le.update(G, S)
+    assert le.count == 2 and le.B_noise == e.B_noise
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_library_choose_batch_matches_oracle(seed):
+    rng = np.random.default_rng(10 + seed)
+    nodes, comm = synth.random_cluster(rng, int(rng.integers(2, 8)))
+    for bn in (0.5, 20.0, 300.0, 4000.0, 1e6):
+        r = ck.choose_batch(nodes, comm, CANDS, 16, bn)
+        assert r["B"] == ogp.choose_batch(nodes, comm, CANDS, 16, bn)
+        for B, T in zip(CANDS, r["T"]):
+            assert T == osp.int_split_greedy(nodes, comm, B)[1]
+
+
+def test_analyzer_choose_batch_cache_equals_brute_force_with_fixed_models():
+    """The OptPerf_init cache picks the brute-force optimum when the learned models do
+    not change between epochs, and recomputes only when the overlap pattern changes."""
+    rng = np.random.default_rng(21)
+    n = 4
+    nodes, comm = synth.random_cluster(rng, n)
+    an = ck.Analyzer(n)
+    it = 0
+    for b in ([20] * n, [35, 28, 24, 18]):  # two batch sizes per node, noiseless
+        for o_i, o in enumerate(synth.simulate_iteration(nodes, comm, b, rng)):
+            an.observe(o_i, it, b[o_i], o["a"], o["P"], o["gamma"], o["t_o"], o["t_u"])
+        it += 1
+    learned, lcomm = an.models()
+    fulls = []
+    for bn in (1.0, 10.0, 100.0, 1000.0, 1e4, 1e4):
+        r = an.choose_batch(CANDS, 16, bn)
+        fulls.append(r["full_recompute"])
+        assert r["B"] == ogp.choose_batch(learned, lcomm, CANDS, 16, bn)
+        assert sum(r["b"]) == r["B"]
+    assert fulls[0] is True and fulls[-1] is False
