@@ -76,6 +76,26 @@ def main():
             p1.record()
         torch.cuda.synchronize()
         res["eager_pair_per_launch"] = statistics.median(p0.elapsed_time(p1) for p0, p1 in pe)
+        # (e) spaced: 2 ms of idle HBM (one spinning warp) before every launch
+        pe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(R)]
+        for p0, p1 in pe:
+            ck.emulate_compute(2e-3)
+            p0.record()
+            k()
+            p1.record()
+        torch.cuda.synchronize()
+        res["spaced_2ms"] = statistics.median(p0.elapsed_time(p1) for p0, p1 in pe)
+        # (f) L2 flushed (write 256 MB) before every launch, graph-free
+        flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+        pe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(R)]
+        for p0, p1 in pe:
+            flush.zero_()
+            p0.record()
+            k()
+            p1.record()
+        torch.cuda.synchronize()
+        res["after_l2_flush"] = statistics.median(p0.elapsed_time(p1) for p0, p1 in pe)
+        del flush
         print(json.dumps({"shape": name, "variant": var, "bytes": nbytes,
                           **{m: round(v * 1e3, 2) for m, v in res.items()},
                           **{m + "_GBps": round(nbytes / (v * 1e-3) / 1e9) for m, v in res.items()}}), flush=True)
