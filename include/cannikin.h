@@ -157,9 +157,10 @@ cannikin_status cannikin_ddp_allreduce_mean(cannikin_ctx* ctx, void* bucket, siz
  * P:158-165) on homogeneous GPUs, as Cluster C's dummy load does.  Errors: DOMAIN, CUDA. */
 cannikin_status cannikin_emulate_compute(double seconds, void* stream);
 
-/* Diagnostics (tracing): per-CTA device timeline of the last weighted_allreduce kernel (world > 1),
- * %globaltimer ns: [start, entry barrier passed, data done, exit barrier passed, end (last CTA
- * only)] for CTA 0..*n_ctas-1, written to out[5*cta + k] (host).  Synchronises the device.
+/* Diagnostics (tracing): per-CTA device timeline of the last two-shot (world > 1) or emulated-rank
+ * (LDG variant) kernel on this ctx, %globaltimer ns: [start, entry barrier passed (two-shot only),
+ * data done, exit barrier passed / partials written, end (last CTA only)] for CTA
+ * 0..*n_ctas-1, written to out[5*cta + k] (host).  Synchronises the device.
  * Errors: INVALID, CUDA. */
 cannikin_status cannikin_trace(cannikin_ctx* ctx, uint64_t* out, int max_ctas, int* n_ctas);
 

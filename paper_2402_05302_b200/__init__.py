@@ -215,7 +215,7 @@ class Context:
     def ddp_allreduce_mean(self, ptr: int, n: int, dtype: int, stream=None):
         _check(lib().cannikin_ddp_allreduce_mean(self._h, ptr, n, dtype, _stream(stream)))
 
-    def trace(self, max_ctas: int = 256):
+    def trace(self, max_ctas: int = 2048):
         """Per-CTA timeline (ns) of the last two-shot kernel: list of [start, entry, data, exit,
         end] (end only set on the last CTA to finish)."""
         buf = (ctypes.c_uint64 * (5 * max_ctas))()

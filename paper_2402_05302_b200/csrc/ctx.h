@@ -30,8 +30,8 @@ struct Ctrl {
   unsigned ar_counter;                                       // [local] dynamic two-shot chunk counter
   int error_code;                                            // [local] protocol error (trap reason)
   double stats[kMaxWorld + 1];                               // [local] accumulated |g_j|^2, |g|^2
-  uint64_t trace[kMaxArBlocks][5];                           // [local] K3 per-CTA timeline (ns)
-  int trace_grid;                                            // [local] CTAs of the last K3 call
+  uint64_t trace[kMaxLocalBlocks][5];                        // [local] per-CTA timeline (ns)
+  int trace_grid;                                            // [local] CTAs of the last traced kernel
   double local_part[kMaxLocalBlocks][kMaxEmu + 1];           // [local] emulated-kernel partials
 };
 

@@ -18,6 +18,8 @@ struct LocalArgs {
   unsigned* ticket;
   double* local_sq;  // [n]
   double* global_sq;
+  uint64_t* trace;   // [grid][5] per-CTA timeline (LDG variant)
+  int* trace_grid;
   int accumulate;
 };
 

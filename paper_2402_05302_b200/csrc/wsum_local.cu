@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(256) wsum_local_kernel(const LocalArgs a) {
   __shared__ double red[32 * (NR + 1)];
   __shared__ bool s_last;
 
+  if (threadIdx.x == 0) a.trace[blockIdx.x * 5] = dev::globaltimer_ns();
   float r[NR];
   const char* in[NR];
 #pragma unroll
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(256) wsum_local_kernel(const LocalArgs a) {
     }
   }
 
+  if (threadIdx.x == 0) a.trace[blockIdx.x * 5 + 2] = dev::globaltimer_ns();
   double vals[NR + 1];
 #pragma unroll
   for (int j = 0; j < NR; ++j) vals[j] = lsq[j];
@@ -107,6 +109,7 @@ __global__ void __launch_bounds__(256) wsum_local_kernel(const LocalArgs a) {
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int j = 0; j <= NR; ++j) a.partials[(size_t)blockIdx.x * (NR + 1) + j] = vals[j];
+    a.trace[blockIdx.x * 5 + 3] = dev::globaltimer_ns();
     __threadfence();
     const unsigned t = atomicAdd(a.ticket, 1u);
     s_last = (t == gridDim.x - 1);
@@ -124,6 +127,8 @@ __global__ void __launch_bounds__(256) wsum_local_kernel(const LocalArgs a) {
       *dst = a.accumulate ? (*dst + tot[j]) : tot[j];
     }
     *a.ticket = 0u;
+    a.trace[blockIdx.x * 5 + 4] = dev::globaltimer_ns();
+    *a.trace_grid = gridDim.x;
   }
 }
 
@@ -194,6 +199,8 @@ cudaError_t launch_wsum_local(cannikin_ctx* ctx, const void* const* in, int nr, 
   a.nvec = n * esz / 16;
   a.partials = &ctx->ctrl->local_part[0][0];
   a.ticket = &ctx->ctrl->ticket_local;
+  a.trace = &ctx->ctrl->trace[0][0];
+  a.trace_grid = &ctx->ctrl->trace_grid;
   a.local_sq = d_local_sq;
   a.global_sq = d_global_sq;
   a.accumulate = accumulate ? 1 : 0;
