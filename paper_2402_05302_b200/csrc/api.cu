@@ -82,7 +82,7 @@ extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world
   if (ctx->grid_ar > cannikin::kMaxArBlocks) ctx->grid_ar = cannikin::kMaxArBlocks;
   if (const char* t = std::getenv("CANNIKIN_K2_IMPL")) ctx->local_tma = std::strcmp(t, "tma") == 0;
   if (const char* t = std::getenv("CANNIKIN_LOCAL_GRID")) ctx->grid_local = std::atoi(t);
-  if (const char* t = std::getenv("CANNIKIN_K2_ALT_U")) ctx->local_alt_u = std::atoi(t) != 0;
+  if (const char* t = std::getenv("CANNIKIN_K2_NT")) ctx->local_nt = std::atoi(t);
   if (const char* t = std::getenv("CANNIKIN_SPIN_TIMEOUT_MS"))
     ctx->spin_timeout_ns = (uint64_t)std::strtoull(t, nullptr, 10) * 1000000ull;
   ctx->heap_bytes = align_up(heap_bytes, 256);

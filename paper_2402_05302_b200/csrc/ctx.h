@@ -43,7 +43,7 @@ struct cannikin_ctx {
   int ar_dyn = -1;          // CANNIKIN_AR_DYN=0|1 forces static/dynamic chunks; -1 = by size
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2
   bool local_tma = false;   // default variant of K2 (CANNIKIN_K2_IMPL=tma|ldg)
-  bool local_alt_u = false; // CANNIKIN_K2_ALT_U=1: twice the loads in flight per thread
+  int local_nt = 256;       // CANNIKIN_K2_NT: CTA size of K2 (256, or one big CTA per SM)
   int num_sms = 148;
   size_t heap_bytes = 0;
   // local allocation = [Ctrl | user heap (heap_bytes) | scratch (heap_bytes)]

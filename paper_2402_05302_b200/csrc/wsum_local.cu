@@ -47,8 +47,8 @@ __device__ __forceinline__ void wsum_vec(const uint4 (&x)[NR], const float (&r)[
   dev::st16(dst, V::pack(acc));
 }
 
-template <typename T, int NR, int U>
-__global__ void __launch_bounds__(256) wsum_local_kernel(const LocalArgs a) {
+template <typename T, int NR, int U, int NT>
+__global__ void __launch_bounds__(NT) wsum_local_kernel(const LocalArgs a) {
   using V = dev::Vec<T>;
   constexpr int E = V::E;
   __shared__ double red[32 * (NR + 1)];
@@ -133,18 +133,20 @@ __global__ void __launch_bounds__(256) wsum_local_kernel(const LocalArgs a) {
 }
 
 // ------------------------------------------------------------------------------ host launcher
-// Loads in flight per thread = NR * U; the default keeps NR * U ~ 4-8 (U_alt = 2 U for sweeps).
+// Loads in flight per thread = NR * U (~4-8).  CTA size NT: 256 (5 CTAs/SM for n = 8) or one big
+// CTA per SM (NT = 1024 for n <= 8, 512 above): fewer, larger CTAs spread less in speed (the
+// cross-CTA L1tex-queue effect) and leave fewer partial rows for the final reduction.
 template <int NR>
 constexpr int u_default() {
   return NR <= 2 ? 4 : (NR <= 4 ? 2 : 1);
 }
 
-template <typename T, int NR, int U>
+template <typename T, int NR, int U, int NT>
 static int occupancy_grid(int num_sms) {
   static int cached = 0;
   if (!cached) {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wsum_local_kernel<T, NR, U>, 256,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wsum_local_kernel<T, NR, U, NT>, NT,
                                                       0) != cudaSuccess ||
         per_sm < 1)
       per_sm = 1;
@@ -154,25 +156,33 @@ static int occupancy_grid(int num_sms) {
   return g > kMaxLocalBlocks ? kMaxLocalBlocks : g;
 }
 
-template <typename T, int NR, int U>
-static cudaError_t launch_u(const LocalArgs& a, int num_sms, int grid_override, cudaStream_t st) {
-  int grid = grid_override > 0 ? grid_override : occupancy_grid<T, NR, U>(num_sms);
+template <typename T, int NR, int U, int NT>
+static cudaError_t launch_nt(const LocalArgs& a, int num_sms, int grid_override, cudaStream_t st) {
+  int grid = grid_override > 0 ? grid_override : occupancy_grid<T, NR, U, NT>(num_sms);
   // do not launch CTAs that would own no vector (keeps tiny buckets cheap)
-  const size_t need = (a.nvec + 255) / 256;
+  const size_t need = (a.nvec + NT - 1) / NT;
   if ((size_t)grid > need) grid = need < 1 ? 1 : (int)need;
   if (grid > kMaxLocalBlocks) grid = kMaxLocalBlocks;
-  wsum_local_kernel<T, NR, U><<<grid, 256, 0, st>>>(a);
+  wsum_local_kernel<T, NR, U, NT><<<grid, NT, 0, st>>>(a);
   return cudaGetLastError();
 }
 
+template <typename T, int NR>
+static cudaError_t launch_u(const LocalArgs& a, int num_sms, int grid_override, int nt,
+                            cudaStream_t st) {
+  constexpr int U = u_default<NR>();
+  constexpr int BIG = NR <= 8 ? 1024 : 512;
+  if (nt >= 512) return launch_nt<T, NR, U, BIG>(a, num_sms, grid_override, st);
+  return launch_nt<T, NR, U, 256>(a, num_sms, grid_override, st);
+}
+
 template <typename T>
-static cudaError_t dispatch(int nr, const LocalArgs& a, int num_sms, int grid_override, bool alt_u,
+static cudaError_t dispatch(int nr, const LocalArgs& a, int num_sms, int grid_override, int nt,
                             cudaStream_t st) {
   switch (nr) {
-#define CANNIKIN_CASE(K)                                                                   \
-  case K:                                                                                  \
-    return alt_u ? launch_u<T, K, 2 * u_default<K>()>(a, num_sms, grid_override, st)       \
-                 : launch_u<T, K, u_default<K>()>(a, num_sms, grid_override, st);
+#define CANNIKIN_CASE(K) \
+  case K:                \
+    return launch_u<T, K>(a, num_sms, grid_override, nt, st);
     CANNIKIN_CASE(1) CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5)
     CANNIKIN_CASE(6) CANNIKIN_CASE(7) CANNIKIN_CASE(8) CANNIKIN_CASE(9) CANNIKIN_CASE(10)
     CANNIKIN_CASE(11) CANNIKIN_CASE(12) CANNIKIN_CASE(13) CANNIKIN_CASE(14) CANNIKIN_CASE(15)
@@ -206,8 +216,8 @@ cudaError_t launch_wsum_local(cannikin_ctx* ctx, const void* const* in, int nr, 
   a.accumulate = accumulate ? 1 : 0;
   // partial rows are (nr+1) doubles wide: reinterpret local_part as a flat array
   if (dt == CANNIKIN_F32)
-    return dispatch<float>(nr, a, ctx->num_sms, grid_override, ctx->local_alt_u, st);
-  return dispatch<__nv_bfloat16>(nr, a, ctx->num_sms, grid_override, ctx->local_alt_u, st);
+    return dispatch<float>(nr, a, ctx->num_sms, grid_override, ctx->local_nt, st);
+  return dispatch<__nv_bfloat16>(nr, a, ctx->num_sms, grid_override, ctx->local_nt, st);
 }
 
 }  // namespace cannikin

@@ -50,7 +50,7 @@ def main():
         for var, grid, altu, dyn in variants:
             if grid is not None:
                 os.environ["CANNIKIN_LOCAL_GRID"] = str(grid)
-            os.environ["CANNIKIN_K2_ALT_U"] = str(altu)
+            os.environ["CANNIKIN_K2_NT"] = "1024" if altu else "256"
             os.environ["CANNIKIN_K2_DYN"] = str(dyn)
             ctx = ck.Context(world=1, device=0)
             for _ in range(3):

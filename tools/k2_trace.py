@@ -22,6 +22,7 @@ def q(xs, p):
 
 def main():
     torch.cuda.set_device(0)
+    nt = os.environ.get("CANNIKIN_K2_NT", "256")
     for name, nr, N, dt in [("c4", 8, 110_000_000, "bf16"), ("c5", 8, 354_823_168, "f32"),
                             ("c4q", 8, 27_500_000, "bf16")]:
         b = list(range(1, nr + 1))
@@ -45,11 +46,13 @@ def main():
         done = [(t[2] - t0) / 1e3 for t in tr]
         last = max(tr, key=lambda t: t[4])
         nbytes = (nr + 1) * N * (4 if dt == "f32" else 2)
-        print(json.dumps({"shape": name, "ctas": len(tr), "event_us": round(e0.elapsed_time(e1) * 1e3, 1),
+        print(json.dumps({"shape": name, "nt": nt, "ctas": len(tr), "event_us": round(e0.elapsed_time(e1) * 1e3, 1),
                           "start_spread_us": round(max(starts), 2),
                           "done_min": round(min(done), 1), "done_med": round(statistics.median(done), 1),
                           "done_p90": round(q(done, 0.9), 1), "done_max": round(max(done), 1),
                           "end_us": round((last[4] - t0) / 1e3, 1),
+                          "last_cta_blocksum_us": round((last[3] - last[2]) / 1e3, 2),
+                          "last_cta_final_us": round((last[4] - last[3]) / 1e3, 2),
                           "GBps_at_median_done": round(nbytes / (statistics.median(done) * 1e-6) / 1e9),
                           "GBps_span": round(nbytes / ((last[4] - t0) * 1e-9) / 1e9)}), flush=True)
         ctx.close()
