@@ -129,6 +129,23 @@ def main():
                  out3=out3, out4=out4, loc=np.array(loc), glob=glob, loc2=np.array(loc2),
                  glob2=glob2, loc3=np.array(loc3), glob3=glob3, loc4=np.array(loc4), glob4=glob4,
                  b=np.array(b))
+    # guard bands: buckets A | B | C adjacent in the heap; reducing B (ragged) must not touch A, C
+    for N in (1, 7, 4099, (1 << 20) + 3):
+        for dtype in ("f32", "bf16"):
+            A = ta.bucket_tensor(ctx, 4096, tdt[dtype])
+            Bk = ta.bucket_tensor(ctx, N, tdt[dtype])
+            C = ta.bucket_tensor(ctx, 4096, tdt[dtype])
+            A.fill_(-3.0)
+            C.fill_(-3.0)
+            Bk.copy_(to_dev(synth.gns_gradients(world, N, [1] * world, seed=N)[rank], "f32").to(tdt[dtype]))
+            ta.weighted_allreduce(ctx, Bk, 1.0 / world)
+            torch.cuda.synchronize()
+            ok = bool(torch.all(A == -3.0)) and bool(torch.all(C == -3.0))
+            np.save(os.path.join(args.out, f"rank{rank}_canary_{dtype}_{N}.npy"), np.array([ok]))
+            ta.free_bucket_tensor(ctx, C)
+            ta.free_bucket_tensor(ctx, Bk)
+            ta.free_bucket_tensor(ctx, A)
+    ctx.gns_stats()
     # DDP baseline semantics: mean of the ranks' buffers
     x = torch.full((1000,), float(rank + 1), device="cuda")
     ta.ddp_allreduce_mean(ctx, x)

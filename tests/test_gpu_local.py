@@ -234,3 +234,27 @@ def test_full_size_c4_sampled(ctx, nr, variant):
         gsum += agg.sq_norm(agg.weighted_sum(parts, r))
     assert np.allclose(ls, lsum, rtol=1e-4)
     assert abs(float(glob.cpu()[0]) - gsum) <= 1e-4 * gsum
+
+
+@pytest.mark.parametrize("variant", ["ldg", "tma"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("N", [1, 7, 9, 4099, 65536 + 3])
+def test_no_out_of_bounds_writes(ctx, dtype, N, variant):
+    """Guard bands (compute-sanitizer is closed on this pool): inputs and output are slices in the
+    middle of canary-filled buffers; every canary byte must survive, ragged tails included."""
+    tdt = TDT[dtype]
+    pad = 4096
+    esz = 4 if dtype == "f32" else 2
+    big = [torch.full((N + 2 * pad,), -7.0, dtype=tdt, device="cuda") for _ in range(4)]
+    gs = synth.gns_gradients(3, N, [1, 2, 3], seed=N, dtype=dtype)
+    for j in range(3):
+        big[j][pad:pad + N] = to_dev(gs[j], dtype)
+    out_big = big[3]
+    stats = torch.full((8,), -5.0, dtype=torch.float64, device="cuda")
+    ta.weighted_sum_local(ctx, [b[pad:pad + N] for b in big[:3]], [0.2, 0.3, 0.5],
+                          out_big[pad:pad + N], stats[2:5], stats[5:6], variant=variant)
+    torch.cuda.synchronize()
+    for bb in big:
+        assert torch.all(bb[:pad] == -7.0) and torch.all(bb[pad + N:] == -7.0)
+    assert torch.all(stats[:2] == -5.0) and torch.all(stats[6:] == -5.0)
+    del esz

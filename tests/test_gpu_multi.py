@@ -79,3 +79,12 @@ def test_ddp_baseline_mean(results):
     world, d = results
     x = np.load(os.path.join(d, "rank0_ddp.npy"))
     assert np.allclose(x, (world + 1) / 2)
+
+
+def test_no_out_of_bounds_writes(results):
+    """Guard bands around heap buckets (compute-sanitizer is closed on this pool)."""
+    world, d = results
+    for N in (1, 7, 4099, (1 << 20) + 3):
+        for dtype in ("f32", "bf16"):
+            for r in range(world):
+                assert bool(np.load(os.path.join(d, f"rank{r}_canary_{dtype}_{N}.npy"))[0]), (N, dtype, r)
