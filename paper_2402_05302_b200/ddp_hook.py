@@ -1,0 +1,41 @@
+"""PyTorch DDP integration: a communication hook that replaces DDP's
+per-bucket average with Cannikin's weighted all-reduce g = sum_i r_i g_i (Eq. 9)
+and collects the GNS norm statistics of every bucket in the same pass (Eq. 10 inputs).
+
+DDP already does the bucketing and overlaps each bucket's sync with the rest of backprop (the
+mechanism §3.2.3 models); the hook only swaps the reduction.  Each rank's local loss
+must be the MEAN over its b_i samples (Eq. 1) and r_i = b_i / B.  After backward,
+`state.ctx.gns_stats()` returns |g_j|^2 for every rank and |g|^2 of the whole gradient.
+
+    state = CannikinHookState(ctx, r_i)
+    ddp_model.register_comm_hook(state, cannikin_hook)
+
+Argument marshalling only: the reduction runs in libcannikin.so (two-shot NVLink kernel; DDP's
+bucket buffers are not in the peer-mapped heap, so each bucket is staged through it).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import Context
+from . import torch_api as ta
+
+
+class CannikinHookState:
+    def __init__(self, ctx: Context, r_i: float):
+        self.ctx = ctx
+        self.r_i = float(r_i)
+        self.buckets = 0
+
+    def set_ratio(self, r_i: float):
+        """Update r_i = b_i / B when the split changes (a new epoch's plan)."""
+        self.r_i = float(r_i)
+
+
+def cannikin_hook(state: CannikinHookState, bucket) -> torch.futures.Future:
+    buf = bucket.buffer()
+    ta.weighted_allreduce(state.ctx, buf, state.r_i)  # enqueued on the current stream
+    state.buckets += 1
+    fut: torch.futures.Future = torch.futures.Future()
+    fut.set_result(buf)
+    return fut

@@ -1,0 +1,48 @@
+"""End-to-end Eq. 9 through torch DDP with the Cannikin comm hook (NEXT-3): with uneven local
+batches b_i and per-rank mean losses, every rank's reduced gradient equals the full-batch mean
+gradient over all B samples, bit-identical across ranks; the hook's statistics equal the
+local and global squared norms."""
+import os
+import socket
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_ddp_hook_equals_full_batch_gradient():
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(torch.cuda.device_count(), 8)
+    d = tempfile.mkdtemp()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           os.path.join(os.path.dirname(__file__), "mp_ddp_worker.py"), "--out", d]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000"))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    ranks = [dict(np.load(os.path.join(d, f"rank{k}.npz"))) for k in range(world)]
+    ref = ranks[0]["ref"].astype(np.float64)
+    scale = np.max(np.abs(ref))
+    for k in range(world):
+        assert int(ranks[k]["buckets"]) >= 2          # several DDP buckets went through the hook
+        got = ranks[k]["got"].astype(np.float64)
+        assert np.max(np.abs(got - ref)) <= 1e-4 * scale
+        assert np.array_equal(ranks[k]["got"], ranks[0]["got"])
+        assert np.array_equal(ranks[k]["loc"], ranks[0]["loc"])
+        assert abs(float(ranks[0]["loc"][k]) - float(ranks[k]["gi_sq"])) <= 1e-4 * float(ranks[k]["gi_sq"])
+    gsq = float((ref ** 2).sum())
+    assert abs(float(ranks[0]["glob"]) - gsq) <= 1e-4 * gsq
