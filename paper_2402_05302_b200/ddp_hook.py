@@ -13,8 +13,6 @@ must be the MEAN over its b_i samples (Eq. 1) and r_i = b_i / B.  After backward
 Argument marshalling only: the reduction runs in libcannikin.so (two-shot NVLink kernel; DDP's
 bucket buffers are not in the peer-mapped heap, so each bucket is staged through it).
 """
-from __future__ import annotations
-
 import torch
 
 from . import Context
@@ -32,10 +30,10 @@ class CannikinHookState:
         self.r_i = float(r_i)
 
 
-def cannikin_hook(state: CannikinHookState, bucket) -> torch.futures.Future:
+def cannikin_hook(state: CannikinHookState, bucket) -> torch.futures.Future[torch.Tensor]:
     buf = bucket.buffer()
     ta.weighted_allreduce(state.ctx, buf, state.r_i)  # enqueued on the current stream
     state.buckets += 1
-    fut: torch.futures.Future = torch.futures.Future()
+    fut = torch.futures.Future()
     fut.set_result(buf)
     return fut
