@@ -58,6 +58,12 @@ def main():
     ddp = nn.parallel.DistributedDataParallel(model, device_ids=[lr], bucket_cap_mb=4)
     state = CannikinHookState(ctx, b[rank] / B)
     ddp.register_comm_hook(state, cannikin_hook)
+    # iteration 1 (DDP builds its buckets), then iteration 2 on the rebuilt buckets
+    ce(ddp(Xl), yl).backward()
+    torch.cuda.synchronize()
+    ctx.gns_stats()
+    model.zero_grad(set_to_none=False)
+    state.buckets = 0
     ce(ddp(Xl), yl).backward()
     torch.cuda.synchronize()
     got = flat_grad(model)

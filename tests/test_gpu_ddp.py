@@ -39,6 +39,7 @@ def test_ddp_hook_equals_full_batch_gradient():
     scale = np.max(np.abs(ref))
     for k in range(world):
         assert int(ranks[k]["buckets"]) >= 2          # several DDP buckets went through the hook
+        assert int(ranks[k]["buckets"]) == int(ranks[0]["buckets"])
         got = ranks[k]["got"].astype(np.float64)
         assert np.max(np.abs(got - ref)) <= 1e-4 * scale
         assert np.array_equal(ranks[k]["got"], ranks[0]["got"])
