@@ -20,10 +20,14 @@ from . import torch_api as ta
 
 
 class CannikinHookState:
-    def __init__(self, ctx: Context, r_i: float):
+    def __init__(self, ctx: Context, r_i: float, timing: bool = False):
         self.ctx = ctx
         self.r_i = float(r_i)
         self.buckets = 0
+        # optional telemetry for the measured-model loop: per bucket a pair of CUDA
+        # events around the reduction (the first one also marks "first bucket ready", Eq. 4)
+        self.timing = timing
+        self.events = []
 
     def set_ratio(self, r_i: float):
         """Update r_i = b_i / B when the split changes (a new epoch's plan)."""
@@ -32,7 +36,14 @@ class CannikinHookState:
 
 def cannikin_hook(state: CannikinHookState, bucket) -> torch.futures.Future[torch.Tensor]:
     buf = bucket.buffer()
+    if state.timing:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
     ta.weighted_allreduce(state.ctx, buf, state.r_i)  # enqueued on the current stream
+    if state.timing:
+        e1.record()
+        state.events.append((e0, e1))
     state.buckets += 1
     fut = torch.futures.Future()
     fut.set_result(buf)
