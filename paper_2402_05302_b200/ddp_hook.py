@@ -24,6 +24,8 @@ class CannikinHookState:
         self.ctx = ctx
         self.r_i = float(r_i)
         self.buckets = 0
+        # reductions run on their own stream so they overlap the rest of backprop (§3.2.3)
+        self.stream = torch.cuda.Stream(device=torch.device("cuda", ctx.device))
         # optional telemetry for the measured-model loop: per bucket a pair of CUDA
         # events around the reduction (the first one also marks "first bucket ready", Eq. 4)
         self.timing = timing
@@ -36,15 +38,19 @@ class CannikinHookState:
 
 def cannikin_hook(state: CannikinHookState, bucket) -> torch.futures.Future[torch.Tensor]:
     buf = bucket.buffer()
-    if state.timing:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-    ta.weighted_allreduce(state.ctx, buf, state.r_i)  # enqueued on the current stream
-    if state.timing:
-        e1.record()
-        state.events.append((e0, e1))
-    state.buckets += 1
-    fut = torch.futures.Future()
-    fut.set_result(buf)
+    cs = state.stream
+    cs.wait_stream(torch.cuda.current_stream())  # this bucket's gradients are complete
+    with torch.cuda.stream(cs):
+        if state.timing:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
+        ta.weighted_allreduce(state.ctx, buf, state.r_i, stream=cs)
+        if state.timing:
+            e1.record(cs)
+            state.events.append((e0, e1))
+        state.buckets += 1
+        # CUDA-aware future: DDP's consumer stream waits for the comm stream, not the host
+        fut = torch.futures.Future(devices=[buf.device])
+        fut.set_result(buf)
     return fut

@@ -38,18 +38,21 @@ NSTAGE = 6
 
 
 class _Delay(torch.autograd.Function):
-    """Identity; its backward spends `box[0]` seconds of emulated compute first."""
+    """Identity; its backward spends `box[0]` seconds of emulated compute first, and the stage-0
+    instance (the last backward op) records `box[1]` = end of backprop compute."""
 
     @staticmethod
-    def forward(ctx, x, box):
-        ctx.box = box
+    def forward(ctx, x, box, last):
+        ctx.box, ctx.last = box, last
         return x.view_as(x)
 
     @staticmethod
     def backward(ctx, g):
         if ctx.box[0] > 0:
             ck.emulate_compute(ctx.box[0])
-        return g, None
+        if ctx.last and ctx.box[1] is not None:
+            ctx.box[1].record()
+        return g, None, None
 
 
 class SlowResNet(nn.Module):
@@ -62,11 +65,13 @@ class SlowResNet(nn.Module):
                                      r.layer2, r.layer3, r.layer4,
                                      nn.Sequential(r.avgpool, nn.Flatten(), r.fc)])
         self.fwd = [0.0]
-        self.bwd = [0.0]
+        self.bwd = [0.0, None]
 
     def forward(self, x):
-        for st in self.stages:
-            x = _Delay.apply(x, self.bwd)
+        for i, st in enumerate(self.stages):
+            if i == 0 and not x.requires_grad:
+                x = x.requires_grad_()  # so that the stage-0 backward hook runs
+            x = _Delay.apply(x, self.bwd, i == 0)
             x = st(x)
             if self.fwd[0] > 0:
                 ck.emulate_compute(self.fwd[0])
@@ -100,8 +105,9 @@ def main():
         bb = min(bb, B)
         for rep in range(4):
             e0, e1, e2 = E(), E(), E()
+            cal.bwd[1] = None
             e0.record()
-            loss = ce(cal(Xall[:bb]), yall[:bb])
+            loss = ce(cal(Xall[:bb].clone()), yall[:bb])
             e1.record()
             loss.backward()
             e2.record()
@@ -126,16 +132,16 @@ def main():
             ddp.register_comm_hook(state, cannikin_hook)
         return m, ddp, torch.optim.SGD(ddp.parameters(), lr=0.01, momentum=0.9)
 
-    def run_iter(ddp, opt, b_i, state=None):
-        X, y = Xall[:b_i], yall[:b_i]
+    def run_iter(ddp, model, opt, b_i, state=None):
+        X, y = Xall[:b_i].clone(), yall[:b_i]
         e0, e1, e2, e3 = E(), E(), E(), E()
+        model.bwd[1] = e2  # recorded at the end of backprop compute (before DDP's final wait)
         if state is not None:
             state.events = []
         e0.record()
         loss = ce(ddp(X), y)
         e1.record()
         loss.backward()
-        e2.record()
         opt.step()
         opt.zero_grad(set_to_none=True)
         e3.record()
@@ -151,7 +157,7 @@ def main():
     steps = []
     for it in range(args.iters + 3):
         dist.barrier()
-        e0, e1, e2, e3 = run_iter(ddp, opt, b_eq[rank])
+        e0, e1, e2, e3 = run_iter(ddp, model, opt, b_eq[rank])
         if it >= 3:
             steps.append(e0.elapsed_time(e3))
     t = torch.tensor([statistics.median(steps)], device="cuda", dtype=torch.float64)
@@ -175,7 +181,7 @@ def main():
         steps = []
         for it in range(args.iters + 2):
             dist.barrier()
-            e0, e1, e2, e3 = run_iter(ddp, opt, b[rank], state)
+            e0, e1, e2, e3 = run_iter(ddp, model, opt, b[rank], state)
             ctx.gns_stats()
             ev = state.events
             a_t = e0.elapsed_time(e1) * 1e-3
