@@ -60,7 +60,8 @@ class SlowResNet(nn.Module):
 
     def __init__(self):
         super().__init__()
-        r = torchvision.models.resnet18(num_classes=10)
+        # GroupNorm: per-sample normalisation, valid for any local batch (BatchNorm needs b_i > 1)
+        r = torchvision.models.resnet18(num_classes=10, norm_layer=lambda c: nn.GroupNorm(8, c))
         self.stages = nn.ModuleList([nn.Sequential(r.conv1, r.bn1, r.relu, r.maxpool), r.layer1,
                                      r.layer2, r.layer3, r.layer4,
                                      nn.Sequential(r.avgpool, nn.Flatten(), r.fc)])
@@ -80,7 +81,7 @@ class SlowResNet(nn.Module):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--B", type=int, default=256)
+    ap.add_argument("--B", type=int, default=512)
     ap.add_argument("--epochs", type=int, default=4)
     ap.add_argument("--iters", type=int, default=10)
     args = ap.parse_args()
