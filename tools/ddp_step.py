@@ -84,6 +84,7 @@ def main():
     ap.add_argument("--B", type=int, default=512)
     ap.add_argument("--epochs", type=int, default=4)
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--grid", type=int, default=24)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr = int(os.environ.get("LOCAL_RANK", rank))
@@ -168,7 +169,9 @@ def main():
     del ddp, opt, model
 
     # ---------------- Cannikin: comm hook + measured-model loop
-    ctx = ta.init_distributed_context(heap_bytes=64 << 20)
+    # a reduction that waits for a slower peer spins on its SMs: overlapping it with backprop needs
+    # a small grid (NCCL uses a few channels for the same reason)
+    ctx = ta.init_distributed_context(heap_bytes=64 << 20, grid=args.grid)
     state = CannikinHookState(ctx, 1.0 / world, timing=True)
     model, ddp, opt = build(state)
     an = ck.Analyzer(world)
@@ -213,6 +216,7 @@ def main():
     if out["predicted_ms"]:
         out["prediction_error"] = round(abs(out["predicted_ms"] - out["cannikin_ms"]) / out["cannikin_ms"], 4)
     out["buckets_per_step"] = len(state.events)
+    out["k3_grid"] = args.grid
     if rank == 0:
         print(json.dumps({"summary": out}), flush=True)
     dist.barrier()
