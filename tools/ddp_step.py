@@ -58,10 +58,11 @@ class _Delay(torch.autograd.Function):
 class SlowResNet(nn.Module):
     """ResNet-18 with per-stage forward/backward delays (seconds in self.fwd[0], self.bwd[0])."""
 
-    def __init__(self):
+    def __init__(self, arch="resnet18", classes=10):
         super().__init__()
         # GroupNorm: per-sample normalisation, valid for any local batch (BatchNorm needs b_i > 1)
-        r = torchvision.models.resnet18(num_classes=10, norm_layer=lambda c: nn.GroupNorm(8, c))
+        r = getattr(torchvision.models, arch)(num_classes=classes,
+                                              norm_layer=lambda c: nn.GroupNorm(8, c))
         self.stages = nn.ModuleList([nn.Sequential(r.conv1, r.bn1, r.relu, r.maxpool), r.layer1,
                                      r.layer2, r.layer3, r.layer4,
                                      nn.Sequential(r.avgpool, nn.Flatten(), r.fc)])
@@ -85,6 +86,8 @@ def main():
     ap.add_argument("--epochs", type=int, default=4)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--grid", type=int, default=24)
+    ap.add_argument("--model", default="resnet18", choices=["resnet18", "resnet50"])
+    ap.add_argument("--img", type=int, default=32)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr = int(os.environ.get("LOCAL_RANK", rank))
@@ -96,14 +99,15 @@ def main():
     ce = nn.CrossEntropyLoss()
     E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     gen = torch.Generator(device="cuda").manual_seed(1 + rank)
-    Xall = torch.randn(B, 3, 32, 32, device="cuda", generator=gen)
-    yall = torch.randint(0, 10, (B,), device="cuda", generator=gen)
+    classes = 10 if args.model == "resnet18" else 1000
+    Xall = torch.randn(B, 3, args.img, args.img, device="cuda", generator=gen)
+    yall = torch.randint(0, classes, (B,), device="cuda", generator=gen)
 
     # ---- calibrate this rank's real forward/backward time (no DDP, no delay) vs batch size
     torch.manual_seed(0)
-    cal = SlowResNet().cuda()
+    cal = SlowResNet(args.model, classes).cuda()
     xs, fa, fp = [], [], []
-    for bb in (8, 32, 64, 128, 192):
+    for bb in (8, 16, 32, 64, 96):
         bb = min(bb, B)
         for rep in range(4):
             e0, e1, e2 = E(), E(), E()
@@ -128,7 +132,7 @@ def main():
 
     def build(state):
         torch.manual_seed(0)
-        m = SlowResNet().cuda()
+        m = SlowResNet(args.model, classes).cuda()
         ddp = nn.parallel.DistributedDataParallel(m, device_ids=[lr])
         if state is not None:
             ddp.register_comm_hook(state, cannikin_hook)
@@ -150,7 +154,9 @@ def main():
         torch.cuda.synchronize()
         return e0, e1, e2, e3
 
-    out = {"mix": [bench.MIX[i % len(bench.MIX)] for i in range(world)], "B": B,
+    out = {"model": args.model, "img": args.img,
+           "params": sum(p.numel() for p in SlowResNet(args.model, classes).parameters()),
+           "mix": [bench.MIX[i % len(bench.MIX)] for i in range(world)], "B": B,
            "calibrated_ms_per_sample": round((qa + kp) * 1e3, 4)}
     # ---------------- equal-split DDP, stock NCCL average
     model, ddp, opt = build(None)
