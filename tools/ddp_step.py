@@ -177,7 +177,8 @@ def main():
     # ---------------- Cannikin: comm hook + measured-model loop
     # a reduction that waits for a slower peer spins on its SMs: overlapping it with backprop needs
     # a small grid (NCCL uses a few channels for the same reason)
-    ctx = ta.init_distributed_context(heap_bytes=64 << 20, grid=args.grid)
+    # DDP's first iteration reduces the whole gradient as one bucket: heap = gradient bytes
+    ctx = ta.init_distributed_context(heap_bytes=out["params"] * 4 + (1 << 20), grid=args.grid)
     state = CannikinHookState(ctx, 1.0 / world, timing=True)
     model, ddp, opt = build(state)
     an = ck.Analyzer(world)
