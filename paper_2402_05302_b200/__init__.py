@@ -89,6 +89,7 @@ SIGNATURES = {
     "cannikin_alloc_bucket": (_I, [_P, _Z, ctypes.POINTER(_P)]),
     "cannikin_free_bucket": (_I, [_P, _P]),
     "cannikin_weighted_allreduce": (_I, [_P, _P, _Z, _I, _D, _P]),
+    "cannikin_weighted_allreduce_nvls": (_I, [_P, _P, _P, _Z, _I, _D, _P]),
     "cannikin_gns_stats": (_I, [_P, _P, _DP, _DP]),
     "cannikin_gns_stats_async": (_I, [_P, _P, _P]),
     "cannikin_weighted_sum_local": (_I, [_P, ctypes.POINTER(_P), _I, _DP, _P, _Z, _I, _P, _P, _U, _P]),
@@ -190,6 +191,11 @@ class Context:
 
     def weighted_allreduce(self, ptr: int, n: int, dtype: int, r_i: float, stream=None):
         _check(lib().cannikin_weighted_allreduce(self._h, ptr, n, dtype, r_i, _stream(stream)))
+
+    def weighted_allreduce_nvls(self, ptr: int, mc_ptr: int, n: int, dtype: int, r_i: float,
+                                stream=None):
+        _check(lib().cannikin_weighted_allreduce_nvls(self._h, ptr, mc_ptr, n, dtype, r_i,
+                                                      _stream(stream)))
 
     def gns_stats(self, stream=None):
         out = (ctypes.c_double * self.world)()

@@ -342,3 +342,25 @@ extern "C" cannikin_status cannikin_trace(cannikin_ctx* ctx, uint64_t* out, int 
   if (g > 0) CK_CUDA(cudaMemcpy(out, ctx->ctrl->trace, sizeof(uint64_t) * 5 * g, cudaMemcpyDeviceToHost));
   return CANNIKIN_OK;
 }
+
+extern "C" cannikin_status cannikin_weighted_allreduce_nvls(cannikin_ctx* ctx, void* bucket,
+                                                            void* mc_bucket, size_t n,
+                                                            cannikin_dtype dt, double r_i,
+                                                            void* stream) {
+  if (!ctx) return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_nvls: ctx == NULL");
+  ctx->last_launches = 0;
+  if (dt != CANNIKIN_F32 && dt != CANNIKIN_BF16)
+    return fail(CANNIKIN_ERR_UNSUPPORTED, "weighted_allreduce_nvls: dtype %d", (int)dt);
+  if (ctx->world < 2) return fail(CANNIKIN_ERR_UNSUPPORTED, "weighted_allreduce_nvls: world < 2");
+  if (n == 0) return CANNIKIN_OK;
+  if (!bucket || !mc_bucket) return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_nvls: NULL pointer");
+  if (reinterpret_cast<uintptr_t>(bucket) % 16 || reinterpret_cast<uintptr_t>(mc_bucket) % 16)
+    return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_nvls: pointers not 16-byte aligned");
+  if ((n * elem_size(dt)) % 16)
+    return fail(CANNIKIN_ERR_UNSUPPORTED, "weighted_allreduce_nvls: n * sizeof(dt) must be a multiple of 16");
+  if (!(r_i == r_i)) return fail(CANNIKIN_ERR_DOMAIN, "weighted_allreduce_nvls: r_i is NaN");
+  CK_CUDA(cudaSetDevice(ctx->device));
+  CK_CUDA(cannikin::launch_nvls(ctx, bucket, mc_bucket, n, dt, r_i, S(stream)));
+  ctx->last_launches = 1;
+  return CANNIKIN_OK;
+}

@@ -80,3 +80,27 @@ def init_distributed_context(heap_bytes: int, grid: int = 0, group=None) -> Cont
     dev = torch.cuda.current_device()
     return Context(rank=rank, world=world, unique_id=obj[0], device=dev, heap_bytes=heap_bytes,
                    grid=grid)
+
+
+class McBucket:
+    """A symmetric, multicast-capable bucket from torch symmetric memory (device-memory plumbing)
+    for cannikin_weighted_allreduce_nvls.  `tensor` is this rank's copy."""
+
+    def __init__(self, numel: int, dtype: torch.dtype, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.tensor = symm_mem.empty(numel, dtype=dtype, device=torch.cuda.current_device())
+        g = group if group is not None else dist.group.WORLD
+        self.handle = symm_mem.rendezvous(self.tensor, g.group_name)
+        self.mc_ptr = int(self.handle.multicast_ptr)
+        if not self.mc_ptr:
+            raise RuntimeError("multicast (NVLS) memory is not available on this system")
+
+
+def weighted_allreduce_nvls(ctx: Context, mcb: "McBucket", r_i: float, view=None, stream=None):
+    """In place over mcb.tensor (or a slice `view` of it): Eq. 9 through NVSwitch multicast."""
+    t = mcb.tensor if view is None else view
+    off = t.data_ptr() - mcb.tensor.data_ptr()
+    ctx.weighted_allreduce_nvls(t.data_ptr(), mcb.mc_ptr + off, t.numel(), dtype_code(t.dtype),
+                                r_i, _cur(stream))
