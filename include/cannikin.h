@@ -118,11 +118,11 @@ cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* bucket, siz
  *   bucket    : this rank's copy of a symmetric, multicast-capable allocation (e.g. torch symmetric
  *               memory), n elements, 16-byte aligned, n * sizeof(dt) a multiple of 16; in place.
  *   mc_bucket : the multicast address of the same bytes (same layout on every rank).
- * Each rank scales its copy in place (r_i g_i rounded to dt -- one extra rounding per term for
- * bf16, reading Q28), the owner of each shard reads the in-switch sum
- * (multimem.ld_reduce, fp32 accumulation) and multicasts it back (multimem.st).  Same statistics
- * side effect as weighted_allreduce; |g|^2 is taken from the reduced values.  NVLink bytes per rank
- * and direction ~ (1 + 1/W) N s.  Errors: INVALID, UNSUPPORTED (dtype, ragged n, world < 2), CUDA. */
+ * Each rank scales its copy in place (r_i g_i rounded to fp32), the owner of each shard reads the
+ * in-switch fp32 sum (multimem.ld_reduce) and multicasts it back (multimem.st).  fp32 only: the
+ * switch's bf16 reduction misses the 1e-2 bf16 tolerance (reading Q28).  Same statistics side
+ * effect as weighted_allreduce; |g|^2 is taken from the reduced values.  NVLink bytes per rank and
+ * direction ~ (1 + 1/W) N s.  Errors: INVALID, UNSUPPORTED (dtype, ragged n, world < 2), CUDA. */
 cannikin_status cannikin_weighted_allreduce_nvls(cannikin_ctx* ctx, void* bucket, void* mc_bucket,
                                                  size_t n, cannikin_dtype dt, double r_i,
                                                  void* stream);

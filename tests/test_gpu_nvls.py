@@ -19,9 +19,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import mp_nvls_worker as W  # noqa: E402
 
 # fp32: the switch sums fp32 terms; the scaled terms r_j g_j are rounded to fp32 first
-# bf16: each term r_j g_j is rounded to bf16 before the in-switch sum (reading Q28), so the bound
-#       is the bf16 tolerance of BASELINE.json
-TOL = {"f32": 1e-5, "bf16": 1e-2}
+TOL = {"f32": 1e-5}
 
 
 def _port():
@@ -71,7 +69,8 @@ def test_nvls_parity(results, case):
             assert float(ranks[q]["glob" + sfx]) == glob
 
 
-def test_nvls_refuses_ragged(results):
+def test_nvls_refuses_ragged_and_bf16(results):
     world, d = results
     for r in range(world):
         assert str(np.load(os.path.join(d, f"rank{r}_ragged.npy"))[0]) == "UNSUPPORTED"
+        assert str(np.load(os.path.join(d, f"rank{r}_bf16.npy"))[0]) == "UNSUPPORTED"

@@ -51,6 +51,7 @@ def main():
     ap.add_argument("--variants", default="0", help="CANNIKIN_AR_DYN values")
     ap.add_argument("--sizes-mb", default="1,4,16,64,256,1024")
     ap.add_argument("--total", type=int, default=TOTAL)
+    ap.add_argument("--nvls", action="store_true", help="also time the NVLS kernel (fp32)")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr = int(os.environ.get("LOCAL_RANK", rank))
@@ -66,6 +67,9 @@ def main():
         os.environ["CANNIKIN_AR_DYN"] = var
         ctx = ta.init_distributed_context(heap_bytes=N * s, grid=grid)
         bucket = ta.bucket_tensor(ctx, N, tdt)
+        mcb = ta.McBucket(N, tdt) if args.nvls else None
+        if mcb is not None:
+            mcb.tensor.normal_()
         bucket.copy_(synth.device_gns_gradients(world, N, b, seed=0, dtype=args.dtype,
                                                 ranks=[rank])[0])
         for mb in [float(x) for x in args.sizes_mb.split(",")]:
@@ -87,6 +91,13 @@ def main():
             stats = torch.zeros(world + 1, dtype=torch.float64, device="cuda")
             t_ours = timed(ours, reps)
             t_nccl = timed(nccl, reps)
+            t_nvls = None
+            if args.nvls and args.dtype == "f32":
+                def nvls():
+                    for a, c in zip(cuts[:-1], cuts[1:]):
+                        ta.weighted_allreduce_nvls(ctx, mcb, r, view=mcb.tensor[a:c])
+                    ctx.gns_stats_async(stats.data_ptr(), torch.cuda.current_stream())
+                t_nvls = timed(nvls, reps)
             bus = lambda t: N * s / (t * 1e-3) * 2 * (world - 1) / world / 1e9  # noqa: E731
             if rank == 0:
                 print(json.dumps({"world": world, "dtype": args.dtype, "grid": grid, "variant": var,
@@ -94,7 +105,10 @@ def main():
                                   "ours_ms": round(t_ours, 4), "nccl_ms": round(t_nccl, 4),
                                   "ours_busbw": round(bus(t_ours), 1),
                                   "nccl_busbw": round(bus(t_nccl), 1),
-                                  "speedup_vs_nccl": round(t_nccl / t_ours, 3)}), flush=True)
+                                  "speedup_vs_nccl": round(t_nccl / t_ours, 3),
+                                  "nvls_ms": None if t_nvls is None else round(t_nvls, 4),
+                                  "nvls_busbw": None if t_nvls is None else round(bus(t_nvls), 1)}),
+                      flush=True)
         ta.free_bucket_tensor(ctx, bucket)
         del bucket
         dist.barrier()
