@@ -141,22 +141,21 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const McArgs a, int W) {
   {
     const size_t lo = a.L * a.rank, hi = (a.rank == W - 1) ? a.nvec : a.L * (a.rank + 1);
     size_t v = lo + (size_t)b * NT + tid;
-    for (; v + stride < hi; v += 2 * stride) {  // two reductions in flight per thread
-      const uint4 x0 = mc::ld_reduce(a.mc + v * 16, T());
-      const uint4 x1 = mc::ld_reduce(a.mc + (v + stride) * 16, T());
-      float f0[E], f1[E];
-      V::unpack(x0, f0);
-      V::unpack(x1, f1);
-      float s0 = 0.0f, s1 = 0.0f;
+    constexpr int R = 4;  // in-switch reductions in flight per thread
+    for (; v + (R - 1) * stride < hi; v += R * stride) {
+      uint4 x[R];
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        s0 = fmaf(f0[e], f0[e], s0);
-        s1 = fmaf(f1[e], f1[e], s1);
+      for (int u = 0; u < R; ++u) x[u] = mc::ld_reduce(a.mc + (v + u * stride) * 16, T());
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        float f[E];
+        V::unpack(x[u], f);
+        float s = 0.0f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) s = fmaf(f[e], f[e], s);
+        gsq += (double)s;
+        mc::st(a.mc + (v + u * stride) * 16, x[u], T());
       }
-      gsq += (double)s0;
-      gsq += (double)s1;
-      mc::st(a.mc + v * 16, x0, T());
-      mc::st(a.mc + (v + stride) * 16, x1, T());
     }
     for (; v < hi; v += stride) {
       const uint4 x = mc::ld_reduce(a.mc + v * 16, T());

@@ -21,18 +21,27 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank))))
     N = 64 << 20
     dyn = os.environ.get("CANNIKIN_AR_DYN", "0")
+    use_nvls = "--nvls" in sys.argv
+    mcb = ta.McBucket(N, torch.float32) if use_nvls else None
+    if mcb is not None:
+        mcb.tensor.normal_()
     ctx = ta.init_distributed_context(heap_bytes=N * 4)
     bucket = ta.bucket_tensor(ctx, N, torch.float32)
     bucket.normal_()
     for mb in [0.004, 0.0625, 1, 4, 16, 64, 256]:
         n = max(8, int(mb * 2**20) // 4)
+        def op():
+            if mcb is not None:
+                ta.weighted_allreduce_nvls(ctx, mcb, 1.0 / world, view=mcb.tensor[:n])
+            else:
+                ta.weighted_allreduce(ctx, bucket[:n], 1.0 / world)
         for _ in range(5):
-            ta.weighted_allreduce(ctx, bucket[:n], 1.0 / world)
+            op()
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        ta.weighted_allreduce(ctx, bucket[:n], 1.0 / world)
+        op()
         e1.record()
         torch.cuda.synchronize()
         tr = ctx.trace()
@@ -40,7 +49,7 @@ def main():
         ph = lambda k: [(t[k + 1] - t[k]) / 1e3 for t in tr]  # noqa: E731
         start_spread = (max(t[0] for t in tr) - t0) / 1e3
         last = max(tr, key=lambda t: t[4])
-        out = {"rank": rank, "dyn": dyn, "bucket_MB": mb, "ctas": len(tr), "event_us": round(e0.elapsed_time(e1) * 1e3, 1),
+        out = {"rank": rank, "nvls": use_nvls, "dyn": dyn, "bucket_MB": mb, "ctas": len(tr), "event_us": round(e0.elapsed_time(e1) * 1e3, 1),
                "start_spread_us": round(start_spread, 2),
                "entry_med": round(statistics.median(ph(0)), 2), "entry_max": round(max(ph(0)), 2),
                "data_med": round(statistics.median(ph(1)), 2), "data_max": round(max(ph(1)), 2),
