@@ -22,6 +22,8 @@ constexpr int kMaxEmu = CANNIKIN_MAX_EMULATED;
 struct Ctrl {
   uint64_t exit_[kMaxArBlocks][kMaxWorld];                   // [peer] "shard pushed" epoch
   uint64_t mid[kMaxArBlocks][kMaxWorld];                     // [peer] NVLS: "my piece is scaled"
+  uint64_t nv_exit[kMaxArBlocks][kMaxWorld];                 // [peer] NVLS: "my stores landed"
+  uint64_t nv_epoch;                                         // [local] NVLS call counter
   uint64_t rv_word[kMaxArBlocks][kMaxWorld];                 // [peer] entry: (float r_src, epoch32)
   uint64_t meta_word[kMaxArBlocks][kMaxWorld];               // [peer] entry: (bucket hash32, epoch32)
   double part[kMaxWorld][kMaxArChunks][kMaxWorld + 1];       // [peer] norm partials [src][row][j]

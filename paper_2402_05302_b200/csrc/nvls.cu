@@ -108,8 +108,10 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const McArgs a, int W) {
   auto nchunks_of = [&](int k) -> unsigned {
     return (unsigned)((shard_len(k) + a.chunk - 1) / a.chunk);
   };
+  // one epoch per call for every CTA (the mid barrier compares flags across CTA indices, so a
+  // per-CTA epoch -- K3's -- would diverge when the grid changes between calls)
   if (tid == 0) {
-    s_ep = a.ctrl->epoch[b] + 1;
+    s_ep = __ldcg(&a.ctrl->nv_epoch) + 1;
     a.ctrl->trace[b][0] = dev::globaltimer_ns();
   }
   __syncthreads();
@@ -229,12 +231,11 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const McArgs a, int W) {
   // ---- C. exit barrier, fixed-order final sum
   if (tid < W) {
     __threadfence_system();
-    dev::st_release_sys(&a.pctrl[tid]->exit_[b][a.rank], ep);
-    mc::wait_at_least(&a.ctrl->exit_[b][tid], ep, a.ctrl, a.timeout_ns, 5);
+    dev::st_release_sys(&a.pctrl[tid]->nv_exit[b][a.rank], ep);
+    mc::wait_at_least(&a.ctrl->nv_exit[b][tid], ep, a.ctrl, a.timeout_ns, 5);
   }
   __syncthreads();
   if (tid == 0) {
-    a.ctrl->epoch[b] = ep;
     a.ctrl->trace[b][3] = dev::globaltimer_ns();
     __threadfence();
     s_last = (atomicAdd(&a.ctrl->ticket_ar, 1u) == gridDim.x - 1);
@@ -257,6 +258,7 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const McArgs a, int W) {
     for (int j = 0; j <= W; ++j) a.ctrl->stats[j] += tot[j];
     a.ctrl->ticket_ar = 0u;
     a.ctrl->ar_counter = 0u;
+    a.ctrl->nv_epoch = ep;  // every CTA read the old value at its start
     a.ctrl->trace[b][4] = dev::globaltimer_ns();
     a.ctrl->trace_grid = G;
   }
