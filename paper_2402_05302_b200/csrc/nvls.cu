@@ -31,7 +31,6 @@ struct McArgs {
   Ctrl* ctrl;
   size_t nvec;              // 16-byte vectors (the NVLS path needs whole vectors)
   size_t L;                 // vectors per shard (last shard: nvec - (W-1) L)
-  size_t chunk;             // phase-B chunk (vectors)
   uint64_t meta;
   uint64_t timeout_ns;
   float r_me;
@@ -101,13 +100,9 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const McArgs a, int W) {
   __shared__ double red[32 * (kMaxWorld + 1)];
   __shared__ double s_part[2];
   __shared__ uint64_t s_ep;
-  __shared__ unsigned s_chunk[2];
   __shared__ bool s_last;
   const int b = blockIdx.x, tid = threadIdx.x, G = gridDim.x, NT = blockDim.x;
   auto shard_len = [&](int k) -> size_t { return (k == W - 1) ? a.nvec - a.L * (W - 1) : a.L; };
-  auto nchunks_of = [&](int k) -> unsigned {
-    return (unsigned)((shard_len(k) + a.chunk - 1) / a.chunk);
-  };
   // one epoch per call for every CTA (the mid barrier compares flags across CTA indices, so a
   // per-CTA epoch -- K3's -- would diverge when the grid changes between calls)
   if (tid == 0) {
@@ -154,43 +149,27 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const McArgs a, int W) {
       dev::st16(a.local + v * 16, V::pack(g));
     }
   }
-  double vals[2] = {lsq, 0.0};
-  dev::block_sum<2>(vals, red);
-  if (tid == 0) s_part[0] = vals[0];
+  // publish "piece b scaled" to every peer (release: the switch reads my copy) and wait for
+  // piece b of every rank: the piece of my shard that CTA b reduces below is scaled everywhere
   __syncthreads();
-  // publish "piece b scaled" (release: the switch reads my copy) + this CTA's |g_me|^2 row
   if (tid < W) {
-    Ctrl* pc = a.pctrl[tid];
-    for (int j = 0; j <= W; ++j)
-      dev::st_relaxed_sys_f64(&pc->part[a.rank][b][j], j == a.rank ? s_part[0] : 0.0);
     __threadfence_system();
-    dev::st_release_sys(&pc->mid[b][a.rank], ep);
-  }
-  // phase B chunks may lie in any piece: wait until every CTA of every rank has scaled its piece
-  for (int i = tid; i < G * W; i += NT)
-    mc::wait_at_least(&a.ctrl->mid[i / W][i % W], ep, a.ctrl, a.timeout_ns, 4);
-  if (tid == 0) {
-    s_chunk[0] = atomicAdd(&a.ctrl->ar_counter, 1u);
-    s_chunk[1] = atomicAdd(&a.ctrl->ar_counter, 1u);
+    dev::st_release_sys(&a.pctrl[tid]->mid[b][a.rank], ep);
+    mc::wait_at_least(&a.ctrl->mid[b][tid], ep, a.ctrl, a.timeout_ns, 4);
   }
   __syncthreads();
   if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
 
-  // ---- B. chunks of my shard, claimed dynamically: in-switch sum, |g|^2, multicast store.
-  // Chunk c's |g|^2 is row G + c of the partial tables (independent of which CTA did it).
-  const unsigned my_chunks = nchunks_of(a.rank);
-  const size_t my_lo = a.L * a.rank, my_hi = my_lo + shard_len(a.rank);
-  for (unsigned it = 0;; ++it) {
-    const unsigned c = s_chunk[it & 1];
-    if (c >= my_chunks) break;
-    const size_t v0 = my_lo + (size_t)c * a.chunk;
-    const size_t v1 = (v0 + a.chunk < my_hi) ? v0 + a.chunk : my_hi;
-    double gsq = 0.0;
-    size_t v = v0 + tid;
-    for (; v + (R - 1) * NT < v1; v += R * NT) {
+  // ---- B. CTA b's piece of my shard (grid-stride, the interleaving the switch serves best):
+  // in-switch sum, |g|^2, multicast store to every copy
+  double gsq = 0.0;
+  {
+    const size_t lo = a.L * a.rank, hi = lo + shard_len(a.rank);
+    size_t v = lo + (size_t)b * NT + tid;
+    for (; v + (R - 1) * stride < hi; v += R * stride) {
       uint4 x[R];
 #pragma unroll
-      for (int u = 0; u < R; ++u) x[u] = mc::ld_reduce(a.mc + (v + u * NT) * 16, T());
+      for (int u = 0; u < R; ++u) x[u] = mc::ld_reduce(a.mc + (v + u * stride) * 16, T());
 #pragma unroll
       for (int u = 0; u < R; ++u) {
         float f[E];
@@ -199,10 +178,10 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const McArgs a, int W) {
 #pragma unroll
         for (int e = 0; e < E; ++e) sq = fmaf(f[e], f[e], sq);
         gsq += (double)sq;
-        mc::st(a.mc + (v + u * NT) * 16, x[u], T());
+        mc::st(a.mc + (v + u * stride) * 16, x[u], T());
       }
     }
-    for (; v < v1; v += NT) {
+    for (; v < hi; v += stride) {
       const uint4 x = mc::ld_reduce(a.mc + v * 16, T());
       float f[E];
       V::unpack(x, f);
@@ -212,20 +191,23 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const McArgs a, int W) {
       gsq += (double)sq;
       mc::st(a.mc + v * 16, x, T());
     }
-    double cv[1] = {gsq};
-    dev::block_sum<1>(cv, red);
-    if (tid == 0) {
-      s_part[1] = cv[0];
-      s_chunk[it & 1] = atomicAdd(&a.ctrl->ar_counter, 1u);
-    }
-    __syncthreads();
-    if (tid < W) {
-      Ctrl* pc = a.pctrl[tid];
-      for (int j = 0; j <= W; ++j)
-        dev::st_relaxed_sys_f64(&pc->part[a.rank][G + c][j], j == W ? s_part[1] : 0.0);
-    }
   }
   if (tid == 0) a.ctrl->trace[b][2] = dev::globaltimer_ns();
+  // row [me][b]: this CTA's |g_me|^2 piece in column me, its |g|^2 piece in column W
+  double vals[2] = {lsq, gsq};
+  dev::block_sum<2>(vals, red);
+  if (tid == 0) {
+    s_part[0] = vals[0];
+    s_part[1] = vals[1];
+  }
+  __syncthreads();
+  if (tid < W) {
+    Ctrl* pc = a.pctrl[tid];
+    for (int j = 0; j <= W; ++j) {
+      const double x = (j == a.rank) ? s_part[0] : (j == W ? s_part[1] : 0.0);
+      dev::st_relaxed_sys_f64(&pc->part[a.rank][b][j], x);
+    }
+  }
   __syncthreads();
 
   // ---- C. exit barrier, fixed-order final sum
@@ -246,18 +228,15 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const McArgs a, int W) {
   double tot[kMaxWorld + 1];
 #pragma unroll
   for (int j = 0; j <= kMaxWorld; ++j) tot[j] = 0.0;
-  for (int src = 0; src < W; ++src) {
-    const int rows = G + (int)nchunks_of(src);
-    for (int i = tid; i < rows; i += NT) {
-      const double* row = &a.ctrl->part[src][i][0];
-      for (int j = 0; j <= W; ++j) tot[j] += __ldcg(row + j);
-    }
+  for (int i = tid; i < W * G; i += NT) {
+    const int src = i / G, cta = i - src * G;
+    const double* row = &a.ctrl->part[src][cta][0];
+    for (int j = 0; j <= W; ++j) tot[j] += __ldcg(row + j);
   }
   dev::block_sum<kMaxWorld + 1>(tot, red);
   if (tid == 0) {
     for (int j = 0; j <= W; ++j) a.ctrl->stats[j] += tot[j];
     a.ctrl->ticket_ar = 0u;
-    a.ctrl->ar_counter = 0u;
     a.ctrl->nv_epoch = ep;  // every CTA read the old value at its start
     a.ctrl->trace[b][4] = dev::globaltimer_ns();
     a.ctrl->trace_grid = G;
@@ -281,13 +260,6 @@ cudaError_t launch_nvls(cannikin_ctx* ctx, void* local, void* mcp, size_t n, can
   int grid = ctx->grid_ar;
   const size_t want = (L + 1023) / 1024;
   if (want < (size_t)grid) grid = want < 1 ? 1 : (int)want;
-  // phase B: ~4 chunks per CTA, at least 4 vectors per thread, rows G + chunks <= kMaxArChunks
-  size_t chunk = (L + (size_t)grid * 4 - 1) / ((size_t)grid * 4);
-  if (chunk > 512 * 16) chunk = 512 * 16;
-  const size_t need = (L + 512 * 8 + (kMaxArChunks - kMaxArBlocks) - 2) / (kMaxArChunks - kMaxArBlocks - 1);
-  if (need > chunk) chunk = need;
-  chunk = (chunk + 2047) / 2048 * 2048;
-  a.chunk = chunk;
   uint64_t meta = (uint64_t)n * 0xC2B2AE3D27D4EB4Full ^ ((uint64_t)grid << 8) ^ (uint64_t)dt ^ 0x6E766C73ull;
   a.meta = meta;
   a.timeout_ns = ctx->spin_timeout_ns;
