@@ -163,6 +163,44 @@ def hetero_step_compare(ctx, bucket, N, s, rank, world, B, steps, dist, ta, ck, 
                     "gamma = 1/buckets; max over ranks"}
 
 
+def nvls_sidecar(ctx, N, rank, world, r_i, steps, dist, ta, torch):
+    """fp32 weighted all-reduce of N elements through NVSwitch multicast (K6) next to the two-shot
+    kernel (K3) on the same bytes: kernel time (CUDA events, max over ranks) and busbw."""
+    s = 4
+    mcb = ta.McBucket(N, torch.float32)
+    mcb.tensor.normal_()
+    heap_bytes_needed = N * s
+    res = {"elements": N, "dtype": "f32"}
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / steps], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    t6 = timed(lambda: ta.weighted_allreduce_nvls(ctx, mcb, r_i))
+    ctx.gns_stats()
+    res["k6_ms"] = round(t6, 4)
+    res["k6_busbw"] = round(N * s / (t6 * 1e-3) * 2 * (world - 1) / world / 1e9, 1)
+    if ctx.world > 1 and heap_bytes_needed <= 2 * N * s:
+        t3 = timed(lambda: ta.weighted_allreduce(ctx, mcb.tensor, r_i))  # staged through the heap
+        ctx.gns_stats()
+        res["k3_staged_ms"] = round(t3, 4)
+    res["note"] = ("NVLS moves ~(1+1/n) N s per direction vs the two-shot's 2(n-1)/n N s, plus a "
+                   "local scaling pass; fp32 only")
+    del mcb
+    return res
+
+
 def esize(dtype):
     return 4 if dtype == "f32" else 2
 
@@ -328,6 +366,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of a CUDA graph")
     ap.add_argument("--no-hetero", action="store_true", help="skip the step-time-vs-DDP comparison")
+    ap.add_argument("--no-nvls", action="store_true", help="skip the NVLS fp32 sidecar")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -525,6 +564,14 @@ def main():
         ddp = {"ms_per_allreduce": round(float(dm.item()), 4),
                "note": "ncclAllReduce(avg) of the same bucket, equal-split DDP semantics (Eq. 2)"}
 
+    # ---- NVSwitch-multicast (NVLS) variant, fp32 sidecar on the same element count (K6)
+    nvls = None
+    if world > 1 and not args.no_nvls:
+        try:
+            nvls = nvls_sidecar(ctx, N, rank, world, r[rank], args.steps, dist, ta, torch)
+        except Exception as e:  # multicast unavailable on this system
+            nvls = {"unavailable": str(e)[:200]}
+
     hetero = None
     if world > 1 and not args.no_hetero:
         hetero = hetero_step_compare(ctx, bucket, N, s, rank, world, max(B, world), args.steps,
@@ -598,7 +645,7 @@ def main():
                        "cuda_graph": graphs is not None,
                        "host_overlap": "host half of step t overlaps device half of step t+1"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "ddp_baseline": ddp,
-            "step_vs_ddp": hetero,
+            "step_vs_ddp": hetero, "nvls_f32": nvls,
             "gpu_launches": launches_per_step() * args.steps,
             "clocks": clk.summary(),
         }
