@@ -169,7 +169,6 @@ def nvls_sidecar(ctx, N, rank, world, r_i, steps, dist, ta, torch):
     s = 4
     mcb = ta.McBucket(N, torch.float32)
     mcb.tensor.normal_()
-    heap_bytes_needed = N * s
     res = {"elements": N, "dtype": "f32"}
 
     def timed(fn):
@@ -191,10 +190,6 @@ def nvls_sidecar(ctx, N, rank, world, r_i, steps, dist, ta, torch):
     ctx.gns_stats()
     res["k6_ms"] = round(t6, 4)
     res["k6_busbw"] = round(N * s / (t6 * 1e-3) * 2 * (world - 1) / world / 1e9, 1)
-    if ctx.world > 1 and heap_bytes_needed <= 2 * N * s:
-        t3 = timed(lambda: ta.weighted_allreduce(ctx, mcb.tensor, r_i))  # staged through the heap
-        ctx.gns_stats()
-        res["k3_staged_ms"] = round(t3, 4)
     res["note"] = ("NVLS moves ~(1+1/n) N s per direction vs the two-shot's 2(n-1)/n N s, plus a "
                    "local scaling pass; fp32 only")
     del mcb
