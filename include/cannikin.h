@@ -135,8 +135,9 @@ cannikin_status cannikin_weighted_allreduce_nvls(cannikin_ctx* ctx, void* bucket
 cannikin_status cannikin_gns_stats(cannikin_ctx* ctx, void* stream, double* out_local_sq,
                                    double* out_global_sq);
 
-/* Stream-ordered variant: copies the (world+1) accumulated doubles [local_sq..., global_sq] to the
- * DEVICE buffer d_out and resets the accumulator, without host synchronisation. */
+/* Stream-ordered variant: copies the (world+1) accumulated doubles [local_sq..., global_sq] to
+ * d_out (device memory, or pinned host memory) and resets the accumulator, without host
+ * synchronisation. */
 cannikin_status cannikin_gns_stats_async(cannikin_ctx* ctx, double* d_out, void* stream);
 
 /* Single-GPU fused pass over n_ranks emulated ranks (the 1-B200 metric kernel; reading of
@@ -145,8 +146,8 @@ cannikin_status cannikin_gns_stats_async(cannikin_ctx* ctx, double* d_out, void*
  *   r     : host array of n_ranks shares r_j
  *   out   : device pointer, n elements of `dt`:  out = sum_j r_j in[j]   (fp32 accumulate, rank order)
  *           out may alias in[j] (in-place).
- *   d_local_sq  : device pointer, n_ranks doubles: |in[j]|^2
- *   d_global_sq : device pointer, 1 double: |out|^2 taken from the fp32 accumulator (reading Q2)
+ *   d_local_sq  : n_ranks doubles |in[j]|^2 -- device memory or pinned (device-mapped) host memory
+ *   d_global_sq : 1 double |out|^2 from the fp32 accumulator (reading Q2), same memory kinds
  *   flags & CANNIKIN_ACCUMULATE: add to d_local_sq/d_global_sq instead of overwriting (multi-bucket)
  *   flags & CANNIKIN_LOCAL_LDG / CANNIKIN_LOCAL_TMA: force the 128-bit-load or the TMA-bulk-staged
  *         kernel variant (identical output bits; norms equal up to fp64 summation grouping);

@@ -264,7 +264,7 @@ extern "C" cannikin_status cannikin_gns_stats_async(cannikin_ctx* ctx, double* d
   if (!ctx || !d_out) return fail(CANNIKIN_ERR_INVALID, "gns_stats_async: NULL argument");
   CK_CUDA(cudaSetDevice(ctx->device));
   const size_t bytes = sizeof(double) * (ctx->world + 1);
-  CK_CUDA(cudaMemcpyAsync(d_out, ctx->ctrl->stats, bytes, cudaMemcpyDeviceToDevice, S(stream)));
+  CK_CUDA(cudaMemcpyAsync(d_out, ctx->ctrl->stats, bytes, cudaMemcpyDefault, S(stream)));
   CK_CUDA(cudaMemsetAsync(ctx->ctrl->stats, 0, bytes, S(stream)));
   return CANNIKIN_OK;
 }

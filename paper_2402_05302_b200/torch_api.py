@@ -57,6 +57,7 @@ def weighted_sum_local(ctx: Context, grads, r, out: torch.Tensor, local_sq: torc
     """Emulated ranks on one GPU: out <- sum_j r_j grads[j]; local_sq[j] <- |grads[j]|^2;
     global_sq <- |out|^2 (float64 device tensors)."""
     dt = dtype_code(out.dtype)
+    # local_sq / global_sq: float64 device tensors or pinned (device-mapped) host tensors
     for g in grads:
         assert g.is_cuda and g.is_contiguous() and g.dtype == out.dtype and g.numel() == out.numel()
     assert local_sq.dtype == torch.float64 and global_sq.dtype == torch.float64
