@@ -90,6 +90,11 @@ extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world
   ctx->user_off = ctx->ctrl_bytes;
   ctx->scratch_off = ctx->user_off + ctx->heap_bytes;
   ctx->total_bytes = ctx->scratch_off + (world > 1 ? ctx->heap_bytes : 0);
+  if (const char* t = std::getenv("CANNIKIN_AR_PUSH")) ctx->ar_push = std::atoi(t) != 0;
+  if (world > 1 && ctx->ar_push) {  // staging for the push variant: W slots of the largest shard
+    ctx->stage_off = ctx->total_bytes;
+    ctx->total_bytes += align_up(ctx->heap_bytes + (size_t)world * world * 64 * 16 + 4096, 4096);
+  }
   ce = cudaMalloc(&ctx->base, ctx->total_bytes);
   if (ce == cudaSuccess) ce = cudaMemset(ctx->base, 0, ctx->ctrl_bytes);
   if (ce == cudaSuccess) ce = cudaMallocHost(&ctx->h_stats, sizeof(double) * (cannikin::kMaxWorld + 1));

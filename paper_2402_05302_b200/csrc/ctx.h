@@ -26,6 +26,7 @@ struct Ctrl {
   uint64_t nv_epoch;                                         // [local] NVLS call counter
   uint64_t rv_word[kMaxArBlocks][kMaxWorld];                 // [peer] entry: (float r_src, epoch32)
   uint64_t meta_word[kMaxArBlocks][kMaxWorld];               // [peer] entry: (bucket hash32, epoch32)
+  uint64_t pmid[kMaxArBlocks][kMaxWorld];                    // [peer] push variant: (r_src, epoch32)
   double part[kMaxWorld][kMaxArChunks][kMaxWorld + 1];       // [peer] norm partials [src][row][j]
   uint64_t epoch[kMaxArBlocks];                              // [local] per-block epoch counter
   unsigned ticket_ar;                                        // [local] last-block-done ticket
@@ -44,6 +45,7 @@ struct cannikin_ctx {
   int rank = 0, world = 1, device = 0;
   int grid_ar = 148;
   int ar_dyn = -1;          // CANNIKIN_AR_DYN=0|1 forces static/dynamic chunks; -1 = by size
+  bool ar_push = false;     // CANNIKIN_AR_PUSH=1: all-write (push) two-shot variant
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2
   bool local_tma = false;   // default variant of K2 (CANNIKIN_K2_IMPL=tma|ldg)
   int local_nt = 256;       // CANNIKIN_K2_NT: CTA size of K2 (256, or one big CTA per SM)
@@ -51,7 +53,7 @@ struct cannikin_ctx {
   size_t heap_bytes = 0;
   // local allocation = [Ctrl | user heap (heap_bytes) | scratch (heap_bytes)]
   char* base = nullptr;
-  size_t ctrl_bytes = 0, user_off = 0, scratch_off = 0, total_bytes = 0;
+  size_t ctrl_bytes = 0, user_off = 0, scratch_off = 0, stage_off = 0, total_bytes = 0;
   char* peer_base[cannikin::kMaxWorld] = {};
   cannikin::Ctrl* ctrl = nullptr;
   void* nccl_comm = nullptr;  // ncclComm_t

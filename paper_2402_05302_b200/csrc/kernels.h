@@ -34,6 +34,8 @@ cudaError_t launch_wsum_local_tma(cannikin_ctx* ctx, const void* const* in, int 
 cudaError_t launch_emulate(double seconds, cudaStream_t st);
 cudaError_t launch_nvls(cannikin_ctx* ctx, void* local, void* mc, size_t n, cannikin_dtype dt,
                         double r_i, cudaStream_t st);
+cudaError_t launch_twoshot_push(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt,
+                                double r_i, cudaStream_t st);
 cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
                            cudaStream_t st);
 

@@ -440,10 +440,293 @@ static cudaError_t dispatch_w(int W, const ArArgs& a, int grid, bool dyn, cudaSt
   }
 }
 
+
+// ============================================================================================
+// Push variant of K3 (CANNIKIN_AR_PUSH=1): every NVLink transfer is a write.
+//   1. scatter: CTA b of rank j writes its piece b of every other shard S_k into slot j of rank
+//      k's staging area (reads local, writes remote) and accumulates |g_j|^2 on the way;
+//   2. mid barrier: epoch-tagged (r_j | epoch) words with release semantics -- also carries r_j,
+//      so no entry barrier is needed (the staging and the buckets are free once the previous
+//      call's exit barrier passed);
+//   3. reduce: CTA b of rank k sums its piece of S_k from its own bucket and the W-1 staging
+//      slots (all LOCAL reads), fp32 in rank order, |g|^2, and pushes the result into every
+//      peer's bucket;
+//   4. partial rows [me][b] = {|g_me|^2 piece, |g|^2 piece}, exit barrier, fixed-order final sum.
+// NVLink bytes per rank and direction: 2 (W-1)/W N s, as the pull variant, but no read requests.
+// ============================================================================================
+struct PushArgs {
+  char* bucket[kMaxWorld];   // this bucket in every rank's mapping
+  char* stage[kMaxWorld];    // staging area of every rank (mapped)
+  Ctrl* pctrl[kMaxWorld];
+  Ctrl* ctrl;
+  size_t nvec, n, L;         // vectors, elements, vectors per shard (last: nvec - (W-1) L)
+  size_t slot_vec;           // staging slot size in vectors (>= the largest shard)
+  uint64_t meta;
+  uint64_t timeout_ns;
+  float r_me;
+  int rank;
+};
+
+template <typename T, int W, int U>
+__global__ void __launch_bounds__(512, 1) twoshot_push_kernel(const PushArgs a) {
+  using V = dev::Vec<T>;
+  constexpr int E = V::E;
+  __shared__ double red[32 * (kMaxWorld + 1)];
+  __shared__ double s_part[2];
+  __shared__ float s_r[W];
+  __shared__ uint64_t s_ep;
+  __shared__ bool s_last;
+  const int b = blockIdx.x, tid = threadIdx.x, G = gridDim.x, NT = blockDim.x;
+  auto shard_lo = [&](int k) -> size_t { return a.L * k; };
+  auto shard_hi = [&](int k) -> size_t { return (k == W - 1) ? a.nvec : a.L * (k + 1); };
+  if (tid == 0) {
+    s_ep = a.ctrl->epoch[b] + 1;
+    a.ctrl->trace[b][0] = dev::globaltimer_ns();
+  }
+  __syncthreads();
+  const uint64_t ep = s_ep;
+  const uint32_t e32 = (uint32_t)ep;
+  const size_t stride = (size_t)G * NT;
+
+  // ---- 1. scatter my pieces of the other shards into their owners' staging slot `rank`
+  double lsq = 0.0;
+  const char* mine = a.bucket[a.rank];
+  for (int kk = 1; kk < W; ++kk) {
+    const int k = (a.rank + kk) % W;  // staggered start: not every rank hits the same peer first
+    const size_t lo = shard_lo(k), hi = shard_hi(k);
+    char* dst = a.stage[k] + ((size_t)a.rank * a.slot_vec - lo) * 16;
+    size_t v = lo + (size_t)b * NT + tid;
+    for (; v + (U - 1) * stride < hi; v += U * stride) {
+      uint4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = dev::ld16(mine + (v + u * stride) * 16);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        float g[E];
+        V::unpack(x[u], g);
+        float sq = 0.0f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) sq = fmaf(g[e], g[e], sq);
+        lsq += (double)sq;
+        dev::st16(dst + (v + u * stride) * 16, x[u]);
+      }
+    }
+    for (; v < hi; v += stride) {
+      const uint4 x = dev::ld16(mine + v * 16);
+      float g[E];
+      V::unpack(x, g);
+      float sq = 0.0f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) sq = fmaf(g[e], g[e], sq);
+      lsq += (double)sq;
+      dev::st16(dst + v * 16, x);
+    }
+  }
+  // own ragged tail (< one vector) -> |g_me|^2, read before the mid barrier: the last rank writes
+  // the reduced tail into every bucket only after CTA 0 of every rank has passed it
+  if (b == 0) {
+    const size_t e = a.nvec * E + tid;
+    if (e < a.n) {
+      const float own = V::load1(mine + e * sizeof(T));
+      lsq += (double)(own * own);
+    }
+  }
+  __syncthreads();  // every scatter store of this CTA has been issued
+
+  // ---- 2. mid barrier: (r_rank | epoch) with release, to every peer; r_j from every peer
+  const uint32_t m32 = (uint32_t)(a.meta ^ (a.meta >> 32));
+  if (tid < W) {
+    Ctrl* pc = a.pctrl[tid];
+    __threadfence_system();
+    dev::st_relaxed_sys_u64(&pc->meta_word[b][a.rank], ((uint64_t)m32 << 32) | e32);
+    dev::st_release_sys(&pc->pmid[b][a.rank],
+                        ((uint64_t)__float_as_uint(a.r_me) << 32) | e32);
+    uint64_t w;
+    {
+      uint64_t t0 = 0;
+      unsigned it = 0;
+      while ((int32_t)((uint32_t)(w = dev::ld_acquire_sys(&a.ctrl->pmid[b][tid])) - e32) < 0) {
+        if ((++it & 1023u) == 0u) {
+          const uint64_t now = dev::globaltimer_ns();
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > a.timeout_ns) { atomicExch(&a.ctrl->error_code, 6); __trap(); }
+        }
+      }
+    }
+    s_r[tid] = __uint_as_float((uint32_t)(w >> 32));
+    const uint64_t wm = spin_word(&a.ctrl->meta_word[b][tid], e32, a.ctrl, a.timeout_ns, 2);
+    if ((uint32_t)(wm >> 32) != m32) {
+      atomicExch(&a.ctrl->error_code, 2);
+      __trap();
+    }
+  }
+  __syncthreads();
+  if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
+
+  // ---- 3. reduce my shard's piece from local memory, push the result to every peer
+  float r[W];
+  char* dstb[W];
+  const char* src[W];
+  const size_t lo = shard_lo(a.rank), hi = shard_hi(a.rank);
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    r[j] = s_r[j];
+    dstb[j] = a.bucket[j];
+    src[j] = (j == a.rank) ? a.bucket[a.rank] + lo * 16
+                           : a.stage[a.rank] + (size_t)j * a.slot_vec * 16;
+  }
+  double gsq = 0.0;
+  for (size_t v = lo + (size_t)b * NT + tid; v < hi; v += stride) {
+    const size_t rel = v - lo;
+    uint4 x[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) x[j] = dev::ld16(src[j] + rel * 16);
+    float acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      float g[E];
+      V::unpack(x[j], g);
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] = fmaf(r[j], g[e], acc[e]);
+      if (j == a.rank) {
+        float sq = 0.0f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) sq = fmaf(g[e], g[e], sq);
+        lsq += (double)sq;
+      }
+    }
+    float gs = 0.0f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) gs = fmaf(acc[e], acc[e], gs);
+    gsq += (double)gs;
+    const uint4 y = V::pack(acc);
+#pragma unroll
+    for (int jj = 0; jj < W; ++jj) {
+      const int j = (a.rank + jj) % W;
+      dev::st16(dstb[j] + v * 16, y);
+    }
+  }
+  // ragged element tail: the last rank's CTA 0 reduces it straight from the peers' buckets
+  // (after the mid barrier every rank's tail elements are still unchanged source data)
+  if (b == 0) {
+    const size_t e = a.nvec * E + tid;
+    if (e < a.n) {
+      if (a.rank == W - 1) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          const float g = V::load1(dstb[j] + e * sizeof(T));
+          acc = fmaf(r[j], g, acc);
+        }
+        gsq += (double)(acc * acc);
+#pragma unroll
+        for (int j = 0; j < W; ++j) V::store1(dstb[j] + e * sizeof(T), acc);
+      }
+    }
+  }
+  if (tid == 0) a.ctrl->trace[b][2] = dev::globaltimer_ns();
+
+  // ---- 4. partial rows, exit barrier, final sum
+  double vals[2] = {lsq, gsq};
+  dev::block_sum<2>(vals, red);
+  if (tid == 0) {
+    s_part[0] = vals[0];
+    s_part[1] = vals[1];
+  }
+  __syncthreads();
+  if (tid < W) {
+    Ctrl* pc = a.pctrl[tid];
+#pragma unroll
+    for (int j = 0; j <= W; ++j) {
+      const double x = (j == a.rank) ? s_part[0] : (j == W ? s_part[1] : 0.0);
+      dev::st_relaxed_sys_f64(&pc->part[a.rank][b][j], x);
+    }
+    __threadfence_system();
+    dev::st_release_sys(&pc->exit_[b][a.rank], ep);
+    spin_until(&a.ctrl->exit_[b][tid], ep, a.ctrl, a.timeout_ns, 3);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    a.ctrl->epoch[b] = ep;
+    a.ctrl->trace[b][3] = dev::globaltimer_ns();
+    __threadfence();
+    s_last = (atomicAdd(&a.ctrl->ticket_ar, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double tot[W + 1];
+#pragma unroll
+  for (int j = 0; j <= W; ++j) tot[j] = 0.0;
+  for (int i = tid; i < W * G; i += NT) {
+    const int sr = i / G, cta = i - sr * G;
+    const double* row = &a.ctrl->part[sr][cta][0];
+#pragma unroll
+    for (int j = 0; j <= W; ++j) tot[j] += __ldcg(row + j);
+  }
+  dev::block_sum<W + 1>(tot, red);
+  if (tid == 0) {
+#pragma unroll
+    for (int j = 0; j <= W; ++j) a.ctrl->stats[j] += tot[j];
+    a.ctrl->ticket_ar = 0u;
+    a.ctrl->trace[b][4] = dev::globaltimer_ns();
+    a.ctrl->trace_grid = G;
+  }
+}
+
+template <typename T>
+static cudaError_t dispatch_push(int W, const PushArgs& a, int grid, cudaStream_t st) {
+  switch (W) {
+#define CANNIKIN_CASE(K) \
+  case K:                \
+    twoshot_push_kernel<T, K, K <= 2 ? 4 : 2><<<grid, kArThreads, 0, st>>>(a); \
+    return cudaGetLastError();
+    CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5) CANNIKIN_CASE(6)
+    CANNIKIN_CASE(7) CANNIKIN_CASE(8)
+#undef CANNIKIN_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_twoshot_push(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt,
+                                double r_i, cudaStream_t st) {
+  const int W = ctx->world;
+  PushArgs a{};
+  for (int j = 0; j < W; ++j) {
+    a.bucket[j] = ctx->peer_base[j] + off;
+    a.stage[j] = ctx->peer_base[j] + ctx->stage_off;
+    a.pctrl[j] = reinterpret_cast<Ctrl*>(ctx->peer_base[j]);
+  }
+  a.ctrl = ctx->ctrl;
+  const size_t esz = dt == CANNIKIN_F32 ? 4 : 2;
+  a.n = n;
+  a.nvec = n * esz / 16;
+  size_t L = a.nvec / W;
+  L -= L % 64;
+  a.L = L;
+  a.slot_vec = a.nvec - L * (size_t)(W - 1);  // the largest shard (the last rank's)
+  int grid = ctx->grid_ar;
+  const size_t want = (L + (size_t)kArThreads * 2 - 1) / ((size_t)kArThreads * 2);
+  if (want < (size_t)grid) grid = want < 1 ? 1 : (int)want;
+  uint64_t meta = (uint64_t)off * 0x9E3779B97F4A7C15ull;
+  meta ^= (uint64_t)n * 0xC2B2AE3D27D4EB4Full;
+  meta ^= ((uint64_t)grid << 8) ^ (uint64_t)dt ^ 0x70757368ull;
+  a.meta = meta;
+  a.timeout_ns = ctx->spin_timeout_ns;
+  a.r_me = (float)r_i;
+  a.rank = ctx->rank;
+  if (dt == CANNIKIN_F32) return dispatch_push<float>(W, a, grid, st);
+  return dispatch_push<__nv_bfloat16>(W, a, grid, st);
+}
+
 // Launch K3 on the bucket at byte offset `off` of every rank's allocation.
 cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
                            cudaStream_t st) {
   const int W = ctx->world;
+  if (ctx->ar_push && ctx->stage_off) return launch_twoshot_push(ctx, off, n, dt, r_i, st);
   ArArgs a{};
   for (int j = 0; j < W; ++j) {
     a.bucket[j] = ctx->peer_base[j] + off;

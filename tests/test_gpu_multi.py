@@ -30,7 +30,7 @@ def _port():
     return p
 
 
-@pytest.fixture(scope="module", params=["static", "dyn"])
+@pytest.fixture(scope="module", params=["static", "dyn", "push"])
 def results(request):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -40,7 +40,8 @@ def results(request):
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
            os.path.join(os.path.dirname(__file__), "mp_allreduce_worker.py"), "--out", d]
     env = dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000",
-               CANNIKIN_AR_DYN="1" if request.param == "dyn" else "0")
+               CANNIKIN_AR_DYN="1" if request.param == "dyn" else "0",
+               CANNIKIN_AR_PUSH="1" if request.param == "push" else "0")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     return world, d

@@ -48,7 +48,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--grids", default="0")
-    ap.add_argument("--variants", default="0", help="CANNIKIN_AR_DYN values")
+    ap.add_argument("--variants", default="0", help="CANNIKIN_AR_DYN values, or 'push'")
     ap.add_argument("--sizes-mb", default="1,4,16,64,256,1024")
     ap.add_argument("--total", type=int, default=TOTAL)
     ap.add_argument("--nvls", action="store_true", help="also time the NVLS kernel (fp32)")
@@ -64,7 +64,8 @@ def main():
     r = b[rank] / sum(b)
     combos = [(int(g), v) for g in args.grids.split(",") for v in args.variants.split(",")]
     for grid, var in combos:
-        os.environ["CANNIKIN_AR_DYN"] = var
+        os.environ["CANNIKIN_AR_PUSH"] = "1" if var == "push" else "0"
+        os.environ["CANNIKIN_AR_DYN"] = "0" if var == "push" else var
         ctx = ta.init_distributed_context(heap_bytes=N * s, grid=grid)
         bucket = ta.bucket_tensor(ctx, N, tdt)
         mcb = ta.McBucket(N, tdt) if args.nvls else None
