@@ -90,8 +90,9 @@ extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world
   ctx->user_off = ctx->ctrl_bytes;
   ctx->scratch_off = ctx->user_off + ctx->heap_bytes;
   ctx->total_bytes = ctx->scratch_off + (world > 1 ? ctx->heap_bytes : 0);
-  if (const char* t = std::getenv("CANNIKIN_AR_PUSH")) ctx->ar_push = std::atoi(t) != 0;
-  if (world > 1 && ctx->ar_push) {  // staging for the push variant: W slots of the largest shard
+  if (const char* t = std::getenv("CANNIKIN_AR_PUSH")) ctx->ar_push = std::atoi(t) != 0 ? 1 : 0;
+  // staging for the push variant (W slots of the largest shard): by default from 4 ranks up
+  if (world > 1 && (ctx->ar_push == 1 || (ctx->ar_push < 0 && world >= 4))) {
     ctx->stage_off = ctx->total_bytes;
     ctx->total_bytes += align_up(ctx->heap_bytes + (size_t)world * world * 64 * 16 + 4096, 4096);
   }

@@ -45,7 +45,7 @@ struct cannikin_ctx {
   int rank = 0, world = 1, device = 0;
   int grid_ar = 148;
   int ar_dyn = -1;          // CANNIKIN_AR_DYN=0|1 forces static/dynamic chunks; -1 = by size
-  bool ar_push = false;     // CANNIKIN_AR_PUSH=1: all-write (push) two-shot variant
+  int ar_push = -1;         // CANNIKIN_AR_PUSH=0|1 forces pull/push two-shot; -1 = by size
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2
   bool local_tma = false;   // default variant of K2 (CANNIKIN_K2_IMPL=tma|ldg)
   int local_nt = 256;       // CANNIKIN_K2_NT: CTA size of K2 (256, or one big CTA per SM)

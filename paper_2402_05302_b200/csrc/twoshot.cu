@@ -726,7 +726,13 @@ cudaError_t launch_twoshot_push(cannikin_ctx* ctx, size_t off, size_t n, canniki
 cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
                            cudaStream_t st) {
   const int W = ctx->world;
-  if (ctx->ar_push && ctx->stage_off) return launch_twoshot_push(ctx, off, n, dt, r_i, st);
+  {
+    // push (all-write) pays for large shards from 4 ranks up (+5% at W = 4, 256 MB-1 GB buckets;
+    // profiles/r01/k3_pull_dyn_push_n4.jsonl); pull is better for small buckets and W = 2
+    const size_t shard_bytes = n * (dt == CANNIKIN_F32 ? 4 : 2) / W;
+    const bool push = ctx->ar_push == 1 || (ctx->ar_push < 0 && W >= 4 && shard_bytes >= (32ull << 20));
+    if (push && ctx->stage_off) return launch_twoshot_push(ctx, off, n, dt, r_i, st);
+  }
   ArArgs a{};
   for (int j = 0; j < W; ++j) {
     a.bucket[j] = ctx->peer_base[j] + off;
