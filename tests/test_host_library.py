@@ -220,3 +220,31 @@ def test_gns_estimate_flags_and_errors():
     with pytest.raises(ck.CannikinError) as e:
         ck.gns_estimate([float("nan"), 1.0], 1.0, [3, 4])
     assert e.value.name == "DOMAIN"
+
+
+def test_analyzer_api_errors():
+    with pytest.raises(ck.CannikinError):
+        ck.Analyzer(0)
+    an = ck.Analyzer(2)
+    with pytest.raises(ck.CannikinError) as e:
+        an.observe(5, 0, 10, 0.1, 0.1, 0.1, 0.0, 0.0)          # node out of range
+    assert e.value.name == "INVALID"
+    with pytest.raises(ck.CannikinError) as e:
+        an.observe(0, 0, 10, -0.1, 0.1, 0.1, 0.0, 0.0)         # negative time
+    assert e.value.name == "DOMAIN"
+    with pytest.raises(ck.CannikinError) as e:
+        an.models()                                            # no data yet
+    assert e.value.name == "SINGULAR"
+    with pytest.raises(ck.CannikinError) as e:
+        an.plan(1)                                             # B < n
+    assert e.value.name == "INVALID"
+    assert an.plan(9, cap=[3, 9])["b"] == [3, 6]               # caps respected in the even split
+    with pytest.raises(ck.CannikinError) as e:
+        an.plan(9, cap=[3, 3])
+    assert e.value.name == "INFEASIBLE"
+
+
+def test_emulate_compute_domain():
+    with pytest.raises(ck.CannikinError) as e:
+        ck.emulate_compute(-1.0)
+    assert e.value.name == "DOMAIN"
