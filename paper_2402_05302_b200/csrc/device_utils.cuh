@@ -109,19 +109,6 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem) {
   __syncthreads();
 }
 
-// Sum of `count` doubles at base[i*stride] (i = 0..count-1) over the whole block, fixed order:
-// thread t sums i = t, t+T, t+2T, ... then the block butterfly/warp-order reduction.
-// Loads go to L2 (.cg): the values were written by other CTAs / other GPUs during this launch.
-// Result valid in thread 0.
-__device__ __forceinline__ double block_strided_sum(const double* base, int count, int stride,
-                                                    double* smem) {
-  double s = 0.0;
-  for (int i = threadIdx.x; i < count; i += blockDim.x) s += __ldcg(base + (size_t)i * stride);
-  double v[1] = {s};
-  block_sum<1>(v, smem);
-  return v[0];
-}
-
 // NV column sums of a row-major table base[i*row_stride + j] (i = 0..count-1, j = 0..NV-1) in ONE
 // pass over the block: thread t accumulates rows t, t+T, t+2T, ... for all columns (independent
 // loads, pipelined), then one butterfly/warp-order reduction.  Fixed order => deterministic.

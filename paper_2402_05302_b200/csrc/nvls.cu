@@ -66,12 +66,6 @@ __device__ __forceinline__ void st(void* p, const uint4& v, __nv_bfloat16) {
                : "memory");
 }
 
-__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
 __device__ __forceinline__ void wait_at_least(const uint64_t* flag, uint64_t ep, Ctrl* ctrl,
                                               uint64_t timeout_ns, int code) {
   uint64_t t0 = 0;
