@@ -459,12 +459,12 @@ def main():
 
     kernel_ms = []
 
+    # the host half of a step (GNS estimate + EMA + next split) is one native call
+    control = ck.ControlStep(b, models, COMM, B)
+
     def host_part(k, record=False):
         ready[k].synchronize()
-        st = stats_h[k].tolist()
-        if n >= 2:
-            ck.gns_estimate(st[:n], st[n], b)
-        ck.opt_split(models, COMM, B)
+        control(stats_h[k].data_ptr())
         if record:
             kernel_ms.extend(a.elapsed_time(c) for a, c in evs[k])
 

@@ -325,6 +325,16 @@ cannikin_status cannikin_analyzer_choose_batch(cannikin_analyzer* an, const int6
                                                int64_t* B_out, int64_t* b_out, double* t_pred,
                                                int* full_recompute);
 
+/* The host half of one training step in one call (replicated on every rank from identical
+ * statistics): stats[n+1] = [|g_0|^2 .. |g_{n-1}|^2, |g|^2] and b[n] -> cannikin_gns_estimate into
+ * *gns_out (n >= 2), the EMA update (ema may be NULL), and, if nodes/cm/b_next are given, the
+ * opt_split of B_next into b_next[n] with its Eq. 7 time in *t_next.  Errors: those of the parts. */
+cannikin_status cannikin_control_step(const double* stats, const int64_t* b, int n,
+                                      cannikin_gns_ema* ema, const cannikin_node_model* nodes,
+                                      const cannikin_comm_model* cm, int64_t B_next,
+                                      cannikin_gns_result* gns_out, int64_t* b_next,
+                                      double* t_next);
+
 #ifdef __cplusplus
 }
 #endif

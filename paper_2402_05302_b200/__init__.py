@@ -114,6 +114,9 @@ SIGNATURES = {
     "cannikin_choose_batch": (_I, [ctypes.POINTER(_NodeModel), _I, ctypes.POINTER(_CommModel), _LP,
                                    _I, _L, _D, _LP, _DP, _DP]),
     "cannikin_analyzer_choose_batch": (_I, [_P, _LP, _I, _L, _D, _LP, _LP, _DP, _IP]),
+    "cannikin_control_step": (_I, [_DP, _LP, _I, ctypes.POINTER(_GnsEma), ctypes.POINTER(_NodeModel),
+                                   ctypes.POINTER(_CommModel), _L, ctypes.POINTER(_GnsResult), _LP,
+                                   _DP]),
 }
 
 
@@ -380,3 +383,36 @@ def choose_batch(nodes, comm, candidates, B0: int, B_noise: float):
     _check(lib().cannikin_choose_batch(arr, len(nodes), ctypes.byref(cm), _i64(candidates), k,
                                        int(B0), float(B_noise), ctypes.byref(Bo), T, G))
     return {"B": Bo.value, "T": list(T), "goodput": list(G)}
+
+
+class ControlStep:
+    """The host half of a training step in one native call: GNS estimate + EMA + next split.
+    Buffers are prepared once; call(stats_ptr) with the address of n+1 float64 statistics
+    (e.g. a pinned host tensor's data_ptr())."""
+
+    def __init__(self, b, nodes, comm, B_next: int, decay: float = 0.9):
+        self.n = len(b)
+        self._b = _i64(b)
+        self._nodes, self._cm = _models(nodes, comm)
+        self._ema = _GnsEma(0.0, 0.0, float(decay), 0)
+        self._res = _GnsResult()
+        self._bn = (ctypes.c_int64 * self.n)()
+        self._t = ctypes.c_double()
+        self.B_next = int(B_next)
+        self._f = lib().cannikin_control_step
+
+    def __call__(self, stats_ptr: int):
+        st = self._f(ctypes.cast(stats_ptr, _DP), self._b, self.n, ctypes.byref(self._ema),
+                     self._nodes, ctypes.byref(self._cm), self.B_next, ctypes.byref(self._res),
+                     self._bn, ctypes.byref(self._t))
+        if st:
+            _check(st)
+        return self._res.B_noise
+
+    @property
+    def result(self):
+        n = self.n
+        r = self._res
+        return {"G2": r.G2, "trS": r.trS, "B_noise": r.B_noise, "wG": list(r.wG[:n]),
+                "wS": list(r.wS[:n]), "b_next": list(self._bn), "T_next": self._t.value,
+                "ema_B_noise": self._ema.trS / self._ema.G2 if self._ema.count else float("nan")}

@@ -413,3 +413,30 @@ extern "C" cannikin_status cannikin_analyzer_choose_batch(cannikin_analyzer* an,
   if (full_recompute) *full_recompute = recompute;
   return CANNIKIN_OK;
 }
+
+// One host control step (the host half of a training step, replicated on every rank): the GNS
+// estimate from the step's norm statistics, the EMA update, and the split for the next step.
+extern "C" cannikin_status cannikin_control_step(const double* stats, const int64_t* b, int n,
+                                                 cannikin_gns_ema* ema,
+                                                 const cannikin_node_model* nodes,
+                                                 const cannikin_comm_model* cm, int64_t B_next,
+                                                 cannikin_gns_result* gns_out, int64_t* b_next,
+                                                 double* t_next) {
+  if (!stats || !b || !gns_out) return fail(CANNIKIN_ERR_INVALID, "control_step: NULL argument");
+  cannikin_status st = CANNIKIN_OK;
+  if (n >= 2) {
+    st = cannikin_gns_estimate(stats, stats[n], b, n, gns_out);
+    if (st != CANNIKIN_OK) return st;
+    if (ema) {
+      st = cannikin_gns_ema_update(ema, gns_out->G2, gns_out->trS);
+      if (st != CANNIKIN_OK) return st;
+    }
+  }
+  if (nodes && cm && b_next) {
+    double t[2];
+    st = cannikin_opt_split(nodes, n, cm, B_next, nullptr, nullptr, 0, b_next, nullptr, t, nullptr);
+    if (st != CANNIKIN_OK) return st;
+    if (t_next) *t_next = t[1];
+  }
+  return CANNIKIN_OK;
+}

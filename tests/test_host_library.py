@@ -248,3 +248,25 @@ def test_emulate_compute_domain():
     with pytest.raises(ck.CannikinError) as e:
         ck.emulate_compute(-1.0)
     assert e.value.name == "DOMAIN"
+
+
+def test_control_step_matches_parts():
+    """cannikin_control_step == gns_estimate + EMA + opt_split called separately."""
+    import ctypes
+    rng = np.random.default_rng(9)
+    for _ in range(20):
+        n = int(rng.integers(2, 8))
+        b = [int(x) for x in rng.integers(1, 100, size=n)]
+        gsq = float(rng.uniform(0.5, 2.0))
+        lsq = [gsq + float(rng.uniform(0.0, 3.0)) for _ in range(n)]
+        nodes, comm = synth.random_cluster(rng, n)
+        Bn = int(rng.integers(n, 500))
+        stats = (ctypes.c_double * (n + 1))(*(lsq + [gsq]))
+        c = ck.ControlStep(b, nodes, comm, Bn)
+        c(ctypes.addressof(stats))
+        r = c.result
+        e = ck.gns_estimate(lsq, gsq, b)
+        assert r["G2"] == e["G2"] and r["trS"] == e["trS"] and r["wS"] == e["wS"]
+        assert r["b_next"] == ck.opt_split(nodes, comm, Bn)["b"]
+        if e["G2"] > 0:
+            assert math.isclose(r["ema_B_noise"], e["trS"] / e["G2"], rel_tol=1e-15)
