@@ -258,3 +258,32 @@ def test_no_out_of_bounds_writes(ctx, dtype, N, variant):
         assert torch.all(bb[:pad] == -7.0) and torch.all(bb[pad + N:] == -7.0)
     assert torch.all(stats[:2] == -5.0) and torch.all(stats[6:] == -5.0)
     del esz
+
+
+def test_full_size_c5_sampled(ctx):
+    """configs[4]'s 355M fp32 gradient at full size on one GPU (3 emulated ranks): sampled
+    elements against the oracle one by one, norms against the oracle over the whole vectors."""
+    N, nr = 354_823_168, 3
+    b = [5, 17, 40]
+    gs = synth.device_gns_gradients(nr, N, b, seed=2, dtype="f32")
+    r = agg.ratios(b)
+    out = torch.empty(N, dtype=torch.float32, device="cuda")
+    local = torch.zeros(nr, dtype=torch.float64, device="cuda")
+    glob = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ta.weighted_sum_local(ctx, gs, r, out, local, glob)
+    torch.cuda.synchronize()
+    idx = torch.from_numpy(np.random.default_rng(1).choice(N, 200_000, replace=False)).cuda()
+    samp = [agg.to_f64(g[idx].cpu().numpy(), "f32") for g in gs]
+    ref = agg.weighted_sum(samp, r)
+    got = out[idx].cpu().numpy().astype(np.float64)
+    scale = np.maximum(agg.elementwise_scale(samp, r), 1e-30)
+    assert np.max(np.abs(got - ref) / scale) <= 1e-5
+    lsum, gsum = np.zeros(nr), 0.0
+    chunk = 20_000_000
+    for a in range(0, N, chunk):
+        parts = [agg.to_f64(g[a:a + chunk].cpu().numpy(), "f32") for g in gs]
+        for j in range(nr):
+            lsum[j] += agg.sq_norm(parts[j])
+        gsum += agg.sq_norm(agg.weighted_sum(parts, r))
+    assert np.allclose(local.cpu().numpy(), lsum, rtol=1e-4)
+    assert abs(float(glob.cpu()[0]) - gsum) <= 1e-4 * gsum
