@@ -253,6 +253,9 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+BIDIR_WRITE_GBS = 690.8  # profiles/r01/nvlink_bw_n2.jsonl (write2, best grid)
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -540,8 +543,14 @@ def main():
         roof = {"bound": "nvlink", "achieved": round(busbw, 1), "peak": 770.0, "unit": "GB/s",
                 "frac": round(busbw / 770.0, 4),
                 "peak_kind": "measured peer copy per GPU per direction (B200_PROFILING.md); 900 nominal",
-                "kernel": "twoshot_kernel (K3)", "kernel_ms": round(kmean, 4),
-                "traffic": ncu_traffic(f"{args.config}_w{n}_{cfg['dtype']}")}
+                "kernel": "K3 two-shot (pull / dynamic / push variant by size)",
+                "kernel_ms": round(kmean, 4),
+                "traffic": ncu_traffic(f"{args.config}_w{n}_{cfg['dtype']}"),
+                # an all-reduce loads BOTH directions at once; the same SM-driven copy with both
+                # directions busy peaks lower than the one-way 770 (tools/nvlink_bw.cu,
+                # profiles/r01/nvlink_bw_n2.jsonl: 690.8 writes, 642.7 reads, 656.9 mixed)
+                "bidir_ceiling": {"peak": BIDIR_WRITE_GBS, "frac": round(busbw / BIDIR_WRITE_GBS, 4),
+                                  "kind": "measured two-GPU bidirectional peer writes per direction"}}
 
     # ---- DDP baseline (equal split, NCCL average) on the same bucket, N > 1
     ddp = None

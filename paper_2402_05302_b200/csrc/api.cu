@@ -90,6 +90,8 @@ extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world
   ctx->user_off = ctx->ctrl_bytes;
   ctx->scratch_off = ctx->user_off + ctx->heap_bytes;
   ctx->total_bytes = ctx->scratch_off + (world > 1 ? ctx->heap_bytes : 0);
+  if (const char* t = std::getenv("CANNIKIN_OS_VPT")) ctx->os_vpt = std::atoi(t) >= 2 ? 2 : 1;
+  if (const char* t = std::getenv("CANNIKIN_AR_ONESHOT")) ctx->ar_oneshot = std::atoi(t) != 0;
   if (const char* t = std::getenv("CANNIKIN_AR_PUSH")) ctx->ar_push = std::atoi(t) != 0 ? 1 : 0;
   // staging for the push variant (W slots of the largest shard): by default from 4 ranks up
   if (world > 1 && (ctx->ar_push == 1 || (ctx->ar_push < 0 && world >= 4))) {
@@ -254,9 +256,7 @@ extern "C" cannikin_status cannikin_gns_stats(cannikin_ctx* ctx, void* stream,
     return fail(CANNIKIN_ERR_INVALID, "gns_stats: NULL argument");
   CK_CUDA(cudaSetDevice(ctx->device));
   const int W = ctx->world;
-  const size_t bytes = sizeof(double) * (W + 1);
-  CK_CUDA(cudaMemcpyAsync(ctx->h_stats, ctx->ctrl->stats, bytes, cudaMemcpyDeviceToHost, S(stream)));
-  CK_CUDA(cudaMemsetAsync(ctx->ctrl->stats, 0, bytes, S(stream)));
+  CK_CUDA(cannikin::launch_stats_finalize(ctx, ctx->h_stats, S(stream)));
   CK_CUDA(cudaStreamSynchronize(S(stream)));
   int code = 0;
   CK_CUDA(cudaMemcpy(&code, &ctx->ctrl->error_code, sizeof code, cudaMemcpyDeviceToHost));
@@ -269,9 +269,7 @@ extern "C" cannikin_status cannikin_gns_stats(cannikin_ctx* ctx, void* stream,
 extern "C" cannikin_status cannikin_gns_stats_async(cannikin_ctx* ctx, double* d_out, void* stream) {
   if (!ctx || !d_out) return fail(CANNIKIN_ERR_INVALID, "gns_stats_async: NULL argument");
   CK_CUDA(cudaSetDevice(ctx->device));
-  const size_t bytes = sizeof(double) * (ctx->world + 1);
-  CK_CUDA(cudaMemcpyAsync(d_out, ctx->ctrl->stats, bytes, cudaMemcpyDefault, S(stream)));
-  CK_CUDA(cudaMemsetAsync(ctx->ctrl->stats, 0, bytes, S(stream)));
+  CK_CUDA(cannikin::launch_stats_finalize(ctx, d_out, S(stream)));
   return CANNIKIN_OK;
 }
 

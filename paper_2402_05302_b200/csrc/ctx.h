@@ -34,6 +34,7 @@ struct Ctrl {
   unsigned ar_counter;                                       // [local] dynamic two-shot chunk counter
   int error_code;                                            // [local] protocol error (trap reason)
   double stats[kMaxWorld + 1];                               // [local] accumulated |g_j|^2, |g|^2
+  double cta_acc[kMaxArBlocks][kMaxWorld + 1];               // [local] per-CTA running stats
   uint64_t trace[kMaxLocalBlocks][5];                        // [local] per-CTA timeline (ns)
   int trace_grid;                                            // [local] CTAs of the last traced kernel
   double local_part[kMaxLocalBlocks][kMaxEmu + 1];           // [local] emulated-kernel partials
@@ -46,6 +47,8 @@ struct cannikin_ctx {
   int grid_ar = 148;
   int ar_dyn = -1;          // CANNIKIN_AR_DYN=0|1 forces static/dynamic chunks; -1 = by size
   int ar_push = -1;         // CANNIKIN_AR_PUSH=0|1 forces pull/push two-shot; -1 = by size
+  int os_vpt = 2;           // CANNIKIN_OS_VPT=1|2: one-shot vectors per thread (sets its grid)
+  int ar_oneshot = -1;      // CANNIKIN_AR_ONESHOT=0|1 forbids/prefers one-shot; -1 = by size
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2
   bool local_tma = false;   // default variant of K2 (CANNIKIN_K2_IMPL=tma|ldg)
   int local_nt = 256;       // CANNIKIN_K2_NT: CTA size of K2 (256, or one big CTA per SM)

@@ -38,5 +38,6 @@ cudaError_t launch_twoshot_push(cannikin_ctx* ctx, size_t off, size_t n, canniki
                                 double r_i, cudaStream_t st);
 cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
                            cudaStream_t st);
+cudaError_t launch_stats_finalize(cannikin_ctx* ctx, double* out, cudaStream_t st);
 
 }  // namespace cannikin

@@ -11,8 +11,9 @@
 //      every peer's bucket at the same place, so all ranks end with identical bits;
 //   3. the CTA's W+1 norm partials are pushed into every peer's partial pad (row a4);
 //   4. exit barrier: "my shard and partials have landed at every peer";
-//   5. the last CTA to finish sums all ranks' partials in fixed (rank, CTA) order and adds them
-//      to the ctx accumulator -- identical bits on every rank (K5).
+//   5. CTA b adds the W partial rows of CTA b (all ranks) in rank order to its running row;
+//      cannikin_gns_stats sums the rows in CTA order -- identical bits on every rank (K5), and no
+//      cross-CTA step inside the kernel.
 // Only rank k ever reads or writes region S_k of any bucket, so two barriers suffice.  Flags are
 // monotonically increasing epochs (no reset), making back-to-back buckets and CUDA-graph replay
 // safe.  NVLink bytes per rank and direction: 2 (W-1)/W N s -- the ring all-reduce's volume
@@ -149,7 +150,6 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
   __shared__ double s_part[W + 1];
   __shared__ float s_r[W];
   __shared__ uint64_t s_ep;
-  __shared__ bool s_last;
   const int b = blockIdx.x, tid = threadIdx.x;
 
   if (tid == 0) {
@@ -234,36 +234,22 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
     spin_until(&a.ctrl->exit_[b][tid], ep, a.ctrl, a.timeout_ns, 3);
   }
   __syncthreads();
+  // ---- 5. CTA b now holds every rank's partial row b: add them, in rank order, to its own
+  // running row (the same sequence of additions on every rank -> identical bits; no cross-CTA
+  // step on the critical path).  cannikin_gns_stats sums the rows in fixed order.
   if (tid == 0) {
     a.ctrl->epoch[b] = ep;
     a.ctrl->trace[b][3] = dev::globaltimer_ns();
-    __threadfence();
-    s_last = (atomicAdd(&a.ctrl->ticket_ar, 1u) == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-
-  // ---- 5. fixed-order total over (rank, CTA) -> ctx accumulator
-  // one pass: thread t sums rows (src, cta) = i, i + T, ... of the W x G partial table in
-  // ascending order for all W+1 columns, then the fixed block tree
-  double tot[W + 1];
+    double* acc = a.ctrl->cta_acc[b];
 #pragma unroll
-  for (int j = 0; j <= W; ++j) tot[j] = 0.0;
-  const int G = gridDim.x;
-  for (int i = tid; i < W * G; i += blockDim.x) {
-    const int src = i / G, cta = i - src * G;
-    const double* row = &a.ctrl->part[src][cta][0];
+    for (int j = 0; j <= W; ++j) {
+      double t = 0.0;
 #pragma unroll
-    for (int j = 0; j <= W; ++j) tot[j] += __ldcg(row + j);
-  }
-  dev::block_sum<W + 1>(tot, red);
-  if (tid == 0) {
-#pragma unroll
-    for (int j = 0; j <= W; ++j) a.ctrl->stats[j] += tot[j];
-    a.ctrl->ticket_ar = 0u;
+      for (int src = 0; src < W; ++src) t += __ldcg(&a.ctrl->part[src][b][j]);
+      acc[j] = __ldcg(&acc[j]) + t;
+    }
     a.ctrl->trace[b][4] = dev::globaltimer_ns();
-    a.ctrl->trace_grid = G;
+    if (b == 0) a.ctrl->trace_grid = gridDim.x;
   }
 }
 
@@ -440,6 +426,186 @@ static cudaError_t dispatch_w(int W, const ArArgs& a, int grid, bool dyn, cudaSt
   }
 }
 
+
+// ============================================================================================
+// One-shot variant of K3 for small buckets (below ~W x 256 KiB): every rank reads the
+// WHOLE bucket of every peer and sums in the same fixed rank order, so every rank computes the
+// identical g (and identical norm partials) by itself -- no all-gather, no partial exchange.
+//   0. entry barrier (as the two-shot): r_j and the bucket identity;
+//   1. CTA b loads its (same on every rank) vectors of all W buckets, reduces in fp32 in rank
+//      order and keeps the result in registers (<= MV vectors per thread), with |g_j|^2 and |g|^2;
+//   2. "done reading" barrier: CTA b tells CTA b of every peer that it has read its part of the
+//      peer's bucket, and waits for the same from every peer;
+//   3. CTA b writes its result into its OWN bucket only (local stores) -- all of that region has
+//      been read by every peer;
+//   4. CTA b adds its partials to its running statistics row (the same on every rank).
+// Nobody writes into a peer's memory except the flag words, so no exit barrier is needed.
+// NVLink bytes per rank, inbound: (W-1) N s (reads); the latency is one entry handshake, one read
+// round trip and one flag handshake.
+// ============================================================================================
+template <typename T, int W, int MV>
+__global__ void __launch_bounds__(kArThreads, 1) oneshot_kernel(const ArArgs a) {
+  using V = dev::Vec<T>;
+  constexpr int E = V::E;
+  __shared__ double red[32 * (W + 1)];
+  __shared__ float s_r[W];
+  __shared__ uint64_t s_ep;
+  const int b = blockIdx.x, tid = threadIdx.x;
+
+  if (tid == 0) {
+    s_ep = a.ctrl->epoch[b] + 1;
+    a.ctrl->trace[b][0] = dev::globaltimer_ns();
+  }
+  __syncthreads();
+  const uint64_t ep = s_ep;
+  if (tid < W) entry_barrier_thread<W>(a, b, ep, s_r);
+  __syncthreads();
+  if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
+
+  float r[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) r[j] = s_r[j];
+  double lsq[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) lsq[j] = 0.0;
+  double gsq = 0.0;
+
+  // ---- 1. loads of every bucket (all issued before any use), fp32 reduction in rank order
+  const size_t stride = (size_t)gridDim.x * kArThreads;
+  const size_t v0 = (size_t)b * kArThreads + tid;
+  uint4 x[MV][W];
+#pragma unroll
+  for (int u = 0; u < MV; ++u) {
+    const size_t v = v0 + u * stride;
+    if (v < a.nvec) {
+#pragma unroll
+      for (int j = 0; j < W; ++j) x[u][j] = dev::ld16(a.bucket[j] + v * 16);
+    }
+  }
+  uint4 y[MV];
+#pragma unroll
+  for (int u = 0; u < MV; ++u) {
+    if (v0 + u * stride < a.nvec) {
+      float acc[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] = 0.0f;
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        float g[E];
+        V::unpack(x[u][j], g);
+        float sq = 0.0f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          acc[e] = fmaf(r[j], g[e], acc[e]);
+          sq = fmaf(g[e], g[e], sq);
+        }
+        lsq[j] += (double)sq;
+      }
+      float gs = 0.0f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) gs = fmaf(acc[e], acc[e], gs);
+      gsq += (double)gs;
+      y[u] = V::pack(acc);
+    }
+  }
+  // ragged tail (< one vector of elements): CTA 0 of every rank
+  const size_t et = a.nvec * E + tid;
+  const bool has_t = b == 0 && tid < E && et < a.n;
+  float acc_t = 0.0f;
+  if (has_t) {
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const float g = V::load1(a.bucket[j] + et * sizeof(T));
+      acc_t = fmaf(r[j], g, acc_t);
+      lsq[j] += (double)(g * g);
+    }
+    gsq += (double)(acc_t * acc_t);
+  }
+  double vals[W + 1];
+#pragma unroll
+  for (int j = 0; j < W; ++j) vals[j] = lsq[j];
+  vals[W] = gsq;
+  dev::block_sum<W + 1>(vals, red);  // ends with __syncthreads: every load of the CTA is consumed
+  if (tid == 0) a.ctrl->trace[b][2] = dev::globaltimer_ns();
+
+  // ---- 2. done-reading barrier with CTA b of every peer
+  if (tid < W) {
+    dev::st_release_sys(&a.pctrl[tid]->exit_[b][a.rank], ep);
+    spin_until(&a.ctrl->exit_[b][tid], ep, a.ctrl, a.timeout_ns, 3);
+  }
+  __syncthreads();
+
+  // ---- 3. local stores of the result
+  char* own = a.bucket[a.rank];
+#pragma unroll
+  for (int u = 0; u < MV; ++u) {
+    const size_t v = v0 + u * stride;
+    if (v < a.nvec) dev::st16(own + v * 16, y[u]);
+  }
+  if (has_t) V::store1(own + et * sizeof(T), acc_t);
+
+  // ---- 4. add the CTA's partials to its running row (identical on every rank)
+  if (tid == 0) {
+    double* acc = a.ctrl->cta_acc[b];
+#pragma unroll
+    for (int j = 0; j <= W; ++j) acc[j] = __ldcg(&acc[j]) + vals[j];
+    a.ctrl->epoch[b] = ep;
+    a.ctrl->trace[b][3] = a.ctrl->trace[b][4] = dev::globaltimer_ns();
+    if (b == 0) a.ctrl->trace_grid = gridDim.x;
+  }
+}
+
+constexpr int kOneShotMV = 2;  // result vectors held per thread across the done-reading barrier
+
+template <typename T>
+static cudaError_t dispatch_oneshot(int W, const ArArgs& a, int grid, cudaStream_t st) {
+  switch (W) {
+#define CANNIKIN_CASE(K) \
+  case K:                \
+    oneshot_kernel<T, K, kOneShotMV><<<grid, kArThreads, 0, st>>>(a); \
+    return cudaGetLastError();
+    CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5) CANNIKIN_CASE(6)
+    CANNIKIN_CASE(7) CANNIKIN_CASE(8)
+#undef CANNIKIN_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+// One-shot launch if the bucket qualifies (returns true and sets *err), else false.
+static bool try_oneshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
+                        cudaStream_t st, cudaError_t* err) {
+  const int W = ctx->world;
+  const size_t esz = dt == CANNIKIN_F32 ? 4 : 2;
+  const size_t bytes = n * esz, nvec = bytes / 16;
+  if (ctx->ar_oneshot == 0) return false;
+  if (ctx->ar_oneshot < 0 && bytes > (size_t)W * (256u << 10)) return false;
+  // os_vpt vectors per thread where the grid allows, up to kOneShotMV
+  const size_t per_cta = (size_t)kArThreads * (size_t)ctx->os_vpt;
+  size_t g = (nvec + per_cta - 1) / per_cta;
+  if (g < 1) g = 1;
+  if (g > (size_t)ctx->grid_ar) g = (size_t)ctx->grid_ar;
+  if (nvec > g * kArThreads * kOneShotMV) return false;
+  const int grid = (int)g;
+  ArArgs a{};
+  for (int j = 0; j < W; ++j) {
+    a.bucket[j] = ctx->peer_base[j] + off;
+    a.pctrl[j] = reinterpret_cast<Ctrl*>(ctx->peer_base[j]);
+  }
+  a.ctrl = ctx->ctrl;
+  a.n = n;
+  a.nvec = nvec;
+  uint64_t meta = (uint64_t)off * 0x9E3779B97F4A7C15ull;
+  meta ^= (uint64_t)n * 0xC2B2AE3D27D4EB4Full;
+  meta ^= ((uint64_t)grid << 8) ^ (uint64_t)dt ^ 0x6f6e65ull;
+  a.meta = meta;
+  a.timeout_ns = ctx->spin_timeout_ns;
+  a.r_me = r_i;
+  a.rank = ctx->rank;
+  *err = dt == CANNIKIN_F32 ? dispatch_oneshot<float>(W, a, grid, st)
+                            : dispatch_oneshot<__nv_bfloat16>(W, a, grid, st);
+  return true;
+}
 
 // ============================================================================================
 // Push variant of K3 (CANNIKIN_AR_PUSH=1): every NVLink transfer is a write.
@@ -727,6 +893,10 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
                            cudaStream_t st) {
   const int W = ctx->world;
   {
+    cudaError_t err;
+    if (try_oneshot(ctx, off, n, dt, r_i, st, &err)) return err;
+  }
+  {
     // push (all-write) pays for large shards from 4 ranks up (+5% at W = 4, 256 MB-1 GB buckets;
     // profiles/r01/k3_pull_dyn_push_n4.jsonl); pull is better for small buckets and W = 2
     const size_t shard_bytes = n * (dt == CANNIKIN_F32 ? 4 : 2) / W;
@@ -776,6 +946,27 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
   a.meta = meta;
   if (dt == CANNIKIN_F32) return dispatch_w<float>(W, a, grid, dyn, st);
   return dispatch_w<__nv_bfloat16>(W, a, grid, dyn, st);
+}
+
+// Finalize the statistics of all calls since the last finalize: out[j] = stats[j] (dynamic / push
+// two-shot, NVLS, world 1) + sum over b of cta_acc[b][j] (static two-shot, one-shot) in ascending
+// b, then zero both.  One warp; `out` may be device or pinned host memory.
+__global__ void stats_finalize_kernel(Ctrl* c, int W, double* out) {
+  const int j = threadIdx.x;
+  if (j > W) return;
+  double t = c->stats[j];
+  c->stats[j] = 0.0;
+  double s = 0.0;
+  for (int b = 0; b < kMaxArBlocks; ++b) {
+    s += c->cta_acc[b][j];
+    c->cta_acc[b][j] = 0.0;
+  }
+  out[j] = t + s;
+}
+
+cudaError_t launch_stats_finalize(cannikin_ctx* ctx, double* out, cudaStream_t st) {
+  stats_finalize_kernel<<<1, 32, 0, st>>>(ctx->ctrl, ctx->world, out);
+  return cudaGetLastError();
 }
 
 }  // namespace cannikin

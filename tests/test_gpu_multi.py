@@ -1,4 +1,4 @@
-"""Multi-GPU parity of cannikin_weighted_allreduce (two-shot NVLink kernel) against the oracle,
+"""Multi-GPU parity of cannikin_weighted_allreduce (two-shot / one-shot NVLink kernels) against the oracle,
 bitwise identity across ranks, run-to-run determinism, staging path, multi-bucket stats.
 Runs tests/mp_allreduce_worker.py under torchrun on every visible GPU (2..8)."""
 import os
@@ -30,7 +30,7 @@ def _port():
     return p
 
 
-@pytest.fixture(scope="module", params=["static", "dyn", "push"])
+@pytest.fixture(scope="module", params=["static", "dyn", "push", "oneshot"])
 def results(request):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -41,7 +41,10 @@ def results(request):
            os.path.join(os.path.dirname(__file__), "mp_allreduce_worker.py"), "--out", d]
     env = dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000",
                CANNIKIN_AR_DYN="1" if request.param == "dyn" else "0",
-               CANNIKIN_AR_PUSH="1" if request.param == "push" else "0")
+               CANNIKIN_AR_PUSH="1" if request.param == "push" else "0",
+               # "oneshot": every bucket that fits the one-shot kernel uses it (larger ones, and
+               # the larger pieces of case (4), fall back to two-shot: mixed sequences)
+               CANNIKIN_AR_ONESHOT="1" if request.param == "oneshot" else "0")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     return world, d

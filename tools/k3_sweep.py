@@ -48,7 +48,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--grids", default="0")
-    ap.add_argument("--variants", default="0", help="CANNIKIN_AR_DYN values, or 'push'")
+    ap.add_argument("--variants", default="0",
+                    help="CANNIKIN_AR_DYN values (two-shot), 'push', 'oneshot' (2 vectors per thread), 'oneshot1' or 'auto'")
     ap.add_argument("--sizes-mb", default="1,4,16,64,256,1024")
     ap.add_argument("--total", type=int, default=TOTAL)
     ap.add_argument("--nvls", action="store_true", help="also time the NVLS kernel (fp32)")
@@ -64,8 +65,14 @@ def main():
     r = b[rank] / sum(b)
     combos = [(int(g), v) for g in args.grids.split(",") for v in args.variants.split(",")]
     for grid, var in combos:
-        os.environ["CANNIKIN_AR_PUSH"] = "1" if var == "push" else "0"
-        os.environ["CANNIKIN_AR_DYN"] = "0" if var == "push" else var
+        if var == "auto":
+            for k in ("CANNIKIN_AR_PUSH", "CANNIKIN_AR_DYN", "CANNIKIN_AR_ONESHOT"):
+                os.environ.pop(k, None)
+        else:
+            os.environ["CANNIKIN_AR_PUSH"] = "1" if var == "push" else "0"
+            os.environ["CANNIKIN_AR_ONESHOT"] = "1" if var.startswith("oneshot") else "0"
+            os.environ["CANNIKIN_OS_VPT"] = "1" if var == "oneshot1" else "2"
+            os.environ["CANNIKIN_AR_DYN"] = "0" if var == "push" or var.startswith("oneshot") else var
         ctx = ta.init_distributed_context(heap_bytes=N * s, grid=grid)
         bucket = ta.bucket_tensor(ctx, N, tdt)
         mcb = ta.McBucket(N, tdt) if args.nvls else None
@@ -78,7 +85,7 @@ def main():
             be -= be % 8
             cuts = list(range(0, N, be)) + [N]
             nb = len(cuts) - 1
-            reps = max(1, min(20, int(2e9 // (N * s))))
+            reps = max(1, min(20, int(2e9 // (N * s)), 4096 // nb))
 
             def ours():
                 for a, c in zip(cuts[:-1], cuts[1:]):
