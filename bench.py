@@ -253,7 +253,9 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-BIDIR_WRITE_GBS = 690.8  # profiles/r01/nvlink_bw_n2.jsonl (write2, best grid)
+# SM-driven peer writes with every GPU sending to every peer at once, per direction (GB/s):
+# profiles/r01/nvlink_bw_n2.jsonl (write2), nvlink_bw_n4.jsonl (a2a_write4); 8 GPUs not measured
+BIDIR_WRITE_GBS = {2: 690.8, 4: 671.4}
 
 
 def measured_peaks():
@@ -547,10 +549,10 @@ def main():
                 "kernel_ms": round(kmean, 4),
                 "traffic": ncu_traffic(f"{args.config}_w{n}_{cfg['dtype']}"),
                 # an all-reduce loads BOTH directions at once; the same SM-driven copy with both
-                # directions busy peaks lower than the one-way 770 (tools/nvlink_bw.cu,
-                # profiles/r01/nvlink_bw_n2.jsonl: 690.8 writes, 642.7 reads, 656.9 mixed)
-                "bidir_ceiling": {"peak": BIDIR_WRITE_GBS, "frac": round(busbw / BIDIR_WRITE_GBS, 4),
-                                  "kind": "measured two-GPU bidirectional peer writes per direction"}}
+                # directions busy peaks lower than the one-way 770 (tools/nvlink_bw.cu)
+                "bidir_ceiling": None if n not in BIDIR_WRITE_GBS else {
+                    "peak": BIDIR_WRITE_GBS[n], "frac": round(busbw / BIDIR_WRITE_GBS[n], 4),
+                    "kind": f"measured {n}-GPU all-to-all peer writes per direction"}}
 
     # ---- DDP baseline (equal split, NCCL average) on the same bucket, N > 1
     ddp = None

@@ -37,6 +37,27 @@ __global__ void copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ d
   for (; i < n; i += stride) dst[i] = src[i];
 }
 
+// all-to-all writes: CTA c writes to peer (c % np); every GPU's egress = its whole buffer
+struct Peers {
+  uint4* dst[8];
+};
+__global__ void a2a_write_kernel(const uint4* __restrict__ src, Peers p, int np, size_t n_per) {
+  const int k = blockIdx.x % np;
+  const int cta = blockIdx.x / np, nct = gridDim.x / np;
+  const uint4* s = src + (size_t)k * n_per;
+  uint4* d = p.dst[k];
+  const size_t stride = (size_t)nct * blockDim.x;
+  size_t i = (size_t)cta * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n_per; i += 4 * stride) {
+    uint4 a = s[i], b = s[i + stride], c = s[i + 2 * stride], e = s[i + 3 * stride];
+    d[i] = a;
+    d[i + stride] = b;
+    d[i + 2 * stride] = c;
+    d[i + 3 * stride] = e;
+  }
+  for (; i < n_per; i += stride) d[i] = s[i];
+}
+
 struct Job {
   int dev;
   const uint4* src;
@@ -73,11 +94,13 @@ int main(int argc, char** argv) {
     fprintf(stderr, "needs 2 GPUs\n");
     return 1;
   }
-  uint4 *a[2], *b[2];
-  cudaStream_t st[2];
-  for (int d = 0; d < 2; ++d) {
+  uint4 *a[8], *b[8];
+  cudaStream_t st[8];
+  const int G = ndev > 8 ? 8 : ndev;
+  for (int d = 0; d < G; ++d) {
     CK(cudaSetDevice(d));
-    CK(cudaDeviceEnablePeerAccess(1 - d, 0));
+    for (int q = 0; q < G; ++q)
+      if (q != d) CK(cudaDeviceEnablePeerAccess(q, 0));
     CK(cudaMalloc(&a[d], bytes));
     CK(cudaMalloc(&b[d], bytes));
     CK(cudaMemset(a[d], 1, bytes));
@@ -121,6 +144,35 @@ int main(int argc, char** argv) {
     printf("{\"case\": \"%s\", \"MiB_per_direction\": %zu, \"grid\": %d, \"threads\": %d, "
            "\"us\": %.1f, \"GBps_per_direction\": %.1f}\n",
            c.name, mib, grid, nt, t * 1e6, c.dir_bytes / t / 1e9);
+  }
+  if (G > 2) {
+    // every GPU writes 1/(G-1) of its buffer into each peer's b (slot = its rank), all at once
+    const int np = G - 1;
+    const size_t n_per = n / np;
+    const int gr = grid / np * np;
+    for (int w = 0; w < 3 + reps; ++w) {
+      if (w == 3) {
+        for (int d = 0; d < G; ++d) CK(cudaStreamSynchronize(st[d]));
+      }
+      static std::chrono::steady_clock::time_point t0;
+      if (w == 3) t0 = std::chrono::steady_clock::now();
+      for (int d = 0; d < G; ++d) {
+        CK(cudaSetDevice(d));
+        Peers p{};
+        int k = 0;
+        for (int q = 0; q < G; ++q)
+          if (q != d) p.dst[k++] = b[q] + (size_t)d * (n / G);
+        a2a_write_kernel<<<gr, nt, 0, st[d]>>>(a[d], p, np, n_per < n / G ? n_per : n / G);
+      }
+      if (w == 3 + reps - 1) {
+        for (int d = 0; d < G; ++d) CK(cudaStreamSynchronize(st[d]));
+        const double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / reps;
+        const double egress = (double)(n_per < n / G ? n_per : n / G) * 16 * np;
+        printf("{\"case\": \"a2a_write%d\", \"MiB_per_gpu\": %.1f, \"grid\": %d, \"threads\": %d, "
+               "\"us\": %.1f, \"GBps_per_direction\": %.1f}\n",
+               G, egress / (1 << 20), gr, nt, t * 1e6, egress / t / 1e9);
+      }
+    }
   }
   return 0;
 }
