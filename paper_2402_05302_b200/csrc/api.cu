@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -92,9 +93,13 @@ extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world
   ctx->total_bytes = ctx->scratch_off + (world > 1 ? ctx->heap_bytes : 0);
   if (const char* t = std::getenv("CANNIKIN_OS_VPT")) ctx->os_vpt = std::atoi(t) >= 2 ? 2 : 1;
   if (const char* t = std::getenv("CANNIKIN_AR_ONESHOT")) ctx->ar_oneshot = std::atoi(t) != 0;
-  if (const char* t = std::getenv("CANNIKIN_AR_PUSH")) ctx->ar_push = std::atoi(t) != 0 ? 1 : 0;
+  if (const char* t = std::getenv("CANNIKIN_AR_PUSH")) {
+    const int v = std::atoi(t);
+    ctx->ar_push = v <= 0 ? 0 : (v == 1 ? 1 : 2);
+  }
+  if (const char* t = std::getenv("CANNIKIN_PD_CHUNK_KB")) ctx->pd_chunk_kb = std::max(16, std::atoi(t));
   // staging for the push variant (W slots of the largest shard): by default from 4 ranks up
-  if (world > 1 && (ctx->ar_push == 1 || (ctx->ar_push < 0 && world >= 4))) {
+  if (world > 1 && (ctx->ar_push >= 1 || (ctx->ar_push < 0 && world >= 4))) {
     ctx->stage_off = ctx->total_bytes;
     ctx->total_bytes += align_up(ctx->heap_bytes + (size_t)world * world * 64 * 16 + 4096, 4096);
   }

@@ -27,6 +27,8 @@ struct Ctrl {
   uint64_t rv_word[kMaxArBlocks][kMaxWorld];                 // [peer] entry: (float r_src, epoch32)
   uint64_t meta_word[kMaxArBlocks][kMaxWorld];               // [peer] entry: (bucket hash32, epoch32)
   uint64_t pmid[kMaxArBlocks][kMaxWorld];                    // [peer] push variant: (r_src, epoch32)
+  uint64_t sflag[kMaxWorld][kMaxArChunks];                   // [peer] dynamic push: chunk landed
+  uint64_t pd_epoch;                                         // [local] dynamic-push call counter
   double part[kMaxWorld][kMaxArChunks][kMaxWorld + 1];       // [peer] norm partials [src][row][j]
   uint64_t epoch[kMaxArBlocks];                              // [local] per-block epoch counter
   unsigned ticket_ar;                                        // [local] last-block-done ticket
@@ -46,7 +48,8 @@ struct cannikin_ctx {
   int rank = 0, world = 1, device = 0;
   int grid_ar = 148;
   int ar_dyn = -1;          // CANNIKIN_AR_DYN=0|1 forces static/dynamic chunks; -1 = by size
-  int ar_push = -1;         // CANNIKIN_AR_PUSH=0|1 forces pull/push two-shot; -1 = by size
+  int ar_push = -1;         // CANNIKIN_AR_PUSH=0|1|2 forces pull / static push / dynamic push
+  int pd_chunk_kb = 256;    // CANNIKIN_PD_CHUNK_KB: dynamic-push chunk (grown to fit the row table)
   int os_vpt = 2;           // CANNIKIN_OS_VPT=1|2: one-shot vectors per thread (sets its grid)
   int ar_oneshot = -1;      // CANNIKIN_AR_ONESHOT=0|1 forbids/prefers one-shot; -1 = by size
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2

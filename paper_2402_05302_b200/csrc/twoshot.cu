@@ -888,6 +888,322 @@ cudaError_t launch_twoshot_push(cannikin_ctx* ctx, size_t off, size_t n, canniki
   return dispatch_push<__nv_bfloat16>(W, a, grid, st);
 }
 
+// ============================================================================================
+// Dynamic push variant of K3 (CANNIKIN_AR_PUSH=2): the push protocol with work items claimed from
+// a per-rank counter, so no CTA waits for a static piece and the two phases overlap.
+//   items 0..S-1 (scatter): chunk c of my part of peer shard S_k -> slot `rank` of k's staging,
+//     chunk-major over the peers, |g_me|^2 on the way; then a per-(source, chunk) flag
+//     (r_rank | call epoch) with release semantics at the owner;
+//   items S..S+R-1 (reduce): chunk c of my own shard, once every peer's flag for c has arrived:
+//     sum own bucket + W-1 staging slots (all LOCAL reads) in rank order (fp32), |g|^2, push the
+//     result into every bucket;
+//   every item's {|g_me|^2, |g|^2} piece is one row of every rank's partial table (so the
+//     statistics do not depend on which CTA did which item); exit barrier (CTA b <-> CTA b: when
+//     all CTAs of this rank pass it, every peer item is done); the last CTA sums all rows in
+//     (rank, row) order.
+// Scatter items never wait, and a CTA claims items in increasing order, so every awaited flag is
+// raised unconditionally: no deadlock for any grid.  NVLink bytes as the other variants.
+// ============================================================================================
+struct PushDynArgs {
+  char* bucket[kMaxWorld];
+  char* stage[kMaxWorld];
+  Ctrl* pctrl[kMaxWorld];
+  Ctrl* ctrl;
+  size_t nvec, n, L, slot_vec, chunk;
+  unsigned C;               // chunks of the largest (last) shard
+  uint64_t meta;
+  uint64_t timeout_ns;
+  float r_me;
+  int rank;
+};
+
+template <typename T, int W, int U>
+__global__ void __launch_bounds__(kArThreads, 1) pushdyn_kernel(const PushDynArgs a) {
+  using V = dev::Vec<T>;
+  constexpr int E = V::E;
+  constexpr int NT = kArThreads;
+  __shared__ double red[32 * 2];
+  __shared__ double s_row[2];
+  __shared__ float s_r[W];
+  __shared__ uint64_t s_ep;
+  __shared__ uint32_t s_ce;
+  __shared__ unsigned s_item[2];
+  __shared__ bool s_last;
+  const int b = blockIdx.x, tid = threadIdx.x, me = a.rank;
+  const bool has_tail = a.n > a.nvec * E;
+  auto lo_of = [&](int k) -> size_t { return a.L * (size_t)k; };
+  auto hi_of = [&](int k) -> size_t { return k == W - 1 ? a.nvec : a.L * (size_t)(k + 1); };
+  auto nck = [&](int k) -> unsigned {
+    unsigned c = (unsigned)((hi_of(k) - lo_of(k) + a.chunk - 1) / a.chunk);
+    if (k == W - 1 && c == 0 && has_tail) c = 1;
+    return c;
+  };
+  const unsigned S = a.C * (W - 1), R = nck(me);
+  const uint32_t m32 = (uint32_t)(a.meta ^ (a.meta >> 32));
+
+  if (tid == 0) {
+    s_ep = a.ctrl->epoch[b] + 1;
+    s_ce = (uint32_t)(a.ctrl->pd_epoch + 1);
+    a.ctrl->trace[b][0] = dev::globaltimer_ns();
+    a.ctrl->trace[b][1] = 0;
+    s_item[0] = atomicAdd(&a.ctrl->ar_counter, 1u);
+    s_item[1] = atomicAdd(&a.ctrl->ar_counter, 1u);
+  }
+  __syncthreads();
+  const uint64_t ep = s_ep;
+  const uint32_t ce = s_ce;
+  if (tid < W)  // bucket identity, checked at the exit barrier
+    dev::st_relaxed_sys_u64(&a.pctrl[tid]->meta_word[b][me], ((uint64_t)m32 << 32) | (uint32_t)ep);
+  const char* mine = a.bucket[me];
+
+  for (unsigned it = 0;; ++it) {
+    const unsigned i = s_item[it & 1];
+    if (i >= S + R) break;
+    double lsq = 0.0, gsq = 0.0;
+    if (i < S) {
+      // ---- scatter item
+      const unsigned c = i / (W - 1);
+      const int k = (me + 1 + (int)(i % (W - 1))) % W;
+      if (c < nck(k)) {
+        const size_t lo = lo_of(k) + (size_t)c * a.chunk;
+        const size_t hi = (lo + a.chunk < hi_of(k)) ? lo + a.chunk : hi_of(k);
+        char* dst = a.stage[k] + ((size_t)me * a.slot_vec - lo_of(k)) * 16;
+        size_t v = lo + tid;
+        for (; v + (U - 1) * NT < hi; v += U * NT) {
+          uint4 x[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) x[u] = dev::ld16(mine + (v + u * NT) * 16);
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            float g[E];
+            V::unpack(x[u], g);
+            float sq = 0.0f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) sq = fmaf(g[e], g[e], sq);
+            lsq += (double)sq;
+            dev::st16(dst + (v + u * NT) * 16, x[u]);
+          }
+        }
+        for (; v < hi; v += NT) {
+          const uint4 x = dev::ld16(mine + v * 16);
+          float g[E];
+          V::unpack(x, g);
+          float sq = 0.0f;
+#pragma unroll
+          for (int e = 0; e < E; ++e) sq = fmaf(g[e], g[e], sq);
+          lsq += (double)sq;
+          dev::st16(dst + v * 16, x);
+        }
+        // my own ragged tail (in shard W-1): its |g_me|^2 goes with the last chunk of that shard,
+        // read before the flag that lets the owner overwrite it
+        if (k == W - 1 && c == nck(k) - 1 && has_tail) {
+          const size_t e = a.nvec * E + tid;
+          if (e < a.n) {
+            const float g = V::load1(mine + e * sizeof(T));
+            lsq += (double)(g * g);
+          }
+        }
+        __syncthreads();  // every store of the chunk has been issued
+        if (tid == 0) {
+          __threadfence_system();
+          dev::st_release_sys(&a.pctrl[k]->sflag[me][c],
+                              ((uint64_t)__float_as_uint(a.r_me) << 32) | ce);
+        }
+      }
+    } else {
+      // ---- reduce item
+      const unsigned c = i - S;
+      if (tid == 0 && a.ctrl->trace[b][1] == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
+      if (tid < W) {
+        if (tid == me) {
+          s_r[tid] = a.r_me;
+        } else {
+          const uint64_t w = spin_word(&a.ctrl->sflag[tid][c], ce, a.ctrl, a.timeout_ns, 6);
+          s_r[tid] = __uint_as_float((uint32_t)(w >> 32));
+        }
+      }
+      __syncthreads();
+      float r[W];
+      const char* src[W];
+      const size_t slo = lo_of(me);
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        r[j] = s_r[j];
+        src[j] = (j == me) ? mine + slo * 16 : a.stage[me] + (size_t)j * a.slot_vec * 16;
+      }
+      const size_t lo = slo + (size_t)c * a.chunk;
+      const size_t hi = (lo + a.chunk < hi_of(me)) ? lo + a.chunk : hi_of(me);
+      for (size_t v = lo + tid; v < hi; v += NT) {
+        const size_t rel = v - slo;
+        uint4 x[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) x[j] = dev::ld16(src[j] + rel * 16);
+        float acc[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          float g[E];
+          V::unpack(x[j], g);
+#pragma unroll
+          for (int e = 0; e < E; ++e) acc[e] = fmaf(r[j], g[e], acc[e]);
+          if (j == me) {
+            float sq = 0.0f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) sq = fmaf(g[e], g[e], sq);
+            lsq += (double)sq;
+          }
+        }
+        float gs = 0.0f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) gs = fmaf(acc[e], acc[e], gs);
+        gsq += (double)gs;
+        const uint4 y = V::pack(acc);
+#pragma unroll
+        for (int jj = 0; jj < W; ++jj) {
+          const int j = (me + jj) % W;
+          dev::st16(a.bucket[j] + v * 16, y);
+        }
+      }
+      // the ragged element tail: owned by the last rank, with its last chunk; every peer's flag
+      // for that chunk has arrived, so every peer has read its own tail (and its bucket is ready)
+      if (me == W - 1 && c == R - 1 && has_tail) {
+        const size_t e = a.nvec * E + tid;
+        if (e < a.n) {
+          float acc = 0.0f;
+#pragma unroll
+          for (int j = 0; j < W; ++j) {
+            const float g = V::load1(a.bucket[j] + e * sizeof(T));
+            acc = fmaf(r[j], g, acc);
+            if (j == me) lsq += (double)(g * g);
+          }
+          gsq += (double)(acc * acc);
+#pragma unroll
+          for (int j = 0; j < W; ++j) V::store1(a.bucket[j] + e * sizeof(T), acc);
+        }
+      }
+    }
+    // ---- this item's row {|g_me|^2, |g|^2} -> every rank's table (zero rows for empty items)
+    double vals[2] = {lsq, gsq};
+    dev::block_sum<2>(vals, red);
+    if (tid == 0) {
+      s_row[0] = vals[0];
+      s_row[1] = vals[1];
+      s_item[it & 1] = atomicAdd(&a.ctrl->ar_counter, 1u);
+    }
+    __syncthreads();
+    if (tid < W) {
+      double* row = &a.pctrl[tid]->part[me][i][0];
+#pragma unroll
+      for (int j = 0; j <= W; ++j)
+        dev::st_relaxed_sys_f64(row + j, j == me ? s_row[0] : (j == W ? s_row[1] : 0.0));
+    }
+  }
+  if (tid == 0) {
+    a.ctrl->trace[b][2] = dev::globaltimer_ns();
+    if (a.ctrl->trace[b][1] == 0) a.ctrl->trace[b][1] = a.ctrl->trace[b][2];
+  }
+  __syncthreads();  // every data, flag and row store of this CTA has been issued
+
+  // ---- exit barrier (+ the bucket-identity check)
+  if (tid < W) {
+    __threadfence_system();
+    dev::st_release_sys(&a.pctrl[tid]->exit_[b][me], ep);
+    spin_until(&a.ctrl->exit_[b][tid], ep, a.ctrl, a.timeout_ns, 3);
+    const uint64_t wm = spin_word(&a.ctrl->meta_word[b][tid], (uint32_t)ep, a.ctrl, a.timeout_ns, 2);
+    if ((uint32_t)(wm >> 32) != m32) {
+      atomicExch(&a.ctrl->error_code, 2);
+      __trap();
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    a.ctrl->epoch[b] = ep;
+    a.ctrl->trace[b][3] = dev::globaltimer_ns();
+    __threadfence();
+    s_last = (atomicAdd(&a.ctrl->ticket_ar, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double tot[W + 1];
+#pragma unroll
+  for (int j = 0; j <= W; ++j) tot[j] = 0.0;
+  for (int src = 0; src < W; ++src) {
+    const unsigned nrows = S + nck(src);
+    for (unsigned i = tid; i < nrows; i += NT) {
+      const double* row = &a.ctrl->part[src][i][0];
+#pragma unroll
+      for (int j = 0; j <= W; ++j) tot[j] += __ldcg(row + j);
+    }
+  }
+  dev::block_sum<W + 1>(tot, red);
+  if (tid == 0) {
+#pragma unroll
+    for (int j = 0; j <= W; ++j) a.ctrl->stats[j] += tot[j];
+    a.ctrl->ticket_ar = 0u;
+    a.ctrl->ar_counter = 0u;
+    a.ctrl->pd_epoch = a.ctrl->pd_epoch + 1;
+    a.ctrl->trace[b][4] = dev::globaltimer_ns();
+    a.ctrl->trace_grid = gridDim.x;
+  }
+}
+
+template <typename T>
+static cudaError_t dispatch_pushdyn(int W, const PushDynArgs& a, int grid, cudaStream_t st) {
+  switch (W) {
+#define CANNIKIN_CASE(K) \
+  case K:                \
+    pushdyn_kernel<T, K, K <= 2 ? 4 : 2><<<grid, kArThreads, 0, st>>>(a); \
+    return cudaGetLastError();
+    CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5) CANNIKIN_CASE(6)
+    CANNIKIN_CASE(7) CANNIKIN_CASE(8)
+#undef CANNIKIN_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_pushdyn(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
+                           cudaStream_t st) {
+  const int W = ctx->world;
+  PushDynArgs a{};
+  for (int j = 0; j < W; ++j) {
+    a.bucket[j] = ctx->peer_base[j] + off;
+    a.stage[j] = ctx->peer_base[j] + ctx->stage_off;
+    a.pctrl[j] = reinterpret_cast<Ctrl*>(ctx->peer_base[j]);
+  }
+  a.ctrl = ctx->ctrl;
+  const size_t esz = dt == CANNIKIN_F32 ? 4 : 2;
+  a.n = n;
+  a.nvec = n * esz / 16;
+  size_t L = a.nvec / W;
+  L -= L % 64;
+  a.L = L;
+  const size_t last = a.nvec - L * (size_t)(W - 1);
+  a.slot_vec = last;
+  // chunk: the preferred size, grown so that W x (chunks of the largest shard) rows fit the table
+  size_t chunk = (size_t)ctx->pd_chunk_kb * 1024 / 16;
+  const size_t cmax = (size_t)(kMaxArChunks - 1) / (size_t)W;
+  const size_t need = (last + cmax - 1) / cmax;
+  if (need > chunk) chunk = need;
+  chunk = (chunk + kArThreads - 1) / kArThreads * kArThreads;
+  a.chunk = chunk;
+  unsigned C = (unsigned)((last + chunk - 1) / chunk);
+  if (C == 0 && n * esz > a.nvec * 16) C = 1;
+  a.C = C;
+  int grid = ctx->grid_ar;
+  uint64_t meta = (uint64_t)off * 0x9E3779B97F4A7C15ull;
+  meta ^= (uint64_t)n * 0xC2B2AE3D27D4EB4Full;
+  meta ^= ((uint64_t)grid << 8) ^ (uint64_t)dt ^ ((uint64_t)chunk * 0x94D049BB133111EBull) ^ 0x7064ull;
+  a.meta = meta;
+  a.timeout_ns = ctx->spin_timeout_ns;
+  a.r_me = (float)r_i;
+  a.rank = ctx->rank;
+  if (dt == CANNIKIN_F32) return dispatch_pushdyn<float>(W, a, grid, st);
+  return dispatch_pushdyn<__nv_bfloat16>(W, a, grid, st);
+}
+
 // Launch K3 on the bucket at byte offset `off` of every rank's allocation.
 cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
                            cudaStream_t st) {
@@ -900,6 +1216,7 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
     // push (all-write) pays for large shards from 4 ranks up (+5% at W = 4, 256 MB-1 GB buckets;
     // profiles/r01/k3_pull_dyn_push_n4.jsonl); pull is better for small buckets and W = 2
     const size_t shard_bytes = n * (dt == CANNIKIN_F32 ? 4 : 2) / W;
+    if (ctx->ar_push == 2 && ctx->stage_off) return launch_pushdyn(ctx, off, n, dt, r_i, st);
     const bool push = ctx->ar_push == 1 || (ctx->ar_push < 0 && W >= 4 && shard_bytes >= (32ull << 20));
     if (push && ctx->stage_off) return launch_twoshot_push(ctx, off, n, dt, r_i, st);
   }

@@ -30,7 +30,7 @@ def _port():
     return p
 
 
-@pytest.fixture(scope="module", params=["static", "dyn", "push", "oneshot"])
+@pytest.fixture(scope="module", params=["static", "dyn", "push", "pushdyn", "oneshot"])
 def results(request):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -41,7 +41,8 @@ def results(request):
            os.path.join(os.path.dirname(__file__), "mp_allreduce_worker.py"), "--out", d]
     env = dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000",
                CANNIKIN_AR_DYN="1" if request.param == "dyn" else "0",
-               CANNIKIN_AR_PUSH="1" if request.param == "push" else "0",
+               CANNIKIN_AR_PUSH={"push": "1", "pushdyn": "2"}.get(request.param, "0"),
+               CANNIKIN_PD_CHUNK_KB="16",  # many chunks (grown where the row table needs it)
                # "oneshot": every bucket that fits the one-shot kernel uses it (larger ones, and
                # the larger pieces of case (4), fall back to two-shot: mixed sequences)
                CANNIKIN_AR_ONESHOT="1" if request.param == "oneshot" else "0")

@@ -49,7 +49,7 @@ def main():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--grids", default="0")
     ap.add_argument("--variants", default="0",
-                    help="CANNIKIN_AR_DYN values (two-shot), 'push', 'oneshot' (2 vectors per thread), 'oneshot1' or 'auto'")
+                    help="CANNIKIN_AR_DYN values (two-shot), 'push', 'oneshot' (2 vectors per thread), 'oneshot1', 'pushdyn[:chunk_kb]' or 'auto'")
     ap.add_argument("--sizes-mb", default="1,4,16,64,256,1024")
     ap.add_argument("--total", type=int, default=TOTAL)
     ap.add_argument("--nvls", action="store_true", help="also time the NVLS kernel (fp32)")
@@ -68,6 +68,10 @@ def main():
         if var == "auto":
             for k in ("CANNIKIN_AR_PUSH", "CANNIKIN_AR_DYN", "CANNIKIN_AR_ONESHOT"):
                 os.environ.pop(k, None)
+        elif var.startswith("pushdyn"):
+            os.environ["CANNIKIN_AR_PUSH"] = "2"
+            os.environ["CANNIKIN_AR_ONESHOT"] = "0"
+            os.environ["CANNIKIN_PD_CHUNK_KB"] = var.split(":")[1] if ":" in var else "256"
         else:
             os.environ["CANNIKIN_AR_PUSH"] = "1" if var == "push" else "0"
             os.environ["CANNIKIN_AR_ONESHOT"] = "1" if var.startswith("oneshot") else "0"
