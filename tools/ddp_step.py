@@ -14,8 +14,14 @@ become ready proportionally later, as on a slower GPU.
   Cannikin: the comm hook (weighted all-reduce + norm statistics); every rank measures a_i, P_i,
             gamma_i (first bucket ready / P_i), T_o,i, T_u,i with CUDA events; the analyzer plans
             epoch 0 even, epoch 1 Eq. 8, then OptPerf.
+With --hetero sm the ranks are made heterogeneous by SM caps instead (BASELINE north_star:
+"per-rank compute-rate caps (restricted grid or SM-partitioned contexts)"): rank i runs its whole
+forward/backward/optimizer on the stream of a CUDA green context holding SM_CAPS[mix_i] SMs
+(A100 148, V100 60, P100 40: Table 1's FP16 TFLOPS ratios); no injected delays. The
+communication (our K3 on the hook's stream, NCCL for DDP) runs in the primary context.
 Rank 0 prints one JSON line per epoch and a summary; step times are max over ranks.
 """
+import contextlib
 import argparse
 import json
 import os
@@ -35,6 +41,7 @@ from paper_2402_05302_b200 import torch_api as ta  # noqa: E402
 from paper_2402_05302_b200.ddp_hook import CannikinHookState, cannikin_hook  # noqa: E402
 
 NSTAGE = 6
+SM_CAPS = {"A100": 148, "V100": 60, "P100": 40}  # 148 x TFLOPS ratio, rounded
 
 
 class _Delay(torch.autograd.Function):
@@ -88,13 +95,23 @@ def main():
     ap.add_argument("--grid", type=int, default=24)
     ap.add_argument("--model", default="resnet18", choices=["resnet18", "resnet50"])
     ap.add_argument("--img", type=int, default=32)
+    ap.add_argument("--hetero", default="delay", choices=["delay", "sm"])
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(lr)
     dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     torch.backends.cudnn.benchmark = True
-    f = bench.TFLOPS["A100"] / bench.TFLOPS[bench.MIX[rank % len(bench.MIX)]]
+    gpu = bench.MIX[rank % len(bench.MIX)]
+    f = bench.TFLOPS["A100"] / bench.TFLOPS[gpu]
+    if args.hetero == "sm":
+        from torch.cuda.green_contexts import GreenContext
+        gctx = GreenContext.create(SM_CAPS[gpu], lr)
+        cstream = gctx.Stream()
+        f = 1.0  # no injected delays: the SM cap is the heterogeneity
+        compute = lambda: torch.cuda.stream(cstream)  # noqa: E731
+    else:
+        compute = contextlib.nullcontext
     B = args.B
     ce = nn.CrossEntropyLoss()
     E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -110,18 +127,19 @@ def main():
     for bb in (8, 16, 32, 64, 96):
         bb = min(bb, B)
         for rep in range(4):
-            e0, e1, e2 = E(), E(), E()
-            cal.bwd[1] = None
-            e0.record()
-            loss = ce(cal(Xall[:bb].clone()), yall[:bb])
-            e1.record()
-            loss.backward()
-            e2.record()
-            torch.cuda.synchronize()
-            if rep >= 1:
-                xs.append(bb)
-                fa.append(e0.elapsed_time(e1) * 1e-3)
-                fp.append(e1.elapsed_time(e2) * 1e-3)
+            with compute():
+                e0, e1, e2 = E(), E(), E()
+                cal.bwd[1] = None
+                e0.record()
+                loss = ce(cal(Xall[:bb].clone()), yall[:bb])
+                e1.record()
+                loss.backward()
+                e2.record()
+                torch.cuda.synchronize()
+                if rep >= 1:
+                    xs.append(bb)
+                    fa.append(e0.elapsed_time(e1) * 1e-3)
+                    fp.append(e1.elapsed_time(e2) * 1e-3)
     qa, sa = ck.fit_linear(xs, fa)
     kp, mp = ck.fit_linear(xs, fp)
     del cal
@@ -139,6 +157,10 @@ def main():
         return m, ddp, torch.optim.SGD(ddp.parameters(), lr=0.01, momentum=0.9)
 
     def run_iter(ddp, model, opt, b_i, state=None):
+        with compute():
+            return _run_iter(ddp, model, opt, b_i, state)
+
+    def _run_iter(ddp, model, opt, b_i, state=None):
         X, y = Xall[:b_i].clone(), yall[:b_i]
         e0, e1, e2, e3 = E(), E(), E(), E()
         model.bwd[1] = e2  # recorded at the end of backprop compute (before DDP's final wait)
@@ -157,7 +179,12 @@ def main():
     out = {"model": args.model, "img": args.img,
            "params": sum(p.numel() for p in SlowResNet(args.model, classes).parameters()),
            "mix": [bench.MIX[i % len(bench.MIX)] for i in range(world)], "B": B,
-           "calibrated_ms_per_sample": round((qa + kp) * 1e3, 4)}
+           "calibrated_ms_per_sample": round((qa + kp) * 1e3, 4), "hetero": args.hetero}
+    per = [None] * world
+    dist.all_gather_object(per, round((qa + kp) * 1e3, 4))
+    out["ms_per_sample_by_rank"] = per
+    if args.hetero == "sm":
+        out["sm_caps"] = [SM_CAPS[bench.MIX[i % len(bench.MIX)]] for i in range(world)]
     # ---------------- equal-split DDP, stock NCCL average
     model, ddp, opt = build(None)
     b_eq = [B // world + (1 if i < B % world else 0) for i in range(world)]
