@@ -447,7 +447,7 @@ def main():
             a, c = cuts[bi], cuts[bi + 1]
             ta.weighted_allreduce(ctx, bucket[a:c], r[rank])
 
-        def read_stats(k):  # straight into pinned host memory (one copy node)
+        def read_stats(k):  # one finalize kernel writes straight into pinned host memory
             ctx.gns_stats_async(stats_h[k].data_ptr(), torch.cuda.current_stream())
 
     # per-kernel timing events on the launching stream (external: recordable inside a graph)
@@ -653,7 +653,8 @@ def main():
                        "host_overlap": "host half of step t overlaps device half of step t+1"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "ddp_baseline": ddp,
             "step_vs_ddp": hetero, "nvls_f32": nvls,
-            "gpu_launches": launches_per_step() * args.steps,
+            # K2 / K3 per bucket, plus (N > 1) the statistics-finalize kernel per step
+            "gpu_launches": (launches_per_step() + (1 if world > 1 else 0)) * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
