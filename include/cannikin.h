@@ -80,8 +80,15 @@ cannikin_status cannikin_get_unique_id(void* out_id);
  *   exchanged through NCCL).  Buckets carved from the heap (cannikin_alloc_bucket) are reduced
  *   zero-copy; other device buffers are staged through a heap scratch area of the same size.
  * `grid` (0 = default 148) fixes the CTA count of the reduction kernels (determinism contract).
- * `flags`: reserved, pass 0.
- * Errors: INVALID (rank/world/device out of range, out == NULL), CUDA, NCCL. */
+ * `flags`: 0, or CANNIKIN_INIT_CHECK_RATIOS -- every weighted_allreduce checks on the device that
+ *   the ranks' shares sum to 1 (SURVEY §8(b) "ratio check"): sum_j r_j is formed in double from
+ *   the fp32 shares the kernel multiplies with (each within 2^-24 relative of the caller's value)
+ *   and must lie within 2^-23 of 1.  A violation does not stop the reduction; it is reported as
+ *   DOMAIN by the next cannikin_gns_stats or cannikin_device_status.  Free (one comparison in one
+ *   thread); not applied by the NVLS variant, which exchanges no shares.
+ * Errors: INVALID (rank/world/device out of range, out == NULL, unknown flag), CUDA, NCCL. */
+#define CANNIKIN_INIT_CHECK_RATIOS 1u
+
 cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world, const void* unique_id,
                               int device, size_t heap_bytes, int grid, unsigned flags);
 
@@ -131,14 +138,21 @@ cannikin_status cannikin_weighted_allreduce_nvls(cannikin_ctx* ctx, void* bucket
  *   out_local_sq[j] = |g_j|^2 for j = 0..world-1, *out_global_sq = |g|^2   (host pointers).
  * Identical bits on every rank.  Synchronises `stream`.
  * The north-star signature carried b_i; batch sizes are not needed to finalise the norms and are
- * passed to cannikin_gns_estimate instead.  Errors: INVALID, CUDA. */
+ * passed to cannikin_gns_estimate instead.  Errors: INVALID, DOMAIN (a reduction since the last
+ * check saw shares not summing to 1, CANNIKIN_INIT_CHECK_RATIOS; the statistics are still
+ * returned), CUDA (also: a device protocol error recorded by a reduction kernel). */
 cannikin_status cannikin_gns_stats(cannikin_ctx* ctx, void* stream, double* out_local_sq,
                                    double* out_global_sq);
 
-/* Stream-ordered variant: copies the (world+1) accumulated doubles [local_sq..., global_sq] to
- * d_out (device memory, or pinned host memory) and resets the accumulator, without host
- * synchronisation. */
+/* Stream-ordered variant: one finalize kernel writes the (world+1) accumulated doubles
+ * [local_sq..., global_sq] to d_out (device memory, or pinned host memory) and resets the
+ * accumulator, without host synchronisation. */
 cannikin_status cannikin_gns_stats_async(cannikin_ctx* ctx, double* d_out, void* stream);
+
+/* Synchronise the ctx's device and report (and clear, if recoverable) a condition recorded by the
+ * reduction kernels: OK, DOMAIN (shares did not sum to 1, see CANNIKIN_INIT_CHECK_RATIOS; cleared),
+ * or CUDA (protocol error code; not cleared). */
+cannikin_status cannikin_device_status(cannikin_ctx* ctx);
 
 /* Single-GPU fused pass over n_ranks emulated ranks (the 1-B200 metric kernel; reading of
  * SURVEY §8(a) row a5):

@@ -92,6 +92,7 @@ SIGNATURES = {
     "cannikin_weighted_allreduce_nvls": (_I, [_P, _P, _P, _Z, _I, _D, _P]),
     "cannikin_gns_stats": (_I, [_P, _P, _DP, _DP]),
     "cannikin_gns_stats_async": (_I, [_P, _P, _P]),
+    "cannikin_device_status": (_I, [_P]),
     "cannikin_weighted_sum_local": (_I, [_P, ctypes.POINTER(_P), _I, _DP, _P, _Z, _I, _P, _P, _U, _P]),
     "cannikin_ddp_allreduce_mean": (_I, [_P, _P, _Z, _I, _P]),
     "cannikin_last_launch_count": (_I, [_P]),
@@ -158,18 +159,23 @@ def _stream(s) -> int | None:
 
 
 # ----------------------------------------------------------------------------- device context
+INIT_CHECK_RATIOS = 1  # cannikin.h CANNIKIN_INIT_CHECK_RATIOS
+
+
 class Context:
     """A cannikin_ctx: one per (process, GPU).  world > 1 is collective (see cannikin_init)."""
 
     def __init__(self, rank: int = 0, world: int = 1, unique_id: bytes | None = None,
-                 device: int = 0, heap_bytes: int = 0, grid: int = 0):
+                 device: int = 0, heap_bytes: int = 0, grid: int = 0,
+                 check_ratios: bool = False):
         L = lib()
         h = ctypes.c_void_p()
         uid = None
         if unique_id is not None:
             assert len(unique_id) == 128
             uid = ctypes.create_string_buffer(bytes(unique_id), 128)
-        _check(L.cannikin_init(ctypes.byref(h), rank, world, uid, device, heap_bytes, grid, 0))
+        flags = INIT_CHECK_RATIOS if check_ratios else 0
+        _check(L.cannikin_init(ctypes.byref(h), rank, world, uid, device, heap_bytes, grid, flags))
         self._h = h
         self.rank, self.world, self.device = rank, world, device
 
@@ -208,6 +214,11 @@ class Context:
 
     def gns_stats_async(self, d_out: int, stream=None):
         _check(lib().cannikin_gns_stats_async(self._h, d_out, _stream(stream)))
+
+    def device_status(self):
+        """Raise CannikinError for a condition the reduction kernels recorded (DOMAIN: shares not
+        summing to 1 under check_ratios -- cleared by this call)."""
+        _check(lib().cannikin_device_status(self._h))
 
     def weighted_sum_local(self, in_ptrs, r, out_ptr: int, n: int, dtype: int, d_local_sq: int,
                            d_global_sq: int, accumulate: bool = False, stream=None,

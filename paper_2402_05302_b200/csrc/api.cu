@@ -59,8 +59,8 @@ static cannikin_status destroy_partial(cannikin_ctx* ctx) {
 extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world,
                                          const void* unique_id, int device, size_t heap_bytes,
                                          int grid, unsigned flags) {
-  (void)flags;
   if (!out) return fail(CANNIKIN_ERR_INVALID, "init: out == NULL");
+  if (flags & ~CANNIKIN_INIT_CHECK_RATIOS) return fail(CANNIKIN_ERR_INVALID, "init: unknown flags %#x", flags);
   *out = nullptr;
   if (world < 1 || world > CANNIKIN_MAX_WORLD || rank < 0 || rank >= world)
     return fail(CANNIKIN_ERR_INVALID, "init: rank=%d world=%d (world must be 1..%d)", rank, world,
@@ -74,6 +74,7 @@ extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world
   cannikin_ctx* ctx = new cannikin_ctx();
   ctx->rank = rank;
   ctx->world = world;
+  ctx->check_ratios = (flags & CANNIKIN_INIT_CHECK_RATIOS) ? 1 : 0;
   ctx->device = device;
   cudaError_t ce = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (ce != cudaSuccess) { destroy_partial(ctx); CK_CUDA(ce); }
@@ -255,6 +256,28 @@ extern "C" cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* 
   return CANNIKIN_OK;
 }
 
+// Report a condition the reduction kernels recorded in the control region (after a sync).
+static cannikin_status check_device_code(cannikin_ctx* ctx, const char* who) {
+  int code = 0;
+  CK_CUDA(cudaMemcpy(&code, &ctx->ctrl->error_code, sizeof code, cudaMemcpyDeviceToHost));
+  if (code == 7) {  // shares did not sum to 1 (CANNIKIN_INIT_CHECK_RATIOS): recoverable, cleared
+    double s = 0.0;
+    CK_CUDA(cudaMemcpy(&s, &ctx->ctrl->rsum_bad, sizeof s, cudaMemcpyDeviceToHost));
+    const int zero = 0;
+    CK_CUDA(cudaMemcpy(&ctx->ctrl->error_code, &zero, sizeof zero, cudaMemcpyHostToDevice));
+    return fail(CANNIKIN_ERR_DOMAIN, "%s: the ranks' shares r_j sum to %.17g, not 1", who, s);
+  }
+  if (code) return fail(CANNIKIN_ERR_CUDA, "%s: device protocol error %d", who, code);
+  return CANNIKIN_OK;
+}
+
+extern "C" cannikin_status cannikin_device_status(cannikin_ctx* ctx) {
+  if (!ctx) return fail(CANNIKIN_ERR_INVALID, "device_status: ctx == NULL");
+  CK_CUDA(cudaSetDevice(ctx->device));
+  CK_CUDA(cudaDeviceSynchronize());
+  return check_device_code(ctx, "device_status");
+}
+
 extern "C" cannikin_status cannikin_gns_stats(cannikin_ctx* ctx, void* stream,
                                               double* out_local_sq, double* out_global_sq) {
   if (!ctx || !out_local_sq || !out_global_sq)
@@ -263,12 +286,9 @@ extern "C" cannikin_status cannikin_gns_stats(cannikin_ctx* ctx, void* stream,
   const int W = ctx->world;
   CK_CUDA(cannikin::launch_stats_finalize(ctx, ctx->h_stats, S(stream)));
   CK_CUDA(cudaStreamSynchronize(S(stream)));
-  int code = 0;
-  CK_CUDA(cudaMemcpy(&code, &ctx->ctrl->error_code, sizeof code, cudaMemcpyDeviceToHost));
-  if (code) return fail(CANNIKIN_ERR_CUDA, "gns_stats: device protocol error %d", code);
   for (int j = 0; j < W; ++j) out_local_sq[j] = ctx->h_stats[j];
   *out_global_sq = ctx->h_stats[W];
-  return CANNIKIN_OK;
+  return check_device_code(ctx, "gns_stats");
 }
 
 extern "C" cannikin_status cannikin_gns_stats_async(cannikin_ctx* ctx, double* d_out, void* stream) {

@@ -35,6 +35,7 @@ struct Ctrl {
   unsigned ticket_local;
   unsigned ar_counter;                                       // [local] dynamic two-shot chunk counter
   int error_code;                                            // [local] protocol error (trap reason)
+  double rsum_bad;                                           // [local] offending sum_j r_j (code 7)
   double stats[kMaxWorld + 1];                               // [local] accumulated |g_j|^2, |g|^2
   double cta_acc[kMaxArBlocks][kMaxWorld + 1];               // [local] per-CTA running stats
   uint64_t trace[kMaxLocalBlocks][5];                        // [local] per-CTA timeline (ns)
@@ -50,6 +51,7 @@ struct cannikin_ctx {
   int ar_dyn = -1;          // CANNIKIN_AR_DYN=0|1 forces static/dynamic chunks; -1 = by size
   int ar_push = -1;         // CANNIKIN_AR_PUSH=0|1|2 forces pull / static push / dynamic push
   int pd_chunk_kb = 256;    // CANNIKIN_PD_CHUNK_KB: dynamic-push chunk (grown to fit the row table)
+  int check_ratios = 0;     // CANNIKIN_INIT_CHECK_RATIOS
   int os_vpt = 2;           // CANNIKIN_OS_VPT=1|2: one-shot vectors per thread (sets its grid)
   int ar_oneshot = -1;      // CANNIKIN_AR_ONESHOT=0|1 forbids/prefers one-shot; -1 = by size
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2

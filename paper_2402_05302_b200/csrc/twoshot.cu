@@ -41,9 +41,24 @@ struct ArArgs {
   size_t shard_len_last;
   double r_me;
   int rank;
+  int check_r;              // CANNIKIN_INIT_CHECK_RATIOS: verify sum_j r_j == 1 on the device
 };
 
 constexpr int kArThreads = 512;
+
+// sum_j r_j in double over the fp32 ratios the kernel uses: each is within 2^-24 relative of the
+// caller's double, so a correct split sums to 1 within 2^-23.  A violation is recorded (code 7,
+// reported as DOMAIN by cannikin_gns_stats / cannikin_device_status), not trapped.
+template <int W>
+__device__ __forceinline__ void check_ratios(const float* r, Ctrl* c) {
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < W; ++j) s += (double)r[j];
+  if (fabs(s - 1.0) > 0x1p-23) {
+    c->rsum_bad = s;
+    atomicCAS(&c->error_code, 0, 7);
+  }
+}
 
 __device__ __forceinline__ void spin_until(const uint64_t* flag, uint64_t ep, Ctrl* ctrl,
                                            uint64_t timeout_ns, int code) {
@@ -162,6 +177,7 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
   // ---- 0. entry barrier (+ exchange of r_j and the bucket identity)
   if (tid < W) entry_barrier_thread<W>(a, b, ep, s_r);
   __syncthreads();
+  if (a.check_r && b == 0 && tid == 0) check_ratios<W>(s_r, a.ctrl);
   if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
 
   float r[W];
@@ -290,6 +306,7 @@ __global__ void __launch_bounds__(kArThreads, 1) twoshot_dyn_kernel(const ArArgs
   const uint64_t ep = s_ep;
   if (tid < W) entry_barrier_thread<W>(a, b, ep, s_r);
   __syncthreads();
+  if (a.check_r && b == 0 && tid == 0) check_ratios<W>(s_r, a.ctrl);
   if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
 
   float r[W];
@@ -460,6 +477,7 @@ __global__ void __launch_bounds__(kArThreads, 1) oneshot_kernel(const ArArgs a) 
   const uint64_t ep = s_ep;
   if (tid < W) entry_barrier_thread<W>(a, b, ep, s_r);
   __syncthreads();
+  if (a.check_r && b == 0 && tid == 0) check_ratios<W>(s_r, a.ctrl);
   if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
 
   float r[W];
@@ -604,6 +622,7 @@ static bool try_oneshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype 
   a.timeout_ns = ctx->spin_timeout_ns;
   a.r_me = r_i;
   a.rank = ctx->rank;
+  a.check_r = ctx->check_ratios;
   *err = dt == CANNIKIN_F32 ? dispatch_oneshot<float>(W, a, grid, st)
                             : dispatch_oneshot<__nv_bfloat16>(W, a, grid, st);
   return true;
@@ -633,6 +652,7 @@ struct PushArgs {
   uint64_t timeout_ns;
   float r_me;
   int rank;
+  int check_r;
 };
 
 template <typename T, int W, int U>
@@ -729,6 +749,7 @@ __global__ void __launch_bounds__(512, 1) twoshot_push_kernel(const PushArgs a) 
     }
   }
   __syncthreads();
+  if (a.check_r && b == 0 && tid == 0) check_ratios<W>(s_r, a.ctrl);
   if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
 
   // ---- 3. reduce my shard's piece from local memory, push the result to every peer
@@ -886,6 +907,7 @@ cudaError_t launch_twoshot_push(cannikin_ctx* ctx, size_t off, size_t n, canniki
   a.timeout_ns = ctx->spin_timeout_ns;
   a.r_me = (float)r_i;
   a.rank = ctx->rank;
+  a.check_r = ctx->check_ratios;
   if (dt == CANNIKIN_F32) return dispatch_push<float>(W, a, grid, st);
   return dispatch_push<__nv_bfloat16>(W, a, grid, st);
 }
@@ -917,6 +939,7 @@ struct PushDynArgs {
   uint64_t timeout_ns;
   float r_me;
   int rank;
+  int check_r;
 };
 
 template <typename T, int W, int U>
@@ -1025,6 +1048,7 @@ __global__ void __launch_bounds__(kArThreads, 1) pushdyn_kernel(const PushDynArg
         }
       }
       __syncthreads();
+      if (a.check_r && c == 0 && tid == 0) check_ratios<W>(s_r, a.ctrl);
       float r[W];
       const char* src[W];
       const size_t slo = lo_of(me);
@@ -1202,6 +1226,7 @@ cudaError_t launch_pushdyn(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
   a.timeout_ns = ctx->spin_timeout_ns;
   a.r_me = (float)r_i;
   a.rank = ctx->rank;
+  a.check_r = ctx->check_ratios;
   if (dt == CANNIKIN_F32) return dispatch_pushdyn<float>(W, a, grid, st);
   return dispatch_pushdyn<__nv_bfloat16>(W, a, grid, st);
 }
@@ -1247,6 +1272,7 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
   a.timeout_ns = ctx->spin_timeout_ns;
   a.r_me = r_i;
   a.rank = ctx->rank;
+  a.check_r = ctx->check_ratios;
   // dynamic variant: chunks of the shard handed out by a per-rank atomic counter (balances the
   // per-CTA NVLink bandwidth spread); per-chunk partial rows keep the statistics deterministic
   // auto: dynamic chunks pay off for large shards (measured crossover ~32-128 MiB per shard)

@@ -148,6 +148,26 @@ def main():
             ta.free_bucket_tensor(ctx, Bk)
             ta.free_bucket_tensor(ctx, A)
     ctx.gns_stats()
+    # CANNIKIN_INIT_CHECK_RATIOS: shares summing to 1 pass; shares summing to 0.95 are reported as
+    # DOMAIN (the reduction itself still runs) and the condition is cleared by the report
+    ctx2 = ta.init_distributed_context(heap_bytes=1 << 20, grid=args.grid, check_ratios=True)
+    chk = {}
+    for tag, scale in (("ok", 1.0), ("bad", 0.95), ("ok_after", 1.0)):
+        t = ta.bucket_tensor(ctx2, 4099, torch.float32)
+        t.fill_(1.0)
+        ta.weighted_allreduce(ctx2, t, scale / world)
+        try:
+            ctx2.gns_stats()
+            chk[tag] = "OK"
+        except ck.CannikinError as e:
+            chk[tag] = e.name
+        chk[tag + "_val"] = float(t[0])
+        ta.free_bucket_tensor(ctx2, t)
+    np.save(os.path.join(args.out, f"rank{rank}_check_ratios.npy"), np.array([chk["ok"], chk["bad"], chk["ok_after"]]))
+    np.save(os.path.join(args.out, f"rank{rank}_check_ratios_val.npy"),
+            np.array([chk["ok_val"], chk["bad_val"], chk["ok_after_val"]]))
+    dist.barrier()
+    ctx2.close()
     # DDP baseline semantics: mean of the ranks' buffers
     x = torch.full((1000,), float(rank + 1), device="cuda")
     ta.ddp_allreduce_mean(ctx, x)

@@ -93,3 +93,15 @@ def test_no_out_of_bounds_writes(results):
         for dtype in ("f32", "bf16"):
             for r in range(world):
                 assert bool(np.load(os.path.join(d, f"rank{r}_canary_{dtype}_{N}.npy"))[0]), (N, dtype, r)
+
+
+def test_check_ratios(results):
+    """CANNIKIN_INIT_CHECK_RATIOS: a split whose shares sum to 0.95 is reported as
+    DOMAIN by gns_stats on every rank, the reduction still runs (all-ones input -> 0.95), and the
+    condition is cleared by the report; correct splits pass."""
+    world, d = results
+    for r in range(world):
+        st = np.load(os.path.join(d, f"rank{r}_check_ratios.npy"))
+        assert list(st) == ["OK", "DOMAIN", "OK"], (r, st)
+        val = np.load(os.path.join(d, f"rank{r}_check_ratios_val.npy"))
+        assert np.allclose(val, [1.0, 0.95, 1.0], rtol=1e-6), (r, val)

@@ -120,3 +120,48 @@ def test_noise_scale_ratio():
     assert math.isclose(r["G2"], 1.0, rel_tol=1e-12)
     assert math.isclose(r["trS"], 100.0, rel_tol=1e-12)
     assert math.isclose(r["B_noise"], 100.0, rel_tol=1e-12)
+
+
+def test_theorem1_matrices_nonsingular_small_clusters():
+    """Theorem 1's printed A_G and A_S are nonsingular for EVERY split with n <= 4
+    and b_i <= 12 (exact rational determinants, entries retyped from the theorem, not from the
+    oracle), so the SINGULAR error is unreachable for such clusters; the oracle's weights exist
+    and sum to 1 there."""
+    import itertools
+    from fractions import Fraction as F
+
+    def det(M):
+        M = [row[:] for row in M]
+        n, d = len(M), F(1)
+        for c in range(n):
+            p = next((r for r in range(c, n) if M[r][c] != 0), None)
+            if p is None:
+                return F(0)
+            if p != c:
+                M[c], M[p] = M[p], M[c]
+                d = -d
+            d *= M[c][c]
+            for r in range(c + 1, n):
+                f = M[r][c] / M[c][c]
+                for k in range(c, n):
+                    M[r][k] -= f * M[c][k]
+        return d
+
+    count = 0
+    for n in (2, 3, 4):
+        for b in itertools.combinations_with_replacement(range(1, 13), n):
+            B = sum(b)
+            AG = [[F(B + 2 * b[i], B * B - B * b[i]) if i == j else
+                   F(B * B - b[i] ** 2 - b[j] ** 2, B * (B - b[i]) * (B - b[j])) for j in range(n)]
+                  for i in range(n)]
+            AS = [[F(B * b[i], B - b[i]) if i == j else
+                   F(b[i] * b[j] * (B - b[i] - b[j]), (B - b[i]) * (B - b[j])) for j in range(n)]
+                  for i in range(n)]
+            assert det(AG) != 0 and det(AS) != 0, b
+            if count % 97 == 0:
+                AGo, ASo = gns.weight_matrices(list(b))
+                for A in (AGo, ASo):
+                    w = gns.optimal_weights(A)
+                    assert np.all(np.isfinite(w)) and abs(float(np.sum(w)) - 1.0) < 1e-12
+            count += 1
+    assert count == 1807
