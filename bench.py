@@ -206,7 +206,7 @@ class ClockSampler:
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,clocks.mem")
 
     def __init__(self, device: int):
         self.device, self.lines, self.proc = device, [], None
@@ -235,7 +235,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, mem, mx, reasons = [], [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             p = [x.strip() for x in ln.split(",")]
@@ -249,7 +249,13 @@ class ClockSampler:
             for nm, v in zip(names, p[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
+            if len(p) > 6:
+                try:
+                    mem.append(float(p[6]))
+                except ValueError:
+                    pass
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "mem_mhz": statistics.median(mem) if mem else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
@@ -528,6 +534,9 @@ def main():
         kmean = float(kk.item())
     else:
         kmean = statistics.mean(kernel_ms)
+    kq = statistics.quantiles(kernel_ms, n=10) if len(kernel_ms) >= 2 else [kmean] * 9
+    kdist = {"p10": round(kq[0], 4), "p50": round(statistics.median(kernel_ms), 4),
+             "p90": round(kq[8], 4), "launches": len(kernel_ms), "rank": rank}
     ms_step = ms / args.steps
     value = step_bytes / (ms_step * 1e-3) / 1e9
 
@@ -538,7 +547,7 @@ def main():
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
                 "peak_kind": peak_kind, "kernel": "wsum_local_kernel (K2)",
-                "kernel_ms": round(kmean, 4),
+                "kernel_ms": round(kmean, 4), "kernel_ms_dist": kdist,
                 "traffic": ncu_traffic(f"{args.config}_n{n}_{cfg['dtype']}_b{launches_per_step()}")}
     else:
         busbw = (N * s / len(cuts[:-1])) / (kmean * 1e-3) * 2 * (n - 1) / n / 1e9
@@ -546,7 +555,7 @@ def main():
                 "frac": round(busbw / 770.0, 4),
                 "peak_kind": "measured peer copy per GPU per direction (B200_PROFILING.md); 900 nominal",
                 "kernel": "K3 two-shot (pull / dynamic / push variant by size)",
-                "kernel_ms": round(kmean, 4),
+                "kernel_ms": round(kmean, 4), "kernel_ms_dist": kdist,
                 "traffic": ncu_traffic(f"{args.config}_w{n}_{cfg['dtype']}"),
                 # an all-reduce loads BOTH directions at once; the same SM-driven copy with both
                 # directions busy peaks lower than the one-way 770 (tools/nvlink_bw.cu)
