@@ -165,3 +165,92 @@ def test_theorem1_matrices_nonsingular_small_clusters():
                     assert np.all(np.isfinite(w)) and abs(float(np.sum(w)) - 1.0) < 1e-12
             count += 1
     assert count == 1807
+
+
+# ---------------------------------------------------------------- corrected-covariance variant
+def _mc_estimates(b, d=128, trials=40_000, G2=1.0, trS=100.0, seed=11):
+    """Per-node Eq. 10 estimates over Monte Carlo draws of the paper's model (Eq. 1: g_i = mean of
+    b_i iid N(G, Sigma) samples, here drawn directly as N(G, Sigma / b_i)), isotropic Sigma."""
+    rng = np.random.default_rng(seed)
+    b = np.asarray(b, dtype=float)
+    n, B = len(b), float(np.sum(b))
+    G = rng.standard_normal(d)
+    G *= math.sqrt(G2) / np.linalg.norm(G)
+    s2 = trS / d
+    Gi = np.empty((trials, n))
+    Si = np.empty((trials, n))
+    for t0 in range(0, trials, 5000):
+        m = min(5000, trials - t0)
+        g = G + np.sqrt(s2 / b)[None, :, None] * rng.standard_normal((m, n, d))
+        gg = np.einsum("i,tid->td", b / B, g)
+        ls = np.einsum("tid,tid->ti", g, g)
+        gs = np.einsum("td,td->t", gg, gg)
+        for i in range(n):
+            Gi[t0:t0 + m, i] = (B * gs - b[i] * ls[:, i]) / (B - b[i])
+            Si[t0:t0 + m, i] = b[i] * B / (B - b[i]) * (ls[:, i] - gs)
+    tau = 2.0 * d * s2 * s2          # 2 tr(Sigma^2)
+    c = 4.0 * s2 * G2                # 4 G^T Sigma G
+    return Gi, Si, tau, c
+
+
+def test_corrected_matrices_match_monte_carlo_covariance():
+    """The exact-Gaussian covariance of the Eq. 10 estimators (Isserlis) against the empirical
+    covariance of 40k draws of the paper's model at C1's b."""
+    b = [32, 64, 96]
+    Gi, Si, tau, c = _mc_estimates(b)
+    AG, AS = gns.corrected_matrices(b, tau / c)
+    for emp, A in ((np.cov(Gi.T) / c, AG), (np.cov(Si.T) / c, AS)):
+        scale = np.sqrt(np.outer(np.diag(A), np.diag(A)))
+        assert np.max(np.abs(emp - A) / scale) < 0.03, (emp, A)
+
+
+def test_corrected_weights_minimum_variance_and_unbiased():
+    """With the exact covariance the combined estimator is unbiased and has smaller variance than
+    both the uniform weights and Theorem 1's printed weights (which lose to uniform at C1's b,
+    SURVEY App. A.8)."""
+    b = [32, 64, 96]
+    Gi, Si, tau, c = _mc_estimates(b, trials=60_000, seed=12)
+    AGt, ASt = gns.weight_matrices(b)
+    r = gns.gns_estimate_corrected([1.0] * 3, 1.0, b, rho=tau / c)
+    variants = {"thm1": (gns.optimal_weights(AGt), gns.optimal_weights(ASt)),
+                "uniform": (np.ones(3) / 3, np.ones(3) / 3),
+                "corrected": (r["wG"], r["wS"])}
+    var = {}
+    for k, (wg, ws) in variants.items():
+        Ge, Se = Gi @ wg, Si @ ws
+        T = len(Ge)
+        assert abs(Ge.mean() - 1.0) < 4 * Ge.std() / math.sqrt(T), k
+        assert abs(Se.mean() - 100.0) < 4 * Se.std() / math.sqrt(T), k
+        var[k] = (Ge.var(), Se.var())
+    assert var["corrected"][0] <= var["uniform"][0] * 1.002
+    assert var["corrected"][1] < var["uniform"][1] < var["thm1"][1]
+    assert var["corrected"][0] < var["thm1"][0]
+
+
+@pytest.mark.parametrize("b", [[32, 64, 96], [1, 2], [5, 5, 5, 90], [7, 300], [3, 9, 27, 81, 243]])
+@pytest.mark.parametrize("rho", [1e-6, 0.5, 50.0, 1e6])
+def test_corrected_weights_closed_form(b, rho):
+    """A_G (B - b) and A_S (B - b) are constant vectors (shown in DESIGN.md reading Q31), so the
+    corrected weights are w_i = (B - b_i) / ((n - 1) B) for G and S, whatever rho; the estimates
+    become the pooled forms G = (n B |g|^2 - sum b_i |g_i|^2) / ((n-1) B) and
+    S = (sum b_i |g_i|^2 - B |g|^2) / (n - 1)."""
+    B, n = sum(b), len(b)
+    w = (B - np.asarray(b, float)) / ((n - 1) * B)
+    rng = np.random.default_rng(len(b))
+    ls = list(1.0 + rng.random(n))
+    gs = 1.0 + 0.1 * float(rng.random())
+    r = gns.gns_estimate_corrected(ls, gs, b, rho=rho)
+    assert np.allclose(r["wG"], w, rtol=0, atol=1e-12) and np.allclose(r["wS"], w, rtol=0, atol=1e-12)
+    bl = sum(bi * x for bi, x in zip(b, ls))
+    assert math.isclose(r["G2"], (n * B * gs - bl) / ((n - 1) * B), rel_tol=1e-11, abs_tol=1e-12)
+    assert math.isclose(r["trS"], (bl - B * gs) / (n - 1), rel_tol=1e-10, abs_tol=1e-10)
+
+
+def test_corrected_first_order_limit_matches_theorem1_diagonal():
+    """At rho -> 0 (the delta-method limit) the corrected A_S diagonal is B b_i / (B - b_i): the
+    entry Theorem 1 prints; the off-diagonals differ (reading Q6)."""
+    b = [32, 64, 96]
+    _, AS0 = gns.corrected_matrices(b, 0.0)
+    B = sum(b)
+    for i, bi in enumerate(b):
+        assert math.isclose(AS0[i, i], B * bi / (B - bi), rel_tol=1e-14)
