@@ -99,6 +99,7 @@ SIGNATURES = {
     "cannikin_emulate_compute": (_I, [_D, _P]),
     "cannikin_trace": (_I, [_P, ctypes.POINTER(ctypes.c_uint64), _I, _IP]),
     "cannikin_gns_estimate": (_I, [_DP, _D, _LP, _I, ctypes.POINTER(_GnsResult)]),
+    "cannikin_gns_estimate_corrected": (_I, [_DP, _D, _LP, _I, ctypes.POINTER(_GnsResult)]),
     "cannikin_node_time": (_D, [ctypes.POINTER(_NodeModel), ctypes.POINTER(_CommModel), _D]),
     "cannikin_opt_split": (_I, [ctypes.POINTER(_NodeModel), _I, ctypes.POINTER(_CommModel), _L, _LP,
                                 _LP, _U, _LP, _DP, _DP, _IP]),
@@ -259,11 +260,12 @@ def get_unique_id() -> bytes:
 
 
 # ----------------------------------------------------------------------------- host solvers
-def gns_estimate(local_sq, global_sq: float, b) -> dict:
+def gns_estimate(local_sq, global_sq: float, b, corrected: bool = False) -> dict:
+    """Theorem 1 as printed (default), or the corrected-covariance variant (corrected=True)."""
     n = len(b)
     res = _GnsResult()
-    _check(lib().cannikin_gns_estimate(_dbl(local_sq), float(global_sq), _i64(b), n,
-                                       ctypes.byref(res)))
+    fn = lib().cannikin_gns_estimate_corrected if corrected else lib().cannikin_gns_estimate
+    _check(fn(_dbl(local_sq), float(global_sq), _i64(b), n, ctypes.byref(res)))
     return {"G2": res.G2, "trS": res.trS, "B_noise": res.B_noise, "Gi": list(res.Gi[:n]),
             "Si": list(res.Si[:n]), "wG": list(res.wG[:n]), "wS": list(res.wS[:n]),
             "flags": res.flags}

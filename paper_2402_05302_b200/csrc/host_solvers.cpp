@@ -146,6 +146,53 @@ extern "C" cannikin_status cannikin_gns_estimate(const double* local_sq, double 
   return CANNIKIN_OK;
 }
 
+// Corrected-covariance variant (reading Q31).  Under the paper's own
+// model (Eq. 1: g_i = mean of b_i iid N(G, Sigma) samples; Eq. 9: g = sum r_j g_j) the exact
+// covariance of the Eq. 10 estimators (Isserlis' theorem) satisfies A_G (B - b) = const and
+// A_S (B - b) = const, so the minimum-variance weights are w_i = (B - b_i) / ((n - 1) B) for both
+// G and S, independent of the unknown G and Sigma.
+extern "C" cannikin_status cannikin_gns_estimate_corrected(const double* local_sq,
+                                                           double global_sq, const int64_t* b,
+                                                           int n, cannikin_gns_result* out) {
+  if (!local_sq || !b || !out)
+    return fail(CANNIKIN_ERR_INVALID, "gns_estimate_corrected: NULL argument");
+  if (n < 2 || n > CANNIKIN_MAX_GNS_NODES)
+    return fail(CANNIKIN_ERR_INVALID, "gns_estimate_corrected: n=%d outside [2, %d]", n,
+                CANNIKIN_MAX_GNS_NODES);
+  int64_t Bi = 0;
+  for (int i = 0; i < n; ++i) {
+    if (b[i] < 1)
+      return fail(CANNIKIN_ERR_DOMAIN, "gns_estimate_corrected: b[%d]=%lld < 1", i, (long long)b[i]);
+    Bi += b[i];
+  }
+  for (int i = 0; i < n; ++i) {
+    if (b[i] >= Bi)
+      return fail(CANNIKIN_ERR_DOMAIN, "gns_estimate_corrected: b[%d] = B (Eq. 10 divides by B - b_i)", i);
+    if (!std::isfinite(local_sq[i]))
+      return fail(CANNIKIN_ERR_DOMAIN, "gns_estimate_corrected: local_sq[%d] not finite", i);
+  }
+  if (!std::isfinite(global_sq))
+    return fail(CANNIKIN_ERR_DOMAIN, "gns_estimate_corrected: global_sq not finite");
+  const double B = (double)Bi;
+  std::memset(out, 0, sizeof *out);
+  out->n = n;
+  double G = 0.0, S = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double bi = (double)b[i];
+    out->Gi[i] = (B * global_sq - bi * local_sq[i]) / (B - bi);       // Eq. 10
+    out->Si[i] = bi * B / (B - bi) * (local_sq[i] - global_sq);
+    out->wG[i] = out->wS[i] = (B - bi) / ((double)(n - 1) * B);
+    G += out->wG[i] * out->Gi[i];
+    S += out->wS[i] * out->Si[i];
+  }
+  out->G2 = G;
+  out->trS = S;
+  out->B_noise = S / G;
+  if (!(G > 0.0)) out->flags |= CANNIKIN_GNS_G_NONPOSITIVE;
+  cannikin::clear_error();
+  return CANNIKIN_OK;
+}
+
 // ============================================================================================
 // OptPerf split
 // ============================================================================================

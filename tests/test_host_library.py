@@ -210,6 +210,27 @@ def test_gns_estimate_vs_oracle():
         assert abs(sum(r["wG"]) - 1) < 1e-12 and abs(sum(r["wS"]) - 1) < 1e-12
 
 
+def test_gns_estimate_corrected_vs_oracle():
+    """The library's closed form against the oracle's general construction (matrix solve)."""
+    rng = np.random.default_rng(13)
+    for _ in range(300):
+        n = int(rng.integers(2, 17))
+        b = [int(x) for x in rng.integers(1, 300, size=n)]
+        gsq = float(rng.uniform(0.5, 3.0))
+        lsq = [gsq + float(rng.uniform(-0.2, 5.0)) for _ in range(n)]
+        r = ck.gns_estimate(lsq, gsq, b, corrected=True)
+        o = ogns.gns_estimate_corrected(lsq, gsq, b)
+        assert np.allclose(r["wG"], o["wG"], rtol=1e-9, atol=1e-11)
+        assert np.allclose(r["wS"], o["wS"], rtol=1e-9, atol=1e-11)
+        scaleG = sum(abs(w * g) for w, g in zip(o["wG"], o["Gi"])) + 1e-300
+        scaleS = sum(abs(w * s) for w, s in zip(o["wS"], o["Si"])) + 1e-300
+        assert abs(r["G2"] - o["G2"]) <= 1e-9 * scaleG
+        assert abs(r["trS"] - o["trS"]) <= 1e-9 * scaleS
+    with pytest.raises(ck.CannikinError) as e:
+        ck.gns_estimate([1.0, 1.0], 1.0, [5, 0], corrected=True)
+    assert e.value.name == "DOMAIN"
+
+
 def test_gns_estimate_flags_and_errors():
     r = ck.gns_estimate([5.0, 5.0], 0.0, [10, 10])   # G_i = -5 < 0
     assert r["flags"] & ck.GNS_G_NONPOSITIVE
