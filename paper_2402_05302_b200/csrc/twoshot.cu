@@ -1240,11 +1240,14 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
     if (try_oneshot(ctx, off, n, dt, r_i, st, &err)) return err;
   }
   {
-    // push (all-write) pays for large shards from 4 ranks up (+5% at W = 4, 256 MB-1 GB buckets;
-    // profiles/r01/k3_pull_dyn_push_n4.jsonl); pull is better for small buckets and W = 2
-    const size_t shard_bytes = n * (dt == CANNIKIN_F32 ? 4 : 2) / W;
+    // push (all-write) pays for large buckets from 4 ranks up (W = 4: equal at 64 MB, +5% at
+    // 256 MB-1 GB; profiles/r01/k3_pull_dyn_push_n4.jsonl); pull is better for small buckets and at
+    // W = 2.  The threshold is on the bucket, not the shard, so that W = 8 (not measurable here)
+    // sends C4's 220 MB bucket through the all-write pattern, which held up best under all-to-all
+    // load at W = 4 (profiles/r01/nvlink_bw_n4.jsonl)
+    const size_t bucket_bytes = n * (dt == CANNIKIN_F32 ? 4 : 2);
     if (ctx->ar_push == 2 && ctx->stage_off) return launch_pushdyn(ctx, off, n, dt, r_i, st);
-    const bool push = ctx->ar_push == 1 || (ctx->ar_push < 0 && W >= 4 && shard_bytes >= (32ull << 20));
+    const bool push = ctx->ar_push == 1 || (ctx->ar_push < 0 && W >= 4 && bucket_bytes >= (128ull << 20));
     if (push && ctx->stage_off) return launch_twoshot_push(ctx, off, n, dt, r_i, st);
   }
   ArArgs a{};
