@@ -56,8 +56,13 @@ def _stale(obj, srcs):
     return any(os.path.getmtime(s) > t for s in srcs)
 
 
+# CANNIKIN_NVCC_EXTRA: extra nvcc flags for build-time experiments (forces a rebuild)
+EXTRA = os.environ.get("CANNIKIN_NVCC_EXTRA", "").split()
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
     nvcc = _nvcc()
+    force = force or bool(EXTRA)
     nccl_inc, nccl_lib = _nccl_dirs()
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
@@ -71,7 +76,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if force or _stale(o, [s] + headers):
             jobs.append([nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v",
                          "-Xcompiler", "-fPIC,-ffp-contract=off", "--expt-relaxed-constexpr",
-                         "-I", INCLUDE, "-I", CSRC, "-I", nccl_inc, "-c", s, "-o", o])
+                         *EXTRA, "-I", INCLUDE, "-I", CSRC, "-I", nccl_inc, "-c", s, "-o", o])
     for src in HOST_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")

@@ -10,11 +10,18 @@ namespace dev {
 
 // ------------------------------------------------------------------ 16-byte memory operations
 // Streaming loads/stores: every gradient byte is touched exactly once per launch, so L1 is bypassed.
+// CANNIKIN_LD_HINT (build-time experiment): 1 = non-coherent path + L2 256-byte prefetch hint,
+// 2 = L2 256-byte prefetch hint only; default none.
+#if defined(CANNIKIN_LD_HINT) && CANNIKIN_LD_HINT == 1
+#define CANNIKIN_LD16 "ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+#elif defined(CANNIKIN_LD_HINT) && CANNIKIN_LD_HINT == 2
+#define CANNIKIN_LD16 "ld.global.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+#else
+#define CANNIKIN_LD16 "ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+#endif
 __device__ __forceinline__ uint4 ld16(const void* p) {
   uint4 v;
-  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
+  asm volatile(CANNIKIN_LD16 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
   return v;
 }
 __device__ __forceinline__ void st16(void* p, const uint4& v) {
