@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--grids", default="0,148,296,444,592,740,888")
     ap.add_argument("--altu-grids", default="0")
     ap.add_argument("--tma", type=int, default=1)
+    ap.add_argument("--tails", default="",
+                    help="CANNIKIN_K2_TAIL percentages (an experiment that was reverted; see DESIGN)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     want = args.shapes.split(",")
@@ -47,7 +49,11 @@ def main():
         variants = [("tma", None, 0, 1)] if args.tma else []
         variants += [("ldg", int(g), 0, dyn) for g in args.grids.split(",") for dyn in (1, 0)]
         variants += [("ldg", int(g), 1, 1) for g in args.altu_grids.split(",") if g]
+        if args.tails:
+            variants = [("ldg", 0, 0, -int(t) - 1) for t in args.tails.split(",")]
         for var, grid, altu, dyn in variants:
+            tail = -dyn - 1 if dyn < 0 else 0
+            os.environ["CANNIKIN_K2_TAIL"] = str(tail)
             if grid is not None:
                 os.environ["CANNIKIN_LOCAL_GRID"] = str(grid)
             os.environ["CANNIKIN_K2_NT"] = "1024" if altu else "256"
@@ -71,7 +77,8 @@ def main():
                 times += [a.elapsed_time(c) for a, c in evs]
             t = statistics.median(times)
             print(json.dumps({"shape": name, "ranks": nr, "N": N, "dtype": dt, "variant": var,
-                              "grid": grid, "alt_u": altu, "dyn": dyn, "ms": round(t, 4),
+                              "grid": grid, "alt_u": altu, "dyn": dyn, "tail_pct": tail,
+                              "ms": round(t, 4),
                               "GBps": round(nbytes / (t * 1e-3) / 1e9, 1)}), flush=True)
             del g
             ctx.close()
