@@ -50,30 +50,36 @@ def from_dev(t, dtype):
     return t.cpu().numpy()
 
 
-def full_case(ctx, rank, world, out):
-    """configs[3] at full size in the bench launch configuration (110M bf16, one zero-copy bucket):
-    saves sampled elements of every rank's input and of the result, this rank's full input
-    norm computed later by the oracle, and the statistics."""
-    N = 110_000_000
-    b = b_for(world, 9)
+FULL = {  # BASELINE configs at full size in the bench launch configuration: (N, dtype, seed)
+    "c4": (110_000_000, "bf16", 9),
+    "c5": (354_823_168, "f32", 19),
+}
+
+
+def full_case(ctx, rank, world, out, cfg):
+    """One BASELINE config at full size in the bench launch configuration (one zero-copy bucket,
+    default grid): saves sampled elements of every rank's input and of the result, the whole
+    inputs (rank 0, chunked, for the oracle norms) and the statistics."""
+    N, dt, seed = FULL[cfg]
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    b = b_for(world, seed)
     B = sum(b)
-    g = synth.device_gns_gradients(world, N, b, seed=9, dtype="bf16", ranks=[rank])[0]
-    bucket = ta.bucket_tensor(ctx, N, torch.bfloat16)
+    g = synth.device_gns_gradients(world, N, b, seed=seed, dtype=dt, ranks=[rank])[0]
+    bucket = ta.bucket_tensor(ctx, N, tdt)
     bucket.copy_(g)
     idx = torch.from_numpy(np.random.default_rng(0).choice(N, 200_000, replace=False)).cuda()
     ins = [torch.empty_like(g) for _ in range(world)]
     dist.all_gather(ins, g)  # plumbing: every rank's input of record, for the oracle on rank 0
     ta.weighted_allreduce(ctx, bucket, b[rank] / B)
     loc, glob = ctx.gns_stats()
-    res = {"idx": idx.cpu().numpy(), "out": from_dev(bucket[idx], "bf16"),
-           "ins": np.stack([from_dev(x[idx], "bf16") for x in ins]), "loc": np.array(loc),
+    res = {"idx": idx.cpu().numpy(), "out": from_dev(bucket[idx], dt),
+           "ins": np.stack([from_dev(x[idx], dt) for x in ins]), "loc": np.array(loc),
            "glob": glob, "b": np.array(b)}
     if rank == 0:
-        # the whole inputs, chunked, for the oracle norms
         chunk = 10_000_000
         for a in range(0, N, chunk):
-            np.save(os.path.join(out, f"full_in_{a}.npy"),
-                    np.stack([from_dev(x[a:a + chunk], "bf16") for x in ins]))
+            np.save(os.path.join(out, f"full_in_{a:012d}.npy"),
+                    np.stack([from_dev(x[a:a + chunk], dt) for x in ins]))
     np.savez(os.path.join(out, f"rank{rank}_full.npz"), **res)
     ta.free_bucket_tensor(ctx, bucket)
     del ins, g
@@ -83,7 +89,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", required=True)
     ap.add_argument("--grid", type=int, default=0)
-    ap.add_argument("--full", action="store_true")
+    ap.add_argument("--full", default="", choices=["", "c4", "c5"])
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr = int(os.environ.get("LOCAL_RANK", rank))
@@ -91,8 +97,10 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     maxN = max(c[1] for c in CASES)
     if args.full:
-        ctx = ta.init_distributed_context(heap_bytes=110_000_000 * 2 + 4096, grid=args.grid)
-        full_case(ctx, rank, world, args.out)
+        N, dt, _ = FULL[args.full]
+        ctx = ta.init_distributed_context(heap_bytes=N * (2 if dt == "bf16" else 4) + 4096,
+                                          grid=args.grid)
+        full_case(ctx, rank, world, args.out, args.full)
         dist.barrier()
         ctx.close()
         dist.destroy_process_group()

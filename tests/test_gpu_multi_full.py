@@ -1,8 +1,10 @@
-"""Multi-GPU parity at configs[3]'s full size (110M bf16) in the bench launch configuration
-(zero-copy heap bucket, default grid): sampled elements against the oracle one by one, the norm
-statistics against the oracle over the whole vectors, identical statistics on every rank."""
+"""Multi-GPU parity at full size in the bench launch configuration (zero-copy heap bucket, default
+grid) for configs[3] (110M bf16) and configs[4] (355M fp32, one 1.42 GB bucket): sampled elements
+against the oracle one by one, the norm statistics against the oracle over the whole vectors,
+identical statistics on every rank."""
 import glob
 import os
+import shutil
 import socket
 import subprocess
 import sys
@@ -25,32 +27,44 @@ def _port():
     return p
 
 
-def test_full_size_c4_multi():
+TOL = {"c4": ("bf16", 1e-2), "c5": ("f32", 1e-5)}
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_full_size_multi(cfg):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
     world = min(torch.cuda.device_count(), 8)
     d = tempfile.mkdtemp()
+    try:
+        _run_and_check(cfg, world, d)
+    finally:
+        shutil.rmtree(d, ignore_errors=True)  # the whole inputs: up to 5.7 GB
+
+
+def _run_and_check(cfg, world, d):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
-           os.path.join(os.path.dirname(__file__), "mp_allreduce_worker.py"), "--out", d, "--full"]
+           os.path.join(os.path.dirname(__file__), "mp_allreduce_worker.py"), "--out", d, "--full", cfg]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,
                        env=dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000"))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     ranks = [dict(np.load(os.path.join(d, f"rank{k}_full.npz"))) for k in range(world)]
     b = [int(x) for x in ranks[0]["b"]]
     rr = agg.ratios(b)
-    ins = [agg.to_f64(x, "bf16") for x in ranks[0]["ins"]]
+    dt, tol = TOL[cfg]
+    ins = [agg.to_f64(x, dt) for x in ranks[0]["ins"]]
     ref = agg.weighted_sum(ins, rr)
     scale = np.maximum(agg.elementwise_scale(ins, rr), 1e-30)
     for k in range(world):
-        got = agg.to_f64(ranks[k]["out"], "bf16")
-        assert np.max(np.abs(got - ref) / scale) <= 1e-2
+        got = agg.to_f64(ranks[k]["out"], dt)
+        assert np.max(np.abs(got - ref) / scale) <= tol
         assert np.array_equal(ranks[k]["loc"], ranks[0]["loc"])
         assert float(ranks[k]["glob"]) == float(ranks[0]["glob"])
     lsum = np.zeros(world)
     gsum = 0.0
     for f in sorted(glob.glob(os.path.join(d, "full_in_*.npy"))):
-        parts = [agg.to_f64(x, "bf16") for x in np.load(f)]
+        parts = [agg.to_f64(x, dt) for x in np.load(f)]
         for j in range(world):
             lsum[j] += agg.sq_norm(parts[j])
         gsum += agg.sq_norm(agg.weighted_sum(parts, rr))
