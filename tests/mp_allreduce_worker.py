@@ -27,7 +27,8 @@ CASES = [  # (name, N, dtype, seed)
     ("mid_f32", (1 << 20) + 3, "f32", 4),
     ("mid_bf16", (1 << 20) + 5, "bf16", 5),
     ("big_bf16", 3_000_011, "bf16", 6),
-    ("resnet18", 11_689_512, "f32", 7),
+    ("resnet18", 11_689_512, "f32", 7),    # configs[1]
+    ("resnet50", 25_557_032, "f32", 11),   # configs[2]
     ("os_f32", 300_001, "f32", 8),     # one-shot sized: several CTAs, ragged tail
     ("os_bf16", 600_007, "bf16", 10),
 ]
