@@ -319,11 +319,50 @@ def cpu_baseline(cfg, n, seconds=10.0, sample_elems=1 << 22):
         if el >= seconds:
             break
     nbytes = (n + 1) * sample_elems * esize(cfg["dtype"])
-    return {"value": round(nbytes * calls / el / 1e9, 4), "unit": "GB/s", "cores": 1,
-            "kind": "oracle",
-            "sample": f"{calls} oracle passes over {n} ranks x {sample_elems} {cfg['dtype']} "
-                      f"elements (first 2^22 of the workload shape), {el:.1f} s, numpy float64 "
-                      "single-threaded"}
+    out = {"value": round(nbytes * calls / el / 1e9, 4), "unit": "GB/s", "cores": 1,
+           "kind": "oracle",
+           "sample": f"{calls} oracle passes over {n} ranks x {sample_elems} {cfg['dtype']} "
+                     f"elements (first 2^22 of the workload shape), {el:.1f} s, numpy float64 "
+                     "single-threaded"}
+    out["all_cores"] = cpu_baseline_all_cores(cfg, n, gs, r)
+    return out
+
+
+def _oracle_chunk_worker(args):
+    """One process: the oracle's Eq. 9 + norms over a fixed chunk, repeated for `seconds`."""
+    gs, r, dtype, seconds = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import aggregate as agg
+
+    calls, t0 = 0, time.perf_counter()
+    while True:
+        agg.aggregate(gs, r, dtype)
+        calls += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return calls, el
+
+
+def cpu_baseline_all_cores(cfg, n, gs, r, seconds=5.0, chunk=1 << 18):
+    """SURVEY §8(d) oracle timing (b): the same oracle over fixed chunks on every host core at
+    once (one process per core, chunk boundaries fixed, results identical); GB/s summed."""
+    import multiprocessing as mp
+
+    cores = max(1, min(os.cpu_count() or 1, 128))
+    N = len(gs[0])
+    bounds = [(a, min(a + chunk, N)) for a in range(0, N, chunk)]
+    jobs = [([g[a:c] for g in gs], r, cfg["dtype"], seconds)
+            for k, (a, c) in enumerate(bounds * ((cores + len(bounds) - 1) // len(bounds)))][:cores]
+    try:
+        with mp.get_context("fork").Pool(cores) as pool:
+            res = pool.map(_oracle_chunk_worker, jobs)
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)[:200]}
+    es = esize(cfg["dtype"])
+    gbps = sum((n + 1) * len(j[0][0]) * es * c / el for j, (c, el) in zip(jobs, res)) / 1e9
+    return {"value": round(gbps, 3), "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "sample": f"{cores} processes, each the oracle's Eq. 9 + norms over a fixed "
+                      f"{chunk}-element chunk of the same {n}-rank sample for {seconds:.0f} s"}
 
 
 def run_reference(args, cfg, rank, world):
