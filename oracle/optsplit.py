@@ -25,6 +25,8 @@ Solutions:
 * ``int_split_greedy`` -- the integer optimum of Eq. 7: starting at lo, hand out the B - sum(lo)
   samples one at a time to argmin_i (f_i(b_i + 1), i).  Integer batches are required.
 * ``int_split_brute`` -- exhaustive enumeration (tiny n, B) with the canonical tie-break.
+* ``algorithm1``   -- Alg. 1 literally, as a cross-check of ``real_split`` (its node-fixing
+  rule is unsound, so it can fail).
 * ``round_paper``  -- the paper's own integer rule: round the real split, implemented
   as largest-remainder with ties to the lower index.
 * ``warmup_split`` -- Eq. 8 (P:317-324).
@@ -156,6 +158,96 @@ def real_split(nodes, comm, B: int, lo=None, cap=None):
     T = cluster_time(nodes, comm, b)
     labels = [1 if is_compute_bound(nodes[i], comm, b[i]) else 0 for i in range(n)]
     return b, T, labels
+
+
+# ----------------------------------------------------------------------------- Algorithm 1, literally
+def _solve_equal(lines, B: float):
+    """Solve slope_i b_i + c_i = t for every i with sum_i b_i = B (unclamped):
+    t = (B + sum_i c_i / slope_i) / sum_i (1 / slope_i),  b_i = (t - c_i) / slope_i."""
+    num = float(B)
+    den = 0.0
+    for a, c in lines:
+        num += c / a
+        den += 1.0 / a
+    t = num / den
+    return t, [(t - c) / a for a, c in lines]
+
+
+def breakpoint_time(node, comm) -> float:
+    """T_i* = f_i(b_i^bp), b_i^bp = (T_o / (1 - gamma) - m_i) / k_i: the node's time where it turns
+    compute-bound.  The ranking key of the mixed search (reading Q14)."""
+    q, s, k, m = node
+    gamma, t_o, _ = comm
+    if k <= 0.0:
+        return math.inf if (1.0 - gamma) * m < t_o else -math.inf
+    return node_time(node, comm, (t_o / (1.0 - gamma) - m) / k)
+
+
+def algorithm1(nodes, comm, B: float):
+    """PAPER.md Algorithm 1, step by step, on the relaxation (real b, no bounds).
+
+    Check 1: solve t_compute^0 = ... = t_compute^{n-1} with sum b = B; if every node is
+      compute-bound ((1 - gamma) P_i >= T_o, P:191) return OptPerf = t_compute + T_u.
+    Check 2: solve syncStart_0 = ... = syncStart_{n-1}; if every node is comm-bound
+      return OptPerf = syncStart + T_comm.
+    Mixed: a node with the same state in Check 1 and Check 2 keeps it; the
+      other "outliers" are ranked by their breakpoint time (reading Q14: the undefined "fixed
+      processing time"), nodes before the boundary C are computing-bottleneck, the rest
+      communication-bottleneck; for each candidate boundary solve
+      T_comb = t_compute' = syncStart' + T_o (P:301) and test
+      (forall syncStart_i <= syncStart') and (forall t_compute_i <= t_compute'); the
+      boundary moves by bisection (reading Q16: a comm-labelled node that is really compute-bound
+      moves it up, a compute-labelled node that is really comm-bound moves it down).
+      OptPerf = T_comb + T_u (P:303).
+    Returns {"b", "T", "case", "labels"} or None when no boundary gives a consistent state (the
+    fixing rule of P:310 is unsound: the exact solver is ``real_split``)."""
+    _check_models(nodes, comm)
+    gamma, t_o, t_u = comm
+    n = len(nodes)
+    comp_line = [(q + k, s + m) for q, s, k, m in nodes]               # t_compute_i = a b + c
+    sync_line = [(q + gamma * k, s + gamma * m) for q, s, k, m in nodes]  # syncStart_i = a b + c
+
+    def state(i, b):
+        return is_compute_bound(nodes[i], comm, b)
+
+    # Check 1
+    t1, b1 = _solve_equal(comp_line, B)
+    lab1 = [state(i, b1[i]) for i in range(n)]
+    if all(lab1):
+        return {"b": b1, "T": t1 + t_u, "case": "compute", "labels": [1] * n}
+    # Check 2
+    s2, b2 = _solve_equal(sync_line, B)
+    lab2 = [state(i, b2[i]) for i in range(n)]
+    if not any(lab2):
+        return {"b": b2, "T": s2 + t_o + t_u, "case": "comm", "labels": [0] * n}
+    # mixed-bottleneck search
+    fixed = {i: lab1[i] for i in range(n) if lab1[i] == lab2[i]}
+    outliers = sorted((i for i in range(n) if lab1[i] != lab2[i]),
+                      key=lambda i: (breakpoint_time(nodes[i], comm), i))
+    beg, end = 0, len(outliers)
+    while beg <= end:
+        C = (beg + end) // 2
+        is_comp = dict(fixed)
+        for j, i in enumerate(outliers):
+            is_comp[i] = j < C
+        # T_comb = t_compute' = syncStart' + T_o: compute nodes a b + c = T_comb, comm nodes
+        # a' b + c' + T_o = T_comb
+        lines = [comp_line[i] if is_comp[i] else (sync_line[i][0], sync_line[i][1] + t_o)
+                 for i in range(n)]
+        t_comb, b = _solve_equal(lines, B)
+        up = any((not is_comp[i]) and compute_time(nodes[i], b[i]) > t_comb for i in range(n))
+        down = any(is_comp[i] and sync_start(nodes[i], comm, b[i]) > t_comb - t_o
+                   for i in range(n))
+        if not up and not down:
+            return {"b": b, "T": t_comb + t_u, "case": "mixed",
+                    "labels": [1 if is_comp[i] else 0 for i in range(n)]}
+        if up and down:
+            return None
+        if up:
+            beg = C + 1
+        else:
+            end = C - 1
+    return None
 
 
 # ----------------------------------------------------------------------------- integer splits

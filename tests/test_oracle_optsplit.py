@@ -185,3 +185,63 @@ def test_errors():
         osp.int_split_greedy([(0.0, 0.01, 0.0, 0.02)] * 2, (0.3, 0.05, 0.01), 10)
     with pytest.raises(ValueError):
         osp.int_split_greedy(nodes, (0.3, 0.05, 0.01), 10, cap=[3, 3])
+
+
+# ------------------------------------------------------------- Algorithm 1, literally
+def test_algorithm1_checks_hand_values(golden):
+    """Alg. 1's Check 1 / Check 2 on SPEC's worked examples."""
+    ex = golden["solve_equal_compute"]
+    r = osp.algorithm1(ex["nodes"], ex["comm"], ex["B"])
+    assert r["case"] == "compute"
+    assert np.allclose(r["b"], ex["b"], rtol=1e-12)
+    assert math.isclose(r["T"], ex["t"] + ex["comm"][2], rel_tol=1e-12)
+    ex = golden["solve_equal_syncstart"]
+    r = osp.algorithm1(ex["nodes"], ex["comm"], ex["B"])
+    assert r["case"] == "comm"
+    assert np.allclose(r["b"], ex["b"], rtol=1e-12)
+    assert math.isclose(r["T"], ex["sync_start"] + ex["comm"][1] + ex["comm"][2], rel_tol=1e-12)
+
+
+def test_algorithm1_counterexample_fixing_rule():
+    """node 2 is comm-bound in Check 1 AND Check 2, so Alg. 1 fixes it as
+    comm-bound, but at the optimum it is compute-bound -- no boundary is consistent.
+    The exact solver finds b = [36.24, 43.53, 11.23], T = 0.532255 with node 2 compute-bound."""
+    comm = (0.1351, 0.2802, 0.0504)
+    nodes = [(0.0031, 0.0833, 0.0012, 0.001), (0.0015, 0.001, 0.0094, 0.0064),
+             (0.0041, 0.0841, 0.0311, 0.0024)]
+    assert osp.algorithm1(nodes, comm, 91) is None
+    b, T, labels = osp.real_split(nodes, comm, 91, lo=[0, 0, 0])
+    assert np.allclose(b, [36.24, 43.53, 11.23], atol=0.01)
+    assert abs(T - 0.532255) < 1e-6 and labels[2] == 1
+
+
+def test_algorithm1_agrees_with_exact_split_whenever_it_answers():
+    """On random mixed clusters the literal Alg. 1, when it answers, equals the exact relaxation
+    (same b and OptPerf); when it fails, the cause is always the P:310 fixing rule: some node with
+    the same state in Check 1 and Check 2 has the other state at the optimum."""
+    import random
+    rng = random.Random(5)
+    answered = failed = 0
+    for _ in range(600):
+        n = rng.randint(2, 6)
+        comm = (rng.uniform(0, 0.9), rng.uniform(0, 0.5), rng.uniform(0, 0.1))
+        nodes = [(rng.uniform(1e-4, 5e-3), rng.uniform(0, 0.1), rng.uniform(1e-4, 4e-2),
+                  rng.uniform(0, 0.01)) for _ in range(n)]
+        B = rng.randint(10 * n, 200)
+        b, T, labels = osp.real_split(nodes, comm, B, lo=[0] * n)
+        if min(b) <= 1e-9:
+            continue  # Alg. 1 works on the unbounded relaxation; skip clamped optima
+        r = osp.algorithm1(nodes, comm, B)
+        if r is None:
+            failed += 1
+            lab = []
+            for line in ([(q + k, s + m) for q, s, k, m in nodes],
+                         [(q + comm[0] * k, s + comm[0] * m) for q, s, k, m in nodes]):
+                _, bb = osp._solve_equal(line, B)
+                lab.append([osp.is_compute_bound(nodes[i], comm, bb[i]) for i in range(n)])
+            assert any(lab[0][i] == lab[1][i] and int(lab[0][i]) != labels[i] for i in range(n))
+            continue
+        answered += 1
+        assert math.isclose(r["T"], T, rel_tol=1e-9)
+        assert np.allclose(r["b"], b, rtol=1e-7, atol=1e-7)
+    assert answered > 10 * max(failed, 1)
