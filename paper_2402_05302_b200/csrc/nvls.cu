@@ -9,7 +9,8 @@
 //   B. rank k pulls the in-switch sum of its shard, sum_j y_j = multimem.ld_reduce(mc + e)
 //      (fp32 accumulation in the switch), accumulates |g|^2 and writes the result to every
 //      rank's copy with one multimem.st;
-//   C. per-CTA norm partials to every peer's pad, exit barrier, fixed-order final sum.
+//   C. per-CTA norm partials to every peer's pad, exit barrier;
+//   D. CTA b adds the W rows b to its running statistics row (fixed rank order).
 // NVLink bytes per rank and direction ~ (1 + 1/W) N s instead of the two-shot's 2 (W-1)/W N s
 // (1.125 vs 1.75 at W = 8), at the price of a local N s read + write in phase A.
 // The piece of every shard that CTA b scales in phase A is exactly the piece CTA b of the shard's
@@ -91,10 +92,9 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const McArgs a, int W) {
   constexpr int E = V::E;
   constexpr int UA = 4;  // phase A: vectors in flight per thread
   constexpr int R = 4;   // phase B: in-switch reductions in flight per thread
-  __shared__ double red[32 * (kMaxWorld + 1)];
+  __shared__ double red[32 * 2];
   __shared__ double s_part[2];
   __shared__ uint64_t s_ep;
-  __shared__ bool s_last;
   const int b = blockIdx.x, tid = threadIdx.x, G = gridDim.x, NT = blockDim.x;
   auto shard_len = [&](int k) -> size_t { return (k == W - 1) ? a.nvec - a.L * (W - 1) : a.L; };
   // one epoch per call for every CTA (the mid barrier compares flags across CTA indices, so a
@@ -211,29 +211,24 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const McArgs a, int W) {
     mc::wait_at_least(&a.ctrl->nv_exit[b][tid], ep, a.ctrl, a.timeout_ns, 5);
   }
   __syncthreads();
+  // ---- D. CTA b holds every rank's row b: add them in rank order to its running row (as K3's
+  // static variant; cannikin_gns_stats sums the rows in CTA order).  The call epoch advances
+  // when the last CTA is done (every CTA read the old value at its start).
   if (tid == 0) {
     a.ctrl->trace[b][3] = dev::globaltimer_ns();
-    __threadfence();
-    s_last = (atomicAdd(&a.ctrl->ticket_ar, 1u) == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  double tot[kMaxWorld + 1];
-#pragma unroll
-  for (int j = 0; j <= kMaxWorld; ++j) tot[j] = 0.0;
-  for (int i = tid; i < W * G; i += NT) {
-    const int src = i / G, cta = i - src * G;
-    const double* row = &a.ctrl->part[src][cta][0];
-    for (int j = 0; j <= W; ++j) tot[j] += __ldcg(row + j);
-  }
-  dev::block_sum<kMaxWorld + 1>(tot, red);
-  if (tid == 0) {
-    for (int j = 0; j <= W; ++j) a.ctrl->stats[j] += tot[j];
-    a.ctrl->ticket_ar = 0u;
-    a.ctrl->nv_epoch = ep;  // every CTA read the old value at its start
+    double* acc = a.ctrl->cta_acc[b];
+    for (int j = 0; j <= W; ++j) {
+      double t = 0.0;
+      for (int src = 0; src < W; ++src) t += __ldcg(&a.ctrl->part[src][b][j]);
+      acc[j] = __ldcg(&acc[j]) + t;
+    }
     a.ctrl->trace[b][4] = dev::globaltimer_ns();
-    a.ctrl->trace_grid = G;
+    __threadfence();
+    if (atomicAdd(&a.ctrl->ticket_ar, 1u) == gridDim.x - 1) {
+      a.ctrl->ticket_ar = 0u;
+      a.ctrl->nv_epoch = ep;
+      a.ctrl->trace_grid = G;
+    }
   }
 }
 

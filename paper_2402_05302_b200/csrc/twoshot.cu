@@ -760,7 +760,10 @@ __global__ void __launch_bounds__(512, 1) twoshot_push_kernel(const PushArgs a) 
 #pragma unroll
   for (int j = 0; j < W; ++j) {
     r[j] = s_r[j];
-    dstb[j] = a.bucket[j];
+    // destinations in staggered order (rank+1, rank+2, ...), rotated ONCE here so that the store
+    // loop indexes the array statically (a per-vector (rank + jj) % W index spills it to local
+    // memory)
+    dstb[j] = a.bucket[(a.rank + j) % W];
     src[j] = (j == a.rank) ? a.bucket[a.rank] + lo * 16
                            : a.stage[a.rank] + (size_t)j * a.slot_vec * 16;
   }
@@ -792,10 +795,7 @@ __global__ void __launch_bounds__(512, 1) twoshot_push_kernel(const PushArgs a) 
     gsq += (double)gs;
     const uint4 y = V::pack(acc);
 #pragma unroll
-    for (int jj = 0; jj < W; ++jj) {
-      const int j = (a.rank + jj) % W;
-      dev::st16(dstb[j] + v * 16, y);
-    }
+    for (int jj = 0; jj < W; ++jj) dev::st16(dstb[jj] + v * 16, y);
   }
   // ragged element tail: the last rank's CTA 0 reduces it straight from the peers' buckets
   // (after the mid barrier every rank's tail elements are still unchanged source data)
@@ -806,12 +806,12 @@ __global__ void __launch_bounds__(512, 1) twoshot_push_kernel(const PushArgs a) 
         float acc = 0.0f;
 #pragma unroll
         for (int j = 0; j < W; ++j) {
-          const float g = V::load1(dstb[j] + e * sizeof(T));
+          const float g = V::load1(a.bucket[j] + e * sizeof(T));
           acc = fmaf(r[j], g, acc);
         }
         gsq += (double)(acc * acc);
 #pragma unroll
-        for (int j = 0; j < W; ++j) V::store1(dstb[j] + e * sizeof(T), acc);
+        for (int j = 0; j < W; ++j) V::store1(a.bucket[j] + e * sizeof(T), acc);
       }
     }
   }
@@ -1051,11 +1051,13 @@ __global__ void __launch_bounds__(kArThreads, 1) pushdyn_kernel(const PushDynArg
       if (a.check_r && c == 0 && tid == 0) check_ratios<W>(s_r, a.ctrl);
       float r[W];
       const char* src[W];
+      char* dst_rot[W];  // staggered destination order, rotated once (static index in the loop)
       const size_t slo = lo_of(me);
 #pragma unroll
       for (int j = 0; j < W; ++j) {
         r[j] = s_r[j];
         src[j] = (j == me) ? mine + slo * 16 : a.stage[me] + (size_t)j * a.slot_vec * 16;
+        dst_rot[j] = a.bucket[(me + j) % W];
       }
       const size_t lo = slo + (size_t)c * a.chunk;
       const size_t hi = (lo + a.chunk < hi_of(me)) ? lo + a.chunk : hi_of(me);
@@ -1086,10 +1088,7 @@ __global__ void __launch_bounds__(kArThreads, 1) pushdyn_kernel(const PushDynArg
         gsq += (double)gs;
         const uint4 y = V::pack(acc);
 #pragma unroll
-        for (int jj = 0; jj < W; ++jj) {
-          const int j = (me + jj) % W;
-          dev::st16(a.bucket[j] + v * 16, y);
-        }
+        for (int jj = 0; jj < W; ++jj) dev::st16(dst_rot[jj] + v * 16, y);
       }
       // the ragged element tail: owned by the last rank, with its last chunk; every peer's flag
       // for that chunk has arrived, so every peer has read its own tail (and its bucket is ready)
