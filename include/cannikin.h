@@ -114,9 +114,14 @@ cannikin_status cannikin_free_bucket(cannikin_ctx* ctx, void* dptr);
  *   r_i    : this rank's share b_i / B.  Trusted (not re-normalised).
  * Side effect: the norm statistics of this bucket -- |g_j|^2 restricted to the bucket for every
  * rank j, and |g|^2 restricted to the bucket -- are added (fixed bucket order) to the ctx
- * accumulator that cannikin_gns_stats reads.  Implementation: two-shot reduce-scatter/all-gather
- * over NVLink peer memory with the scaling, the fp32 accumulation, both norms and the partial
- * exchange fused into one kernel.  world == 1: g = r_0 g_0 in place.
+ * accumulator that cannikin_gns_stats reads.  Implementation: one kernel over NVLink peer memory
+ * with the scaling, the fp32 accumulation in rank order, both norms and the partial exchange
+ * fused (DESIGN.md §6 K3).  Variant by size (a function of n, dt, world and grid only, so every
+ * rank picks the same): one-shot (world 2, <= 2 x 256 KiB: every rank reads every peer's bucket),
+ * two-shot pull (static, or dynamic chunks for shards >= 64 MiB), two-shot push (world >= 4,
+ * buckets >= 128 MiB: every NVLink transfer a write); CANNIKIN_AR_* environment knobs force one.
+ * The result bits do not depend on the variant; the statistics' summation grouping does.
+ * world == 1: g = r_0 g_0 in place.
  * Errors: INVALID (NULL, misaligned, too large), UNSUPPORTED (dtype), CUDA. */
 cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* bucket, size_t n,
                                             cannikin_dtype dt, double r_i, void* stream);
