@@ -91,12 +91,34 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--full", default="", choices=["", "c4", "c5"])
+    ap.add_argument("--variants", action="store_true")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(lr)
     dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     maxN = max(c[1] for c in CASES)
+    if args.variants:
+        # the same inputs through every K3 variant: the result bits must not depend on it
+        VARS = {"static": ("0", "0", "0"), "dyn": ("1", "0", "0"), "push": ("0", "1", "0"),
+                "pushdyn": ("0", "2", "0"), "oneshot": ("0", "0", "1")}
+        for name, (dyn, push, one) in VARS.items():
+            os.environ.update(CANNIKIN_AR_DYN=dyn, CANNIKIN_AR_PUSH=push, CANNIKIN_AR_ONESHOT=one,
+                              CANNIKIN_PD_CHUNK_KB="16")
+            ctx = ta.init_distributed_context(heap_bytes=(1 << 22), grid=args.grid)
+            for N, dtype in ((100_003, "f32"), (200_011, "bf16")):
+                b = b_for(world, 21)
+                gs = synth.gns_gradients(world, N, b, seed=21, dtype=dtype)
+                t = ta.bucket_tensor(ctx, N, {"f32": torch.float32, "bf16": torch.bfloat16}[dtype])
+                t.copy_(to_dev(gs[rank], dtype))
+                ta.weighted_allreduce(ctx, t, b[rank] / sum(b))
+                ctx.gns_stats()
+                np.save(os.path.join(args.out, f"rank{rank}_var_{name}_{dtype}.npy"), from_dev(t, dtype))
+                ta.free_bucket_tensor(ctx, t)
+            dist.barrier()
+            ctx.close()
+        dist.destroy_process_group()
+        return
     if args.full:
         N, dt, _ = FULL[args.full]
         ctx = ta.init_distributed_context(heap_bytes=N * (2 if dt == "bf16" else 4) + 4096,

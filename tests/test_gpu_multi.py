@@ -105,3 +105,25 @@ def test_check_ratios(results):
         assert list(st) == ["OK", "DOMAIN", "OK"], (r, st)
         val = np.load(os.path.join(d, f"rank{r}_check_ratios_val.npy"))
         assert np.allclose(val, [1.0, 0.95, 1.0], rtol=1e-6), (r, val)
+
+
+def test_result_bits_independent_of_variant():
+    """Every K3 variant (static / dynamic pull, static / dynamic push, one-shot) sums
+    fmaf(r_j, g_j, acc) in rank order in fp32 and rounds once: identical result bits."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(torch.cuda.device_count(), 8)
+    d = tempfile.mkdtemp()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           os.path.join(os.path.dirname(__file__), "mp_allreduce_worker.py"), "--out", d,
+           "--variants"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000"))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    for dtype in ("f32", "bf16"):
+        ref = np.load(os.path.join(d, f"rank0_var_static_{dtype}.npy"))
+        for name in ("static", "dyn", "push", "pushdyn", "oneshot"):
+            for k in range(world):
+                got = np.load(os.path.join(d, f"rank{k}_var_{name}_{dtype}.npy"))
+                assert np.array_equal(got, ref), (name, dtype, k)
