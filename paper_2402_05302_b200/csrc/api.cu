@@ -92,6 +92,7 @@ extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world
   ctx->user_off = ctx->ctrl_bytes;
   ctx->scratch_off = ctx->user_off + ctx->heap_bytes;
   ctx->total_bytes = ctx->scratch_off + (world > 1 ? ctx->heap_bytes : 0);
+  if (const char* t = std::getenv("CANNIKIN_AR_CHUNK")) ctx->ar_chunk_max = std::max(512, std::atoi(t));
   if (const char* t = std::getenv("CANNIKIN_OS_VPT")) ctx->os_vpt = std::atoi(t) >= 2 ? 2 : 1;
   if (const char* t = std::getenv("CANNIKIN_AR_ONESHOT")) ctx->ar_oneshot = std::atoi(t) != 0;
   if (const char* t = std::getenv("CANNIKIN_AR_PUSH")) {

@@ -53,6 +53,7 @@ struct cannikin_ctx {
   int pd_chunk_kb = 256;    // CANNIKIN_PD_CHUNK_KB: dynamic-push chunk (grown to fit the row table)
   int check_ratios = 0;     // CANNIKIN_INIT_CHECK_RATIOS
   int os_vpt = 2;           // CANNIKIN_OS_VPT=1|2: one-shot vectors per thread (sets its grid)
+  int ar_chunk_max = 512 * 16;  // CANNIKIN_AR_CHUNK: dynamic two-shot max chunk (16-B vectors)
   int ar_oneshot = -1;      // CANNIKIN_AR_ONESHOT=0|1 forbids/prefers one-shot; -1 = by size
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2
   bool local_tma = false;   // default variant of K2 (CANNIKIN_K2_IMPL=tma|ldg)

@@ -1281,7 +1281,7 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
   const bool dyn = ctx->ar_dyn < 0 ? (L * 16 >= (64ull << 20)) : (ctx->ar_dyn != 0);
   // ~4 chunks per CTA, between one vector per thread and 16 per thread, <= kMaxArChunks-1 chunks
   size_t chunk = (L + (size_t)grid * 4 - 1) / ((size_t)grid * 4);
-  if (chunk > (size_t)kArThreads * 16) chunk = (size_t)kArThreads * 16;
+  if (chunk > (size_t)ctx->ar_chunk_max) chunk = (size_t)ctx->ar_chunk_max;
   const size_t need = (L + kMaxArChunks - 2) / (kMaxArChunks - 1);
   if (need > chunk) chunk = need;
   chunk = (chunk + kArThreads - 1) / kArThreads * kArThreads;

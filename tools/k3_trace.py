@@ -19,17 +19,24 @@ def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
     dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank))))
-    N = 64 << 20
+    bf16 = "--bf16" in sys.argv
+    tdt, es = (torch.bfloat16, 2) if bf16 else (torch.float32, 4)
+    sizes = [0.004, 0.0625, 1, 4, 16, 64, 256]
+    for a in sys.argv:
+        if a.startswith("--sizes="):
+            sizes = [float(x) for x in a.split("=", 1)[1].split(",")]
+    N = max(64 << 20, int(max(sizes) * 2**20) // es + 64)
     dyn = os.environ.get("CANNIKIN_AR_DYN", "0")
     use_nvls = "--nvls" in sys.argv
     mcb = ta.McBucket(N, torch.float32) if use_nvls else None
     if mcb is not None:
         mcb.tensor.normal_()
-    ctx = ta.init_distributed_context(heap_bytes=N * 4)
-    bucket = ta.bucket_tensor(ctx, N, torch.float32)
+    ctx = ta.init_distributed_context(heap_bytes=N * es)
+    bucket = ta.bucket_tensor(ctx, N, tdt)
     bucket.normal_()
-    for mb in [0.004, 0.0625, 1, 4, 16, 64, 256]:
-        n = max(8, int(mb * 2**20) // 4)
+    for mb in sizes:
+        n = max(8, int(mb * 2**20) // es)
+        n -= n % 8
         def op():
             if mcb is not None:
                 ta.weighted_allreduce_nvls(ctx, mcb, 1.0 / world, view=mcb.tensor[:n])
