@@ -117,9 +117,11 @@ cannikin_status cannikin_free_bucket(cannikin_ctx* ctx, void* dptr);
  * accumulator that cannikin_gns_stats reads.  Implementation: one kernel over NVLink peer memory
  * with the scaling, the fp32 accumulation in rank order, both norms and the partial exchange
  * fused (DESIGN.md §6 K3).  Variant by size (a function of n, dt, world and grid only, so every
- * rank picks the same): one-shot (world 2, <= 2 x 256 KiB: every rank reads every peer's bucket),
- * two-shot pull (static, or dynamic chunks for shards >= 64 MiB), two-shot push (world >= 4,
- * buckets >= 128 MiB: every NVLink transfer a write); CANNIKIN_AR_* environment knobs force one.
+ * rank picks the same): low-latency LL (<= 2 MiB / (world-1): data and flag in one 8-byte NVLink
+ * store, no barrier; the bucket may then be any device memory), two-shot pull (static, or
+ * dynamic chunks for shards >= 64 MiB), two-shot push (world >= 4, buckets >= 128 MiB: every
+ * NVLink transfer a write); one-shot and dynamic push on request.  CANNIKIN_AR_* environment
+ * knobs force one.
  * The result bits do not depend on the variant; the statistics' summation grouping does.
  * world == 1: g = r_0 g_0 in place.
  * Errors: INVALID (NULL, misaligned, too large), UNSUPPORTED (dtype), CUDA. */

@@ -105,8 +105,17 @@ extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world
     ctx->stage_off = ctx->total_bytes;
     ctx->total_bytes += align_up(ctx->heap_bytes + (size_t)world * world * 64 * 16 + 4096, 4096);
   }
+  if (const char* t = std::getenv("CANNIKIN_AR_LL")) ctx->ar_ll = std::atoi(t) != 0 ? 1 : 0;
+  // low-latency (LL) buffers: 2 parities x W source slots, zeroed (epoch halves start at 0)
+  if (world > 1) {
+    ctx->ll_off = ctx->total_bytes;
+    ctx->ll_max_bytes = cannikin::ll_max_bytes(world);
+    ctx->total_bytes += align_up(cannikin::ll_region_bytes(world), 4096);
+  }
   ce = cudaMalloc(&ctx->base, ctx->total_bytes);
   if (ce == cudaSuccess) ce = cudaMemset(ctx->base, 0, ctx->ctrl_bytes);
+  if (ce == cudaSuccess && ctx->ll_off)
+    ce = cudaMemset(ctx->base + ctx->ll_off, 0, cannikin::ll_region_bytes(world));
   if (ce == cudaSuccess) ce = cudaMallocHost(&ctx->h_stats, sizeof(double) * (cannikin::kMaxWorld + 1));
   if (ce != cudaSuccess) { destroy_partial(ctx); CK_CUDA(ce); }
   ctx->ctrl = reinterpret_cast<cannikin::Ctrl*>(ctx->base);
@@ -235,6 +244,12 @@ extern "C" cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* 
     const double r[1] = {r_i};
     CK_CUDA(cannikin::launch_wsum_local(ctx, in, 1, r, bucket, n, dt, &ctx->ctrl->stats[0],
                                         &ctx->ctrl->stats[1], true, 0, S(stream)));
+    ctx->last_launches = 1;
+    return CANNIKIN_OK;
+  }
+  if (cannikin::ll_eligible(ctx, bytes)) {
+    // small bucket: the LL kernel reads and writes only this rank's bucket (any device memory)
+    CK_CUDA(cannikin::launch_ll(ctx, bucket, n, dt, r_i, S(stream)));
     ctx->last_launches = 1;
     return CANNIKIN_OK;
   }

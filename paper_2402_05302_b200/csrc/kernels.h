@@ -39,5 +39,10 @@ cudaError_t launch_twoshot_push(cannikin_ctx* ctx, size_t off, size_t n, canniki
 cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
                            cudaStream_t st);
 cudaError_t launch_stats_finalize(cannikin_ctx* ctx, double* out, cudaStream_t st);
+size_t ll_max_bytes(int world);
+size_t ll_region_bytes(int world);
+bool ll_eligible(const cannikin_ctx* ctx, size_t bytes);
+cudaError_t launch_ll(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt, double r_i,
+                      cudaStream_t st);
 
 }  // namespace cannikin

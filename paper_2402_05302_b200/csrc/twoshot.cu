@@ -597,9 +597,10 @@ static bool try_oneshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype 
   const size_t esz = dt == CANNIKIN_F32 ? 4 : 2;
   const size_t bytes = n * esz, nvec = bytes / 16;
   if (ctx->ar_oneshot == 0) return false;
-  // auto: W = 2 only, up to W x 256 KiB; at W = 4 reading every peer's whole
-  // bucket loses to two-shot at every size measured (profiles/r01/k3_os_n4.jsonl)
-  if (ctx->ar_oneshot < 0 && (W != 2 || bytes > (size_t)W * (256u << 10))) return false;
+  // not chosen automatically any more: the LL kernel (ll.cu) is faster wherever one-shot beat
+  // two-shot (W = 2, <= 512 KiB; profiles/r01/k3_ll_n2.jsonl), and at W = 4 one-shot loses to
+  // two-shot at every size (k3_os_n4.jsonl).  CANNIKIN_AR_ONESHOT=1 still selects it.
+  if (ctx->ar_oneshot != 1) return false;
   // os_vpt vectors per thread where the grid allows, up to kOneShotMV
   const size_t per_cta = (size_t)kArThreads * (size_t)ctx->os_vpt;
   size_t g = (nvec + per_cta - 1) / per_cta;

@@ -30,7 +30,7 @@ def _port():
     return p
 
 
-@pytest.fixture(scope="module", params=["static", "dyn", "push", "pushdyn", "oneshot"])
+@pytest.fixture(scope="module", params=["static", "dyn", "push", "pushdyn", "oneshot", "ll"])
 def results(request):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -45,7 +45,9 @@ def results(request):
                CANNIKIN_PD_CHUNK_KB="16",  # many chunks (grown where the row table needs it)
                # "oneshot": every bucket that fits the one-shot kernel uses it (larger ones, and
                # the larger pieces of case (4), fall back to two-shot: mixed sequences)
-               CANNIKIN_AR_ONESHOT="1" if request.param == "oneshot" else "0")
+               CANNIKIN_AR_ONESHOT="1" if request.param == "oneshot" else "0",
+               # "ll": buckets <= 256 KiB through the low-latency kernel (no heap bucket needed)
+               CANNIKIN_AR_LL="1" if request.param == "ll" else "0")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     return world, d
@@ -108,7 +110,7 @@ def test_check_ratios(results):
 
 
 def test_result_bits_independent_of_variant():
-    """Every K3 variant (static / dynamic pull, static / dynamic push, one-shot) sums
+    """Every K3 variant (static / dynamic pull, static / dynamic push, one-shot, LL) sums
     fmaf(r_j, g_j, acc) in rank order in fp32 and rounds once: identical result bits."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -123,7 +125,7 @@ def test_result_bits_independent_of_variant():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for dtype in ("f32", "bf16"):
         ref = np.load(os.path.join(d, f"rank0_var_static_{dtype}.npy"))
-        for name in ("static", "dyn", "push", "pushdyn", "oneshot"):
+        for name in ("static", "dyn", "push", "pushdyn", "oneshot", "ll"):
             for k in range(world):
                 got = np.load(os.path.join(d, f"rank{k}_var_{name}_{dtype}.npy"))
                 assert np.array_equal(got, ref), (name, dtype, k)

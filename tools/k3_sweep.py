@@ -65,9 +65,12 @@ def main():
     r = b[rank] / sum(b)
     combos = [(int(g), v) for g in args.grids.split(",") for v in args.variants.split(",")]
     for grid, var in combos:
+        os.environ["CANNIKIN_AR_LL"] = "1" if var == "ll" else "0"
         if var == "auto":
-            for k in ("CANNIKIN_AR_PUSH", "CANNIKIN_AR_DYN", "CANNIKIN_AR_ONESHOT"):
+            for k in ("CANNIKIN_AR_PUSH", "CANNIKIN_AR_DYN", "CANNIKIN_AR_ONESHOT", "CANNIKIN_AR_LL"):
                 os.environ.pop(k, None)
+        elif var == "ll":
+            os.environ.update(CANNIKIN_AR_PUSH="0", CANNIKIN_AR_DYN="0", CANNIKIN_AR_ONESHOT="0")
         elif var.startswith("pushdyn"):
             os.environ["CANNIKIN_AR_PUSH"] = "2"
             os.environ["CANNIKIN_AR_ONESHOT"] = "0"
