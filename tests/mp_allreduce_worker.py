@@ -34,6 +34,9 @@ CASES = [  # (name, N, dtype, seed)
 ]
 
 
+MIXED_CALLS = 40
+
+
 def b_for(world, seed):
     rng = np.random.default_rng(100 + seed)
     return [int(x) for x in rng.integers(1, 97, size=world)]
@@ -92,12 +95,41 @@ def main():
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--full", default="", choices=["", "c4", "c5"])
     ap.add_argument("--variants", action="store_true")
+    ap.add_argument("--mixed", action="store_true")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(lr)
     dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     maxN = max(c[1] for c in CASES)
+    if args.mixed:
+        # a seeded random sequence of sizes, dtypes and buffer kinds under the automatic variant
+        # choice: LL, two-shot pull/dynamic/push and staged calls interleave on one ctx, so the
+        # epochs, parities and statistics rows of the different kernels must compose
+        ctx = ta.init_distributed_context(heap_bytes=(24 << 20), grid=args.grid)
+        rng = np.random.default_rng(77)
+        tdt = {"f32": torch.float32, "bf16": torch.bfloat16}
+        for t in range(MIXED_CALLS):
+            N = int(rng.choice([1, 3, 1000, 4099, 65_537, 300_001, 1_000_003, 2_500_001, 5_000_011]))
+            dtype = "f32" if rng.random() < 0.5 else "bf16"
+            staged = bool(rng.random() < 0.3)
+            b = b_for(world, 200 + t)
+            gs = synth.gns_gradients(world, N, b, seed=200 + t, dtype=dtype)
+            if staged:
+                x = to_dev(gs[rank], dtype)
+            else:
+                x = ta.bucket_tensor(ctx, N, tdt[dtype])
+                x.copy_(to_dev(gs[rank], dtype))
+            ta.weighted_allreduce(ctx, x, b[rank] / sum(b))
+            loc, glob = ctx.gns_stats()
+            np.savez(os.path.join(args.out, f"rank{rank}_mixed_{t}.npz"), out=from_dev(x, dtype),
+                     loc=np.array(loc), glob=glob, N=N, dtype=dtype, b=np.array(b))
+            if not staged:
+                ta.free_bucket_tensor(ctx, x)
+        dist.barrier()
+        ctx.close()
+        dist.destroy_process_group()
+        return
     if args.variants:
         # the same inputs through every K3 variant: the result bits must not depend on it
         VARS = {"static": ("0", "0", "0", "0"), "dyn": ("1", "0", "0", "0"),

@@ -129,3 +129,34 @@ def test_result_bits_independent_of_variant():
             for k in range(world):
                 got = np.load(os.path.join(d, f"rank{k}_var_{name}_{dtype}.npy"))
                 assert np.array_equal(got, ref), (name, dtype, k)
+
+
+def test_mixed_sequence_of_sizes_dtypes_and_variants():
+    """40 calls of seeded random size (1 .. 5M elements), dtype and buffer kind (heap bucket or
+    staged tensor) on ONE ctx under the automatic variant choice: every result matches the oracle,
+    is bitwise identical on every rank, and every call's statistics match the oracle."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(torch.cuda.device_count(), 8)
+    d = tempfile.mkdtemp()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           os.path.join(os.path.dirname(__file__), "mp_allreduce_worker.py"), "--out", d, "--mixed"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000"))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    for t in range(W.MIXED_CALLS):
+        ranks = [dict(np.load(os.path.join(d, f"rank{k}_mixed_{t}.npz"))) for k in range(world)]
+        N, dtype = int(ranks[0]["N"]), str(ranks[0]["dtype"])
+        b = [int(x) for x in ranks[0]["b"]]
+        gs = synth.gns_gradients(world, N, b, seed=200 + t, dtype=dtype)
+        rr = agg.ratios(b)
+        g_ref, ls_ref, gsq_ref = agg.aggregate(gs, rr, dtype)
+        scale = np.maximum(agg.elementwise_scale([agg.to_f64(g, dtype) for g in gs], rr), 1e-30)
+        got = agg.to_f64(ranks[0]["out"], dtype)
+        assert np.max(np.abs(got - g_ref) / scale) <= TOL[dtype], (t, N, dtype)
+        assert np.allclose(ranks[0]["loc"], ls_ref, rtol=1e-4, atol=0), (t, N)
+        assert abs(float(ranks[0]["glob"]) - gsq_ref) <= 1e-4 * max(gsq_ref, 1e-300), (t, N)
+        for k in range(1, world):
+            assert np.array_equal(ranks[k]["out"], ranks[0]["out"]), (t, k)
+            assert np.array_equal(ranks[k]["loc"], ranks[0]["loc"]), (t, k)
