@@ -54,7 +54,12 @@ __global__ void __launch_bounds__(NT) wsum_local_kernel(const LocalArgs a) {
   __shared__ double red[32 * (NR + 1)];
   __shared__ bool s_last;
 
-  if (threadIdx.x == 0) a.trace[blockIdx.x * 5] = dev::globaltimer_ns();
+  if (threadIdx.x == 0) {
+    a.trace[blockIdx.x * 5] = dev::globaltimer_ns();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    a.trace[blockIdx.x * 5 + 1] = smid;  // which SM ran this CTA (diagnostics)
+  }
   float r[NR];
   const char* in[NR];
 #pragma unroll
