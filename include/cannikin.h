@@ -92,6 +92,17 @@ cannikin_status cannikin_get_unique_id(void* out_id);
 cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world, const void* unique_id,
                               int device, size_t heap_bytes, int grid, unsigned flags);
 
+/* In-process group on ONE device (test and single-GPU use of the multi-GPU kernels): creates
+ * `world` contexts out[0..world-1], ranks 0..world-1, in this process, each with its own region
+ * and the others' regions as its "peers" (same address space: no IPC, no NCCL).  The ranks'
+ * reductions must run CONCURRENTLY (one stream per rank) and their kernels must be co-resident,
+ * so `grid` is required and world * grid must not exceed the SM count (the kernels spin on their
+ * peer CTAs; a violation traps after CANNIKIN_SPIN_TIMEOUT_MS instead of hanging).
+ * cannikin_ddp_allreduce_mean is UNSUPPORTED on such contexts; each is destroyed separately.
+ * Errors: INVALID (world outside 2..CANNIKIN_MAX_WORLD, grid <= 0, unknown flag), CUDA. */
+cannikin_status cannikin_init_group_local(cannikin_ctx** out, int world, int device,
+                                          size_t heap_bytes, int grid, unsigned flags);
+
 /* Destroy a ctx (synchronises its device first).  NULL is accepted and ignored. */
 cannikin_status cannikin_destroy(cannikin_ctx* ctx);
 

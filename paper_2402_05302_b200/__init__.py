@@ -86,6 +86,7 @@ SIGNATURES = {
     "cannikin_get_unique_id": (_I, [_P]),
     "cannikin_init": (_I, [ctypes.POINTER(_P), _I, _I, _P, _I, _Z, _I, _U]),
     "cannikin_destroy": (_I, [_P]),
+    "cannikin_init_group_local": (_I, [ctypes.POINTER(_P), _I, _I, _Z, _I, _U]),
     "cannikin_alloc_bucket": (_I, [_P, _Z, ctypes.POINTER(_P)]),
     "cannikin_free_bucket": (_I, [_P, _P]),
     "cannikin_weighted_allreduce": (_I, [_P, _P, _Z, _I, _D, _P]),
@@ -179,6 +180,22 @@ class Context:
         _check(L.cannikin_init(ctypes.byref(h), rank, world, uid, device, heap_bytes, grid, flags))
         self._h = h
         self.rank, self.world, self.device = rank, world, device
+
+    @classmethod
+    def group_local(cls, world: int, device: int = 0, heap_bytes: int = 0, grid: int = 0,
+                    check_ratios: bool = False) -> list:
+        """cannikin_init_group_local: `world` ranks on ONE device in this process (their
+        reductions must be issued concurrently, one stream per rank)."""
+        hs = (_P * world)()
+        flags = INIT_CHECK_RATIOS if check_ratios else 0
+        _check(lib().cannikin_init_group_local(hs, world, device, heap_bytes, grid, flags))
+        out = []
+        for k in range(world):
+            c = cls.__new__(cls)
+            c._h = ctypes.c_void_p(hs[k])
+            c.rank, c.world, c.device = k, world, device
+            out.append(c)
+        return out
 
     def close(self):
         if getattr(self, "_h", None):

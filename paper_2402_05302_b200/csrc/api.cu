@@ -48,7 +48,7 @@ static cannikin_status destroy_partial(cannikin_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   for (int j = 0; j < ctx->world; ++j)
-    if (j != ctx->rank && ctx->peer_base[j]) cudaIpcCloseMemHandle(ctx->peer_base[j]);
+    if (j != ctx->rank && ctx->peer_base[j] && !ctx->in_process) cudaIpcCloseMemHandle(ctx->peer_base[j]);
   if (ctx->nccl_comm) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl_comm));
   if (ctx->base) cudaFree(ctx->base);
   if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
@@ -56,16 +56,10 @@ static cannikin_status destroy_partial(cannikin_ctx* ctx) {
   return CANNIKIN_OK;
 }
 
-extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world,
-                                         const void* unique_id, int device, size_t heap_bytes,
-                                         int grid, unsigned flags) {
-  if (!out) return fail(CANNIKIN_ERR_INVALID, "init: out == NULL");
-  if (flags & ~CANNIKIN_INIT_CHECK_RATIOS) return fail(CANNIKIN_ERR_INVALID, "init: unknown flags %#x", flags);
+// Allocate and initialise this rank's ctx and its device region (no communicator, no peers).
+static cannikin_status create_local(cannikin_ctx** out, int rank, int world, int device,
+                                    size_t heap_bytes, int grid, unsigned flags) {
   *out = nullptr;
-  if (world < 1 || world > CANNIKIN_MAX_WORLD || rank < 0 || rank >= world)
-    return fail(CANNIKIN_ERR_INVALID, "init: rank=%d world=%d (world must be 1..%d)", rank, world,
-                CANNIKIN_MAX_WORLD);
-  if (world > 1 && !unique_id) return fail(CANNIKIN_ERR_INVALID, "init: world > 1 needs a unique id");
   int ndev = 0;
   CK_CUDA(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev)
@@ -121,7 +115,26 @@ extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world
   ctx->ctrl = reinterpret_cast<cannikin::Ctrl*>(ctx->base);
   if (ctx->heap_bytes) ctx->free_blocks[0] = ctx->heap_bytes;
   ctx->peer_base[rank] = ctx->base;
+  *out = ctx;
+  return CANNIKIN_OK;
+}
 
+extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world,
+                                         const void* unique_id, int device, size_t heap_bytes,
+                                         int grid, unsigned flags) {
+  if (!out) return fail(CANNIKIN_ERR_INVALID, "init: out == NULL");
+  *out = nullptr;
+  if (flags & ~CANNIKIN_INIT_CHECK_RATIOS) return fail(CANNIKIN_ERR_INVALID, "init: unknown flags %#x", flags);
+  if (world < 1 || world > CANNIKIN_MAX_WORLD || rank < 0 || rank >= world)
+    return fail(CANNIKIN_ERR_INVALID, "init: rank=%d world=%d (world must be 1..%d)", rank, world,
+                CANNIKIN_MAX_WORLD);
+  if (world > 1 && !unique_id) return fail(CANNIKIN_ERR_INVALID, "init: world > 1 needs a unique id");
+  cannikin_ctx* ctx = nullptr;
+  {
+    const cannikin_status st = create_local(&ctx, rank, world, device, heap_bytes, grid, flags);
+    if (st != CANNIKIN_OK) return st;
+  }
+  cudaError_t ce = cudaSuccess;
   if (world > 1) {
     ncclComm_t comm;
     ncclUniqueId id;
@@ -184,6 +197,31 @@ extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world
 }
 
 extern "C" cannikin_status cannikin_destroy(cannikin_ctx* ctx) { return destroy_partial(ctx); }
+
+extern "C" cannikin_status cannikin_init_group_local(cannikin_ctx** out, int world, int device,
+                                                     size_t heap_bytes, int grid, unsigned flags) {
+  if (!out) return fail(CANNIKIN_ERR_INVALID, "init_group_local: out == NULL");
+  if (flags & ~CANNIKIN_INIT_CHECK_RATIOS)
+    return fail(CANNIKIN_ERR_INVALID, "init_group_local: unknown flags %#x", flags);
+  if (world < 2 || world > CANNIKIN_MAX_WORLD)
+    return fail(CANNIKIN_ERR_INVALID, "init_group_local: world=%d (must be 2..%d)", world,
+                CANNIKIN_MAX_WORLD);
+  if (grid <= 0) return fail(CANNIKIN_ERR_INVALID, "init_group_local: an explicit grid is required");
+  for (int k = 0; k < world; ++k) out[k] = nullptr;
+  for (int k = 0; k < world; ++k) {
+    const cannikin_status st = create_local(&out[k], k, world, device, heap_bytes, grid, flags);
+    if (st != CANNIKIN_OK) {
+      for (int j = 0; j < k; ++j) destroy_partial(out[j]);
+      for (int j = 0; j < world; ++j) out[j] = nullptr;
+      return st;
+    }
+    out[k]->in_process = true;
+  }
+  for (int k = 0; k < world; ++k)
+    for (int j = 0; j < world; ++j) out[k]->peer_base[j] = out[j]->base;
+  cannikin::clear_error();
+  return CANNIKIN_OK;
+}
 
 extern "C" cannikin_status cannikin_alloc_bucket(cannikin_ctx* ctx, size_t bytes, void** dptr) {
   if (!ctx || !dptr || bytes == 0) return fail(CANNIKIN_ERR_INVALID, "alloc_bucket: bad arguments");
@@ -360,6 +398,8 @@ extern "C" cannikin_status cannikin_ddp_allreduce_mean(cannikin_ctx* ctx, void* 
     return fail(CANNIKIN_ERR_UNSUPPORTED, "ddp_allreduce_mean: dtype %d", (int)dt);
   if (n == 0 || ctx->world == 1) return CANNIKIN_OK;
   if (!bucket) return fail(CANNIKIN_ERR_INVALID, "ddp_allreduce_mean: bucket == NULL");
+  if (!ctx->nccl_comm)
+    return fail(CANNIKIN_ERR_UNSUPPORTED, "ddp_allreduce_mean: no NCCL communicator (in-process group)");
   CK_CUDA(cudaSetDevice(ctx->device));
   CK_NCCL(ncclAllReduce(bucket, bucket, n, dt == CANNIKIN_F32 ? ncclFloat32 : ncclBfloat16, ncclAvg,
                         static_cast<ncclComm_t>(ctx->nccl_comm), S(stream)));

@@ -70,6 +70,7 @@ struct cannikin_ctx {
   char* peer_base[cannikin::kMaxWorld] = {};
   cannikin::Ctrl* ctrl = nullptr;
   void* nccl_comm = nullptr;  // ncclComm_t
+  bool in_process = false;    // cannikin_init_group_local: peers are this process's allocations
   std::map<size_t, size_t> free_blocks;  // offset -> size within the user heap
   std::map<size_t, size_t> used_blocks;
   double* h_stats = nullptr;  // pinned host staging for gns_stats

@@ -1,0 +1,175 @@
+"""The multi-GPU reduction kernels on ONE GPU: cannikin_init_group_local makes W ranks in this
+process (same device, each with its own region, the others' regions as peers), and every rank's
+cannikin_weighted_allreduce is issued on its own stream so the W kernels run concurrently, exactly
+as they do on W GPUs (grid * W <= SMs keeps them co-resident).  Every K3 variant (static / dynamic
+pull, static / dynamic push, one-shot, LL) against the oracle (Eq. 9, Eq. 10 inputs), bitwise
+identical results and statistics on every rank, result bits identical across variants, staged
+(non-heap) buffers, and the ratio check.  Runs on a single-GPU box, where the torchrun-based
+multi-GPU tests skip."""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import cannikin_synth as synth  # noqa: E402
+import paper_2402_05302_b200 as ck  # noqa: E402
+from oracle import aggregate as agg  # noqa: E402
+from paper_2402_05302_b200 import torch_api as ta  # noqa: E402
+
+TOL = {"f32": 1e-5, "bf16": 1e-2}
+TDT = {"f32": torch.float32, "bf16": torch.bfloat16}
+VARIANTS = {  # CANNIKIN_AR_DYN, _PUSH, _ONESHOT, _LL
+    "static": ("0", "0", "0", "0"), "dyn": ("1", "0", "0", "0"), "push": ("0", "1", "0", "0"),
+    "pushdyn": ("0", "2", "0", "0"), "oneshot": ("0", "0", "1", "0"), "ll": ("0", "0", "0", "1"),
+}
+CASES = [(1, "f32", 1), (7, "bf16", 2), (4099, "f32", 3), (300_001, "f32", 4),
+         ((1 << 20) + 5, "bf16", 5), (3_000_011, "f32", 6)]
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+
+
+def _group(world, variant, check_ratios=False):
+    dyn, push, one, ll = VARIANTS[variant]
+    os.environ.update(CANNIKIN_AR_DYN=dyn, CANNIKIN_AR_PUSH=push, CANNIKIN_AR_ONESHOT=one,
+                      CANNIKIN_AR_LL=ll, CANNIKIN_PD_CHUNK_KB="16", CANNIKIN_SPIN_TIMEOUT_MS="20000")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    grid = min(32, sms // world)
+    try:
+        return ck.Context.group_local(world, device=0, heap_bytes=16 << 20, grid=grid,
+                                      check_ratios=check_ratios)
+    finally:
+        for k in ("CANNIKIN_AR_DYN", "CANNIKIN_AR_PUSH", "CANNIKIN_AR_ONESHOT", "CANNIKIN_AR_LL",
+                  "CANNIKIN_PD_CHUNK_KB"):
+            os.environ.pop(k, None)
+
+
+def _reduce(ctxs, tensors, r, streams):
+    """Issue every rank's reduction on its own stream (concurrent), then wait for all."""
+    torch.cuda.synchronize()
+    for c, t, ri, s in zip(ctxs, tensors, r, streams):
+        ta.weighted_allreduce(c, t, ri, stream=s)
+    torch.cuda.synchronize()
+
+
+def _stats(ctxs, streams):
+    return [c.gns_stats(stream=s) for c, s in zip(ctxs, streams)]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_group_local_parity(world, variant):
+    _need_gpu()
+    ctxs = _group(world, variant)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    try:
+        for N, dtype, seed in CASES:
+            b = [int(x) for x in np.random.default_rng(seed).integers(1, 97, size=world)]
+            gs = synth.gns_gradients(world, N, b, seed=seed, dtype=dtype)
+            r = agg.ratios(b)
+            g_ref, ls_ref, gsq_ref = agg.aggregate(gs, r, dtype)
+            scale = np.maximum(agg.elementwise_scale([agg.to_f64(g, dtype) for g in gs], r), 1e-30)
+            for staged in (False, True):
+                if staged:
+                    ts = [_to_dev(gs[k], dtype) for k in range(world)]
+                else:
+                    ts = [ta.bucket_tensor(ctxs[k], N, TDT[dtype]) for k in range(world)]
+                    for k in range(world):
+                        ts[k].copy_(_to_dev(gs[k], dtype))
+                _reduce(ctxs, ts, r, streams)
+                outs = [_from_dev(t, dtype) for t in ts]
+                st = _stats(ctxs, streams)
+                got = agg.to_f64(outs[0], dtype)
+                assert np.max(np.abs(got - g_ref) / scale) <= TOL[dtype], (variant, N, staged)
+                for k in range(1, world):
+                    assert np.array_equal(outs[k], outs[0]), (variant, N, k)
+                    assert st[k][0] == st[0][0] and st[k][1] == st[0][1], (variant, N, k)
+                assert np.allclose(st[0][0], ls_ref, rtol=1e-4, atol=0), (variant, N)
+                assert abs(st[0][1] - gsq_ref) <= 1e-4 * max(gsq_ref, 1e-300), (variant, N)
+                if not staged:
+                    for k in range(world):
+                        ta.free_bucket_tensor(ctxs[k], ts[k])
+    finally:
+        for c in ctxs:
+            c.close()
+
+
+def test_group_local_bits_identical_across_variants():
+    _need_gpu()
+    world = 2
+    results = {}
+    for variant in VARIANTS:
+        ctxs = _group(world, variant)
+        streams = [torch.cuda.Stream() for _ in range(world)]
+        try:
+            for N, dtype, seed in ((100_003, "f32", 21), (200_011, "bf16", 22)):
+                b = [5, 17]
+                gs = synth.gns_gradients(world, N, b, seed=seed, dtype=dtype)
+                ts = [_to_dev(gs[k], dtype) for k in range(world)]
+                _reduce(ctxs, ts, agg.ratios(b), streams)
+                _stats(ctxs, streams)
+                results.setdefault((N, dtype), {})[variant] = _from_dev(ts[0], dtype)
+        finally:
+            for c in ctxs:
+                c.close()
+    for key, per in results.items():
+        ref = per["static"]
+        for variant, out in per.items():
+            assert np.array_equal(out, ref), (key, variant)
+
+
+def test_group_local_check_ratios():
+    _need_gpu()
+    world = 2
+    for variant in ("static", "ll"):
+        ctxs = _group(world, variant, check_ratios=True)
+        streams = [torch.cuda.Stream() for _ in range(world)]
+        try:
+            for scale, want in ((1.0, None), (0.9, "DOMAIN"), (1.0, None)):
+                ts = [torch.ones(4099, device="cuda") for _ in range(world)]
+                _reduce(ctxs, ts, [scale / world] * world, streams)
+                for c, s in zip(ctxs, streams):
+                    if want is None:
+                        c.gns_stats(stream=s)
+                    else:
+                        with pytest.raises(ck.CannikinError) as e:
+                            c.gns_stats(stream=s)
+                        assert e.value.name == want
+        finally:
+            for c in ctxs:
+                c.close()
+
+
+def test_group_local_errors():
+    _need_gpu()
+    with pytest.raises(ck.CannikinError) as e:
+        ck.Context.group_local(1, device=0, heap_bytes=1 << 20, grid=8)
+    assert e.value.name == "INVALID"
+    with pytest.raises(ck.CannikinError) as e:
+        ck.Context.group_local(2, device=0, heap_bytes=1 << 20, grid=0)
+    assert e.value.name == "INVALID"
+    ctxs = ck.Context.group_local(2, device=0, heap_bytes=1 << 20, grid=8)
+    try:
+        with pytest.raises(ck.CannikinError) as e:
+            ta.ddp_allreduce_mean(ctxs[0], torch.ones(8, device="cuda"))
+        assert e.value.name == "UNSUPPORTED"
+    finally:
+        for c in ctxs:
+            c.close()
+
+
+def _to_dev(a, dtype):
+    if dtype == "bf16":
+        return torch.from_numpy(a.view(np.int16).copy()).cuda().view(torch.bfloat16)
+    return torch.from_numpy(a.copy()).cuda()
+
+
+def _from_dev(t, dtype):
+    if dtype == "bf16":
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
