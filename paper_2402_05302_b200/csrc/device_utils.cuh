@@ -95,8 +95,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // Reduce NV doubles over the block; the result is valid in thread 0.  `smem` holds >= 32*NV
 // doubles.  Fixed order (butterfly within warps, then warps 0..nw-1 in sequence).
-template <int NV>
-__device__ __forceinline__ void block_sum(double (&v)[NV], double* smem) {
+template <int NV, int N>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double (&smem)[N]) {
+  static_assert(N >= 32 * NV, "block_sum: scratch must hold 32 warps x NV doubles");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
@@ -120,9 +121,9 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem) {
 // pass over the block: thread t accumulates rows t, t+T, t+2T, ... for all columns (independent
 // loads, pipelined), then one butterfly/warp-order reduction.  Fixed order => deterministic.
 // Result valid in thread 0.
-template <int NV>
+template <int NV, int N>
 __device__ __forceinline__ void block_table_sum(const double* base, int count, int row_stride,
-                                                double (&out)[NV], double* smem) {
+                                                double (&out)[NV], double (&smem)[N]) {
 #pragma unroll
   for (int j = 0; j < NV; ++j) out[j] = 0.0;
   for (int i = threadIdx.x; i < count; i += blockDim.x) {
@@ -130,7 +131,7 @@ __device__ __forceinline__ void block_table_sum(const double* base, int count, i
 #pragma unroll
     for (int j = 0; j < NV; ++j) out[j] += __ldcg(row + j);
   }
-  block_sum<NV>(out, smem);
+  block_sum(out, smem);
 }
 
 // ------------------------------------------------------------------ system-scope flags

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_kernel(const LLArgs a) {
 #pragma unroll
   for (int j = 0; j < W; ++j) vals[j] = lsq[j];
   vals[W] = gsq;
-  dev::block_sum<W + 1>(vals, red);
+  dev::block_sum(vals, red);
   if (tid == 0) {
     double* acc = a.ctrl->cta_acc[b];
 #pragma unroll

@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const McArgs a, int W) {
   if (tid == 0) a.ctrl->trace[b][2] = dev::globaltimer_ns();
   // row [me][b]: this CTA's |g_me|^2 piece in column me, its |g|^2 piece in column W
   double vals[2] = {lsq, gsq};
-  dev::block_sum<2>(vals, red);
+  dev::block_sum(vals, red);
   if (tid == 0) {
     s_part[0] = vals[0];
     s_part[1] = vals[1];

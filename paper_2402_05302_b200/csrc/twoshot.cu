@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
 #pragma unroll
   for (int j = 0; j < W; ++j) vals[j] = lsq[j];
   vals[W] = gsq;
-  dev::block_sum<W + 1>(vals, red);
+  dev::block_sum(vals, red);
   if (tid == 0) {
 #pragma unroll
     for (int j = 0; j <= W; ++j) s_part[j] = vals[j];
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kArThreads, 1) twoshot_dyn_kernel(const ArArgs
 #pragma unroll
     for (int j = 0; j < W; ++j) vals[j] = lsq[j];
     vals[W] = gsq;
-    dev::block_sum<W + 1>(vals, red);
+    dev::block_sum(vals, red);
     if (tid == 0) {
 #pragma unroll
       for (int j = 0; j <= W; ++j) s_part[j] = vals[j];
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kArThreads, 1) twoshot_dyn_kernel(const ArArgs
     }
     base += nc;
   }
-  dev::block_sum<W + 1>(tot, red);
+  dev::block_sum(tot, red);
   if (tid == 0) {
 #pragma unroll
     for (int j = 0; j <= W; ++j) a.ctrl->stats[j] += tot[j];
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(kArThreads, 1) oneshot_kernel(const ArArgs a) 
 #pragma unroll
   for (int j = 0; j < W; ++j) vals[j] = lsq[j];
   vals[W] = gsq;
-  dev::block_sum<W + 1>(vals, red);  // ends with __syncthreads: every load of the CTA is consumed
+  dev::block_sum(vals, red);  // ends with __syncthreads: every load of the CTA is consumed
   if (tid == 0) a.ctrl->trace[b][2] = dev::globaltimer_ns();
 
   // ---- 2. done-reading barrier with CTA b of every peer
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(512, 1) twoshot_push_kernel(const PushArgs a) 
 
   // ---- 4. partial rows, exit barrier, final sum
   double vals[2] = {lsq, gsq};
-  dev::block_sum<2>(vals, red);
+  dev::block_sum(vals, red);
   if (tid == 0) {
     s_part[0] = vals[0];
     s_part[1] = vals[1];
@@ -856,7 +856,7 @@ __global__ void __launch_bounds__(512, 1) twoshot_push_kernel(const PushArgs a) 
 #pragma unroll
     for (int j = 0; j <= W; ++j) tot[j] += __ldcg(row + j);
   }
-  dev::block_sum<W + 1>(tot, red);
+  dev::block_sum(tot, red);
   if (tid == 0) {
 #pragma unroll
     for (int j = 0; j <= W; ++j) a.ctrl->stats[j] += tot[j];
@@ -948,7 +948,7 @@ __global__ void __launch_bounds__(kArThreads, 1) pushdyn_kernel(const PushDynArg
   using V = dev::Vec<T>;
   constexpr int E = V::E;
   constexpr int NT = kArThreads;
-  __shared__ double red[32 * 2];
+  __shared__ double red[32 * (W + 1)];
   __shared__ double s_row[2];
   __shared__ float s_r[W];
   __shared__ uint64_t s_ep;
@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(kArThreads, 1) pushdyn_kernel(const PushDynArg
     }
     // ---- this item's row {|g_me|^2, |g|^2} -> every rank's table (zero rows for empty items)
     double vals[2] = {lsq, gsq};
-    dev::block_sum<2>(vals, red);
+    dev::block_sum(vals, red);
     if (tid == 0) {
       s_row[0] = vals[0];
       s_row[1] = vals[1];
@@ -1163,7 +1163,7 @@ __global__ void __launch_bounds__(kArThreads, 1) pushdyn_kernel(const PushDynArg
       for (int j = 0; j <= W; ++j) tot[j] += __ldcg(row + j);
     }
   }
-  dev::block_sum<W + 1>(tot, red);
+  dev::block_sum(tot, red);
   if (tid == 0) {
 #pragma unroll
     for (int j = 0; j <= W; ++j) a.ctrl->stats[j] += tot[j];

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(NT) wsum_local_kernel(const LocalArgs a) {
 #pragma unroll
   for (int j = 0; j < NR; ++j) vals[j] = lsq[j];
   vals[NR] = gsq;
-  dev::block_sum<NR + 1>(vals, red);
+  dev::block_sum(vals, red);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int j = 0; j <= NR; ++j) a.partials[(size_t)blockIdx.x * (NR + 1) + j] = vals[j];
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(NT) wsum_local_kernel(const LocalArgs a) {
   __threadfence();
   // last CTA: fixed-order tree over the per-CTA partials (K5)
   double tot[NR + 1];
-  dev::block_table_sum<NR + 1>(a.partials, gridDim.x, NR + 1, tot, red);
+  dev::block_table_sum(a.partials, gridDim.x, NR + 1, tot, red);
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int j = 0; j <= NR; ++j) {

@@ -4,8 +4,9 @@ cannikin_weighted_allreduce is issued on its own stream so the W kernels run con
 as they do on W GPUs (grid * W <= SMs keeps them co-resident).  Every K3 variant (static / dynamic
 pull, static / dynamic push, one-shot, LL) against the oracle (Eq. 9, Eq. 10 inputs), bitwise
 identical results and statistics on every rank, result bits identical across variants, staged
-(non-heap) buffers, and the ratio check.  Runs on a single-GPU box, where the torchrun-based
-multi-GPU tests skip."""
+(non-heap) buffers, and the ratio check -- for W = 2, 3, 4 and 8 (the 8-rank protocol, otherwise
+only reachable on an 8-GPU box).  Runs on a single-GPU box, where the torchrun-based multi-GPU
+tests skip."""
 import os
 
 import numpy as np
@@ -39,7 +40,7 @@ def _group(world, variant, check_ratios=False):
     os.environ.update(CANNIKIN_AR_DYN=dyn, CANNIKIN_AR_PUSH=push, CANNIKIN_AR_ONESHOT=one,
                       CANNIKIN_AR_LL=ll, CANNIKIN_PD_CHUNK_KB="16", CANNIKIN_SPIN_TIMEOUT_MS="20000")
     sms = torch.cuda.get_device_properties(0).multi_processor_count
-    grid = min(32, sms // world)
+    grid = min(32, sms // world)  # W = 8: 18 CTAs per rank, 144 co-resident
     try:
         return ck.Context.group_local(world, device=0, heap_bytes=16 << 20, grid=grid,
                                       check_ratios=check_ratios)
@@ -61,7 +62,7 @@ def _stats(ctxs, streams):
     return [c.gns_stats(stream=s) for c, s in zip(ctxs, streams)]
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 @pytest.mark.parametrize("variant", list(VARIANTS))
 def test_group_local_parity(world, variant):
     _need_gpu()
