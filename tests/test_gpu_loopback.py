@@ -174,3 +174,34 @@ def _from_dev(t, dtype):
     if dtype == "bf16":
         return t.view(torch.int16).cpu().numpy().view(np.uint16)
     return t.cpu().numpy()
+
+
+def test_group_local_config2_eight_ranks():
+    """configs[2]'s ResNet-50 gradient (25,557,032 fp32) at its 8 ranks, automatic variant, one
+    bucket per rank: the oracle over the whole vectors, identical bits and statistics."""
+    _need_gpu()
+    world, N = 8, 25_557_032
+    os.environ["CANNIKIN_SPIN_TIMEOUT_MS"] = "20000"
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    ctxs = ck.Context.group_local(world, device=0, heap_bytes=N * 4 + 4096, grid=sms // world)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    try:
+        b = [21, 8, 5, 21, 8, 5, 20, 8]  # the emulated A100/V100/P100 mix's split at B = 96
+        gs = synth.gns_gradients(world, N, b, seed=31, dtype="f32")
+        r = agg.ratios(b)
+        ts = [ta.bucket_tensor(ctxs[k], N, torch.float32) for k in range(world)]
+        for k in range(world):
+            ts[k].copy_(_to_dev(gs[k], "f32"))
+        _reduce(ctxs, ts, r, streams)
+        st = _stats(ctxs, streams)
+        outs = [_from_dev(t, "f32") for t in ts]
+        g_ref, ls_ref, gsq_ref = agg.aggregate(gs, r, "f32")
+        scale = np.maximum(agg.elementwise_scale([agg.to_f64(g, "f32") for g in gs], r), 1e-30)
+        assert np.max(np.abs(outs[0].astype(np.float64) - g_ref) / scale) <= 1e-5
+        for k in range(1, world):
+            assert np.array_equal(outs[k], outs[0]) and st[k] == st[0]
+        assert np.allclose(st[0][0], ls_ref, rtol=1e-4, atol=0)
+        assert abs(st[0][1] - gsq_ref) <= 1e-4 * gsq_ref
+    finally:
+        for c in ctxs:
+            c.close()
