@@ -205,3 +205,45 @@ def test_group_local_config2_eight_ranks():
     finally:
         for c in ctxs:
             c.close()
+
+
+def test_group_local_config3_eight_ranks_full_size():
+    """configs[3] at full size (110M bf16, one 220 MB bucket per rank) at 8 ranks: the automatic
+    variant is the push two-shot (W >= 4, >= 128 MiB) -- the path an 8-GPU bench takes.  Sampled
+    elements against the oracle one by one, norms against the oracle over the whole vectors."""
+    _need_gpu()
+    world, N = 8, 110_000_000
+    os.environ["CANNIKIN_SPIN_TIMEOUT_MS"] = "20000"
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    ctxs = ck.Context.group_local(world, device=0, heap_bytes=N * 2 + 4096, grid=sms // world)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    try:
+        b = [21, 8, 5, 21, 8, 5, 20, 8]
+        r = agg.ratios(b)
+        gs = synth.device_gns_gradients(world, N, b, seed=9, dtype="bf16")
+        idx = torch.from_numpy(np.random.default_rng(0).choice(N, 100_000, replace=False)).cuda()
+        ins_s = [agg.to_f64(_from_dev(g[idx], "bf16"), "bf16") for g in gs]
+        # whole-vector oracle norms, chunked (inputs of record = the device bits)
+        lsum, gsum = np.zeros(world), 0.0
+        for a in range(0, N, 10_000_000):
+            parts = [agg.to_f64(_from_dev(g[a:a + 10_000_000], "bf16"), "bf16") for g in gs]
+            for j in range(world):
+                lsum[j] += agg.sq_norm(parts[j])
+            gsum += agg.sq_norm(agg.weighted_sum(parts, r))
+        ts = [ta.bucket_tensor(ctxs[k], N, torch.bfloat16) for k in range(world)]
+        for k in range(world):
+            ts[k].copy_(gs[k])
+        del gs
+        _reduce(ctxs, ts, r, streams)
+        st = _stats(ctxs, streams)
+        ref = agg.weighted_sum(ins_s, r)
+        scale = np.maximum(agg.elementwise_scale(ins_s, r), 1e-30)
+        got = [agg.to_f64(_from_dev(t[idx], "bf16"), "bf16") for t in ts]
+        assert np.max(np.abs(got[0] - ref) / scale) <= 1e-2
+        for k in range(1, world):
+            assert np.array_equal(got[k], got[0]) and st[k] == st[0]
+        assert np.allclose(st[0][0], lsum, rtol=1e-4, atol=0)
+        assert abs(st[0][1] - gsum) <= 1e-4 * gsum
+    finally:
+        for c in ctxs:
+            c.close()
