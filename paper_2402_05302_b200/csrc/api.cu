@@ -106,10 +106,23 @@ static cannikin_status create_local(cannikin_ctx** out, int rank, int world, int
     ctx->ll_max_bytes = cannikin::ll_max_bytes(world);
     ctx->total_bytes += align_up(cannikin::ll_region_bytes(world), 4096);
   }
+  // LL128 buffers (flag-in-line two-shot for mid-size buckets): 2 parities x {scatter, gather} x
+  // W source slots of the largest shard, plus headers; zeroed (flags start at epoch 0)
+  if (const char* t = std::getenv("CANNIKIN_AR_LL128")) ctx->ar_ll128 = std::atoi(t) != 0 ? 1 : 0;
+  if (world > 1 && ctx->ar_ll128 != 0) {
+    size_t mb = 64;
+    if (const char* t = std::getenv("CANNIKIN_LL128_MAX_MB")) mb = (size_t)std::max(1, std::atoi(t));
+    ctx->ll128_max_bytes = mb << 20;
+    ctx->ll128_off = ctx->total_bytes;
+    ctx->total_bytes += align_up(cannikin::ll128_region_bytes(world, ctx->ll128_max_bytes), 4096);
+  }
   ce = cudaMalloc(&ctx->base, ctx->total_bytes);
   if (ce == cudaSuccess) ce = cudaMemset(ctx->base, 0, ctx->ctrl_bytes);
   if (ce == cudaSuccess && ctx->ll_off)
     ce = cudaMemset(ctx->base + ctx->ll_off, 0, cannikin::ll_region_bytes(world));
+  if (ce == cudaSuccess && ctx->ll128_off)
+    ce = cudaMemset(ctx->base + ctx->ll128_off, 0,
+                    cannikin::ll128_region_bytes(world, ctx->ll128_max_bytes));
   if (ce == cudaSuccess) ce = cudaMallocHost(&ctx->h_stats, sizeof(double) * (cannikin::kMaxWorld + 1));
   if (ce != cudaSuccess) { destroy_partial(ctx); CK_CUDA(ce); }
   ctx->ctrl = reinterpret_cast<cannikin::Ctrl*>(ctx->base);
@@ -282,6 +295,12 @@ extern "C" cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* 
     const double r[1] = {r_i};
     CK_CUDA(cannikin::launch_wsum_local(ctx, in, 1, r, bucket, n, dt, &ctx->ctrl->stats[0],
                                         &ctx->ctrl->stats[1], true, 0, S(stream)));
+    ctx->last_launches = 1;
+    return CANNIKIN_OK;
+  }
+  if (cannikin::ll128_eligible(ctx, bytes)) {
+    // mid-size bucket: flag-in-line two-shot, no barrier; touches only this rank's bucket
+    CK_CUDA(cannikin::launch_ll128(ctx, bucket, n, dt, r_i, S(stream)));
     ctx->last_launches = 1;
     return CANNIKIN_OK;
   }

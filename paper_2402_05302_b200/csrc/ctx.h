@@ -31,6 +31,8 @@ struct Ctrl {
   uint64_t pd_epoch;                                         // [local] dynamic-push call counter
   uint64_t ll_epoch;                                         // [local] LL-kernel call counter
   unsigned ticket_ll;                                        // [local] LL last-CTA ticket
+  uint64_t ll128_epoch;                                      // [local] LL128-kernel call counter
+  unsigned ticket_ll128;                                     // [local] LL128 last-CTA ticket
   double part[kMaxWorld][kMaxArChunks][kMaxWorld + 1];       // [peer] norm partials [src][row][j]
   uint64_t epoch[kMaxArBlocks];                              // [local] per-block epoch counter
   unsigned ticket_ar;                                        // [local] last-block-done ticket
@@ -58,6 +60,8 @@ struct cannikin_ctx {
   int ar_chunk_max = 512 * 16;  // CANNIKIN_AR_CHUNK: dynamic two-shot max chunk (16-B vectors)
   int ar_ll = -1;           // CANNIKIN_AR_LL=0|1 forbids/prefers the LL kernel; -1 = by size
   size_t ll_max_bytes = 0;  // largest LL bucket = its slot payload: 2 MiB / (W - 1), 64 KiB steps
+  int ar_ll128 = -1;        // CANNIKIN_AR_LL128=0|1 forbids/prefers the LL128 kernel; -1 = by size
+  size_t ll128_max_bytes = 0;  // largest LL128 bucket (CANNIKIN_LL128_MAX_MB), sizes its slots
   int ar_oneshot = -1;      // CANNIKIN_AR_ONESHOT=0|1 forbids/prefers one-shot; -1 = by size
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2
   bool local_tma = false;   // default variant of K2 (CANNIKIN_K2_IMPL=tma|ldg)
@@ -66,7 +70,7 @@ struct cannikin_ctx {
   size_t heap_bytes = 0;
   // local allocation = [Ctrl | user heap (heap_bytes) | scratch (heap_bytes)]
   char* base = nullptr;
-  size_t ctrl_bytes = 0, user_off = 0, scratch_off = 0, stage_off = 0, ll_off = 0, total_bytes = 0;
+  size_t ctrl_bytes = 0, user_off = 0, scratch_off = 0, stage_off = 0, ll_off = 0, ll128_off = 0, total_bytes = 0;
   char* peer_base[cannikin::kMaxWorld] = {};
   cannikin::Ctrl* ctrl = nullptr;
   void* nccl_comm = nullptr;  // ncclComm_t

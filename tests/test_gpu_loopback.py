@@ -22,9 +22,11 @@ from paper_2402_05302_b200 import torch_api as ta  # noqa: E402
 
 TOL = {"f32": 1e-5, "bf16": 1e-2}
 TDT = {"f32": torch.float32, "bf16": torch.bfloat16}
-VARIANTS = {  # CANNIKIN_AR_DYN, _PUSH, _ONESHOT, _LL
-    "static": ("0", "0", "0", "0"), "dyn": ("1", "0", "0", "0"), "push": ("0", "1", "0", "0"),
-    "pushdyn": ("0", "2", "0", "0"), "oneshot": ("0", "0", "1", "0"), "ll": ("0", "0", "0", "1"),
+VARIANTS = {  # CANNIKIN_AR_DYN, _PUSH, _ONESHOT, _LL, _LL128
+    "static": ("0", "0", "0", "0", "0"), "dyn": ("1", "0", "0", "0", "0"),
+    "push": ("0", "1", "0", "0", "0"), "pushdyn": ("0", "2", "0", "0", "0"),
+    "oneshot": ("0", "0", "1", "0", "0"), "ll": ("0", "0", "0", "1", "0"),
+    "ll128": ("0", "0", "0", "0", "1"),
 }
 CASES = [(1, "f32", 1), (7, "bf16", 2), (4099, "f32", 3), (300_001, "f32", 4),
          ((1 << 20) + 5, "bf16", 5), (3_000_011, "f32", 6)]
@@ -36,9 +38,10 @@ def _need_gpu():
 
 
 def _group(world, variant, check_ratios=False):
-    dyn, push, one, ll = VARIANTS[variant]
+    dyn, push, one, ll, ll128 = VARIANTS[variant]
     os.environ.update(CANNIKIN_AR_DYN=dyn, CANNIKIN_AR_PUSH=push, CANNIKIN_AR_ONESHOT=one,
-                      CANNIKIN_AR_LL=ll, CANNIKIN_PD_CHUNK_KB="16", CANNIKIN_SPIN_TIMEOUT_MS="20000")
+                      CANNIKIN_AR_LL=ll, CANNIKIN_AR_LL128=ll128, CANNIKIN_PD_CHUNK_KB="16",
+                      CANNIKIN_SPIN_TIMEOUT_MS="20000")
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     grid = min(32, sms // world)  # W = 8: 18 CTAs per rank, 144 co-resident
     try:
@@ -46,7 +49,7 @@ def _group(world, variant, check_ratios=False):
                                       check_ratios=check_ratios)
     finally:
         for k in ("CANNIKIN_AR_DYN", "CANNIKIN_AR_PUSH", "CANNIKIN_AR_ONESHOT", "CANNIKIN_AR_LL",
-                  "CANNIKIN_PD_CHUNK_KB"):
+                  "CANNIKIN_AR_LL128", "CANNIKIN_PD_CHUNK_KB"):
             os.environ.pop(k, None)
 
 
@@ -124,10 +127,48 @@ def test_group_local_bits_identical_across_variants():
             assert np.array_equal(out, ref), (key, variant)
 
 
+@pytest.mark.parametrize("variant", ["static", "ll", "ll128"])
+@pytest.mark.parametrize("world", [2, 4])
+def test_group_local_back_to_back(world, variant):
+    """40 calls of mixed sizes and dtypes enqueued back to back (no host sync in between), each on
+    its own bucket: the epoch/parity buffer reuse of the flag protocols under pipelining."""
+    _need_gpu()
+    ctxs = _group(world, variant)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    rng = np.random.default_rng(7)
+    try:
+        calls = []
+        for t in range(40):
+            N = int(rng.choice([1, 33, 4099, 65_537, 300_001, 1_000_003]))
+            dtype = "bf16" if t % 3 == 1 else "f32"
+            b = [int(x) for x in rng.integers(1, 97, size=world)]
+            gs = synth.gns_gradients(world, N, b, seed=1000 + t, dtype=dtype)
+            calls.append((N, dtype, b, gs, [_to_dev(gs[k], dtype) for k in range(world)]))
+        torch.cuda.synchronize()
+        for N, dtype, b, gs, ts in calls:
+            for c, x, ri, s in zip(ctxs, ts, agg.ratios(b), streams):
+                ta.weighted_allreduce(c, x, ri, stream=s)
+        torch.cuda.synchronize()
+        for N, dtype, b, gs, ts in calls:
+            r = agg.ratios(b)
+            g_ref, _, _ = agg.aggregate(gs, r, dtype)
+            scale = np.maximum(agg.elementwise_scale([agg.to_f64(g, dtype) for g in gs], r), 1e-30)
+            outs = [_from_dev(t, dtype) for t in ts]
+            assert np.max(np.abs(agg.to_f64(outs[0], dtype) - g_ref) / scale) <= TOL[dtype], (N, dtype)
+            for k in range(1, world):
+                assert np.array_equal(outs[k], outs[0]), (N, dtype, k)
+        st = _stats(ctxs, streams)
+        for k in range(1, world):
+            assert st[k] == st[0]
+    finally:
+        for c in ctxs:
+            c.close()
+
+
 def test_group_local_check_ratios():
     _need_gpu()
     world = 2
-    for variant in ("static", "ll"):
+    for variant in ("static", "ll", "ll128"):
         ctxs = _group(world, variant, check_ratios=True)
         streams = [torch.cuda.Stream() for _ in range(world)]
         try:

@@ -30,7 +30,7 @@ def _port():
     return p
 
 
-@pytest.fixture(scope="module", params=["static", "dyn", "push", "pushdyn", "oneshot", "ll"])
+@pytest.fixture(scope="module", params=["static", "dyn", "push", "pushdyn", "oneshot", "ll", "ll128"])
 def results(request):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -47,7 +47,10 @@ def results(request):
                # the larger pieces of case (4), fall back to two-shot: mixed sequences)
                CANNIKIN_AR_ONESHOT="1" if request.param == "oneshot" else "0",
                # "ll": buckets <= 256 KiB through the low-latency kernel (no heap bucket needed)
-               CANNIKIN_AR_LL="1" if request.param == "ll" else "0")
+               CANNIKIN_AR_LL="1" if request.param == "ll" else "0",
+               # "ll128": every bucket up to 64 MiB (all but the 355M full-size case) through the
+               # flag-in-line two-shot kernel
+               CANNIKIN_AR_LL128="1" if request.param == "ll128" else "0")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     return world, d
@@ -125,7 +128,7 @@ def test_result_bits_independent_of_variant():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for dtype in ("f32", "bf16"):
         ref = np.load(os.path.join(d, f"rank0_var_static_{dtype}.npy"))
-        for name in ("static", "dyn", "push", "pushdyn", "oneshot", "ll"):
+        for name in ("static", "dyn", "push", "pushdyn", "oneshot", "ll", "ll128"):
             for k in range(world):
                 got = np.load(os.path.join(d, f"rank{k}_var_{name}_{dtype}.npy"))
                 assert np.array_equal(got, ref), (name, dtype, k)

@@ -49,7 +49,7 @@ def main():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--grids", default="0")
     ap.add_argument("--variants", default="0",
-                    help="CANNIKIN_AR_DYN values (two-shot), 'push', 'oneshot' (2 vectors per thread), 'oneshot1', 'pushdyn[:chunk_kb]' or 'auto'")
+                    help="CANNIKIN_AR_DYN values (two-shot), 'push', 'oneshot' (2 vectors per thread), 'oneshot1', 'pushdyn[:chunk_kb]', 'll', 'll128' or 'auto'")
     ap.add_argument("--sizes-mb", default="1,4,16,64,256,1024")
     ap.add_argument("--total", type=int, default=TOTAL)
     ap.add_argument("--nvls", action="store_true", help="also time the NVLS kernel (fp32)")
@@ -66,10 +66,12 @@ def main():
     combos = [(int(g), v) for g in args.grids.split(",") for v in args.variants.split(",")]
     for grid, var in combos:
         os.environ["CANNIKIN_AR_LL"] = "1" if var == "ll" else "0"
+        os.environ["CANNIKIN_AR_LL128"] = "1" if var == "ll128" else "0"
         if var == "auto":
-            for k in ("CANNIKIN_AR_PUSH", "CANNIKIN_AR_DYN", "CANNIKIN_AR_ONESHOT", "CANNIKIN_AR_LL"):
+            for k in ("CANNIKIN_AR_PUSH", "CANNIKIN_AR_DYN", "CANNIKIN_AR_ONESHOT", "CANNIKIN_AR_LL",
+                      "CANNIKIN_AR_LL128"):
                 os.environ.pop(k, None)
-        elif var == "ll":
+        elif var in ("ll", "ll128"):
             os.environ.update(CANNIKIN_AR_PUSH="0", CANNIKIN_AR_DYN="0", CANNIKIN_AR_ONESHOT="0")
         elif var.startswith("pushdyn"):
             os.environ["CANNIKIN_AR_PUSH"] = "2"
