@@ -109,6 +109,7 @@ static cannikin_status create_local(cannikin_ctx** out, int rank, int world, int
   // LL128 buffers (flag-in-line two-shot for mid-size buckets): 2 parities x {scatter, gather} x
   // W source slots of the largest shard, plus headers; zeroed (flags start at epoch 0)
   if (const char* t = std::getenv("CANNIKIN_AR_LL128")) ctx->ar_ll128 = std::atoi(t) != 0 ? 1 : 0;
+  if (const char* t = std::getenv("CANNIKIN_LL128_FUSE")) ctx->ll128_fuse = std::atoi(t) != 0;
   if (world > 1 && ctx->ar_ll128 != 0) {
     size_t mb = 64;
     if (const char* t = std::getenv("CANNIKIN_LL128_MAX_MB")) mb = (size_t)std::max(1, std::atoi(t));

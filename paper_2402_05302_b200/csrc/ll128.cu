@@ -58,6 +58,7 @@ struct LL128Args {
   float r_me;
   int rank;
   int check_r;
+  int fuse;  // scatter kLagS steps ahead inside the reduction loop (CANNIKIN_LL128_FUSE)
 };
 
 __device__ __forceinline__ void st_vol16(void* p, const uint4& v) {
@@ -211,36 +212,61 @@ __global__ void __launch_bounds__(kL8Threads, 1) ll128_kernel(const LL128Args a)
     g1 = l + c * (size_t)(b + 1) / G;
   };
 
-  // ---- 1. scatter: raw pieces of the other shards, and r_me
+  // per-peer piece bounds live in shared memory (registers are the limit at large W)
+  if (tid < W) {
+    size_t h0, h1;
+    piece(tid, h0, h1);
+    s_h0[tid] = h0;
+    s_h1[tid] = h1;
+    s_lo[tid] = lo(tid);
+  }
+  __syncthreads();
+  // Warp-sequence index t: this warp's t-th group of a piece is h0 + warp + t * 16.
+  auto gcount = [&](int k) -> long {
+    const size_t h0 = s_h0[k] + warp, h1 = s_h1[k];
+    return h0 < h1 ? (long)((h1 - h0 + kL8Warps - 1) / kL8Warps) : 0;
+  };
+  long Tmax = 0;  // longest of the peers' pieces (scatter and gather run over the same pieces)
+#pragma unroll 1
+  for (int k = 0; k < W; ++k)
+    if (k != me) Tmax = gcount(k) > Tmax ? gcount(k) : Tmax;
+  constexpr int kGU = W <= 4 ? 2 : 1;  // steps of every peer in flight
+
+  // ---- 1. scatter: raw pieces of the other shards (groups t < ns are sent), and r_me
+  long ns = 0;
+  auto scatter_to = [&](long tend) {
+    while (ns < tend) {
+      const int nu = (ns + kGU <= tend) ? kGU : 1;
+      uint4 v[kGU][W];
+#pragma unroll
+      for (int u = 0; u < kGU; ++u)
+#pragma unroll
+        for (int jj = 1; jj < W; ++jj) {
+          const int k = (me + jj) % W;
+          const size_t g = s_h0[k] + warp + (size_t)(ns + u) * kL8Warps;
+          if (u < nu && g < s_h1[k]) v[u][jj] = load_payload(a.bucket, a.bytes, g * kGroupPayload + poff, pb);
+        }
+#pragma unroll
+      for (int u = 0; u < kGU; ++u)
+#pragma unroll
+        for (int jj = 1; jj < W; ++jj) {
+          const int k = (me + jj) % W;
+          const size_t g = s_h0[k] + warp + (size_t)(ns + u) * kL8Warps;
+          if (u >= nu || g >= s_h1[k]) continue;
+          if (fl) {
+            v[u][jj].z = e32;
+            v[u][jj].w = (uint32_t)(e >> 32);
+          }
+          st_vol16(data(k, 0, me) + (size_t)lane * 16 + (g - s_lo[k]) * kGroupWire, v[u][jj]);
+        }
+      ns += nu;
+    }
+  };
+  // fused: only the first kLagS steps now, the rest kLagS steps ahead of the reduction
+  constexpr long kLagS = 2 * kGU;
   if (tid < W && tid != me)
     st_word(hdr(tid, me), ((uint64_t)e32 << 32) | __float_as_uint(a.r_me));
-#pragma unroll 1
-  for (int jj = 1; jj < W; ++jj) {
-    const int k = (me + jj) % W;
-    size_t g0, g1;
-    piece(k, g0, g1);
-    char* dst = data(k, 0, me) + (size_t)lane * 16;
-    const size_t l = lo(k);
-    size_t g = g0 + warp;
-    for (; g + kL8Warps < g1; g += 2 * kL8Warps) {  // two groups per warp in flight
-      uint4 v0 = load_payload(a.bucket, a.bytes, g * kGroupPayload + poff, pb);
-      uint4 v1 = load_payload(a.bucket, a.bytes, (g + kL8Warps) * kGroupPayload + poff, pb);
-      if (fl) {
-        v0.z = v1.z = e32;
-        v0.w = v1.w = (uint32_t)(e >> 32);
-      }
-      st_vol16(dst + (g - l) * kGroupWire, v0);
-      st_vol16(dst + (g - l + kL8Warps) * kGroupWire, v1);
-    }
-    if (g < g1) {
-      uint4 v0 = load_payload(a.bucket, a.bytes, g * kGroupPayload + poff, pb);
-      if (fl) {
-        v0.z = e32;
-        v0.w = (uint32_t)(e >> 32);
-      }
-      st_vol16(dst + (g - l) * kGroupWire, v0);
-    }
-  }
+  scatter_to(a.fuse ? (kLagS < Tmax ? kLagS : Tmax) : Tmax);
   if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
 
   // ---- shares of every rank (header entry b of every source)
@@ -339,25 +365,7 @@ __global__ void __launch_bounds__(kL8Threads, 1) ll128_kernel(const LL128Args a)
     // reduction: the peers reduce their pieces at the same pace, so their groups have landed by
     // the time they are copied and the copy overlaps the NVLink traffic instead of following it.
     // Warp-sequence index t: this warp's t-th group of a piece is g0 + warp + t * 16.
-    // per-peer piece bounds live in shared memory (registers are the limit at large W)
-    if (tid < W) {
-      size_t h0, h1;
-      piece(tid, h0, h1);
-      s_h0[tid] = h0;
-      s_h1[tid] = h1;
-      s_lo[tid] = lo(tid);
-    }
-    __syncthreads();
-    auto gcount = [&](int k) -> long {
-      const size_t h0 = s_h0[k] + warp, h1 = s_h1[k];
-      return h0 < h1 ? (long)((h1 - h0 + kL8Warps - 1) / kL8Warps) : 0;
-    };
-    long Tmax = 0;
-#pragma unroll 1
-    for (int k = 0; k < W; ++k)
-      if (k != me) Tmax = gcount(k) > Tmax ? gcount(k) : Tmax;
     long ng = 0;  // groups t < ng are gathered
-    constexpr int kGU = W <= 4 ? 2 : 1;  // steps of every peer in flight
     auto gather_to = [&](long tend) {
       while (ng < tend) {
         const int nu = (ng + kGU <= tend) ? kGU : 1;
@@ -390,10 +398,15 @@ __global__ void __launch_bounds__(kL8Threads, 1) ll128_kernel(const LL128Args a)
     const long Tme = g0 + warp < g1 ? (long)((g1 - g0 - warp + kL8Warps - 1) / kL8Warps) : 0;
     long t = 0;
     for (; t + kU <= Tme; t += kU) {
+      if (a.fuse) scatter_to(t + kU + kLagS < Tmax ? t + kU + kLagS : Tmax);
       step(g0 + warp + (size_t)t * kL8Warps, std::integral_constant<int, kU>{});
       if (t + kU - kLag > ng) gather_to(t + kU - kLag < Tmax ? t + kU - kLag : Tmax);
     }
-    for (; t < Tme; ++t) step(g0 + warp + (size_t)t * kL8Warps, std::integral_constant<int, 1>{});
+    for (; t < Tme; ++t) {
+      if (a.fuse) scatter_to(t + 1 + kLagS < Tmax ? t + 1 + kLagS : Tmax);
+      step(g0 + warp + (size_t)t * kL8Warps, std::integral_constant<int, 1>{});
+    }
+    scatter_to(Tmax);
     if (tid == 0) a.ctrl->trace[b][2] = dev::globaltimer_ns();
     // statistics row of (me, b) to every peer's header entry b (all reduction done)
     {
@@ -498,6 +511,7 @@ cudaError_t launch_ll128(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dty
   a.r_me = (float)r_i;
   a.rank = ctx->rank;
   a.check_r = ctx->check_ratios;
+  a.fuse = ctx->ll128_fuse;
   // about two groups per warp and phase; every rank derives the same grid from (n, W)
   const size_t per_shard = (a.ngroups + W - 1) / W;
   size_t g = (per_shard + 2 * kL8Warps - 1) / (2 * kL8Warps);
