@@ -619,6 +619,27 @@ def main():
         ddp = {"ms_per_allreduce": round(float(dm.item()), 4),
                "note": "ncclAllReduce(avg) of the same bucket, equal-split DDP semantics (Eq. 2)"}
 
+    # ---- the same weighted all-reduce through NCCL reduce-scatter / all-gather (K4), N > 1
+    if world > 1:
+        for _ in range(3):
+            ta.weighted_allreduce_nccl(ctx, bucket, r[rank])
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            ta.weighted_allreduce_nccl(ctx, bucket, r[rank])
+        e1.record(stream)
+        barrier()
+        km = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda", dtype=torch.float64)
+        dist.all_reduce(km, op=dist.ReduceOp.MAX)
+        ctx.gns_stats()
+        k4ms = float(km.item())
+        ddp["k4_nccl_path"] = {
+            "ms": round(k4ms, 4),
+            "busbw": round(N * s / (k4ms * 1e-3) * 2 * (world - 1) / world / 1e9, 1),
+            "note": "cannikin_weighted_allreduce_nccl: fp32 pre-kernel + ncclReduceScatter + "
+                    "post-kernel + ncclAllGather, same bucket, statistics included"}
+
     # ---- NVSwitch-multicast (NVLS) variant, fp32 sidecar on the same element count (K6)
     nvls = None
     if world > 1 and not args.no_nvls:

@@ -141,6 +141,22 @@ cannikin_status cannikin_free_bucket(cannikin_ctx* ctx, void* dptr);
 cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* bucket, size_t n,
                                             cannikin_dtype dt, double r_i, void* stream);
 
+/* The same operation through NCCL collectives instead of peer memory (the north
+ * star's "NCCL reduce-scatter/all-gather with the r_i scaling and norm partials fused into the
+ * pre- and post-kernels"): pre-kernel y = r_i g_i in fp32 + |g_i|^2 partials -> ncclReduceScatter
+ * (fp32 sum) -> post-kernel (one rounding to dt, |g|^2 partials) -> ncclAllGather of the shards
+ * and of the 2 statistics per rank -> fixed-order accumulation (identical bits on every rank).
+ * Same arguments, contract and statistics as cannikin_weighted_allreduce (Eq. 9, P:328-331;
+ * Eq. 10 inputs), except: the fp32 summation order is NCCL's, so the result bits differ
+ * from the peer-memory kernels by fp32 rounding (same tolerances); the bucket may be any device
+ * memory (no heap limit); a work buffer of ~8 n bytes is allocated on first use / growth, which
+ * synchronises the device.  Needs no peer mapping: the path for ranks NCCL connects but NVLink
+ * peer memory does not.  COLLECTIVE.  world == 1: as cannikin_weighted_allreduce.
+ * Errors: INVALID (NULL, misaligned), UNSUPPORTED (dtype; in-process group: no communicator),
+ * DOMAIN (r_i NaN), CUDA, NCCL. */
+cannikin_status cannikin_weighted_allreduce_nccl(cannikin_ctx* ctx, void* bucket, size_t n,
+                                                 cannikin_dtype dt, double r_i, void* stream);
+
 /* NVSwitch-multicast (NVLS) variant of cannikin_weighted_allreduce, world >= 2.
  *   bucket    : this rank's copy of a symmetric, multicast-capable allocation (e.g. torch symmetric
  *               memory), n elements, 16-byte aligned, n * sizeof(dt) a multiple of 16; in place.

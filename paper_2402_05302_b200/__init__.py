@@ -7,6 +7,7 @@ Entry points mirror include/cannikin.h:
     Context(...)                      cannikin_init / cannikin_destroy
     Context.alloc_bucket / free_bucket
     Context.weighted_allreduce        Eq. 9 + fused |g_i|^2, |g|^2
+    Context.weighted_allreduce_nccl   the same through NCCL reduce-scatter / all-gather (K4)
     Context.gns_stats                 finalise the norm statistics
     Context.weighted_sum_local        emulated ranks on one GPU
     gns_estimate                      Eq. 10 + Theorem 1
@@ -91,6 +92,7 @@ SIGNATURES = {
     "cannikin_free_bucket": (_I, [_P, _P]),
     "cannikin_weighted_allreduce": (_I, [_P, _P, _Z, _I, _D, _P]),
     "cannikin_weighted_allreduce_nvls": (_I, [_P, _P, _P, _Z, _I, _D, _P]),
+    "cannikin_weighted_allreduce_nccl": (_I, [_P, _P, _Z, _I, _D, _P]),
     "cannikin_gns_stats": (_I, [_P, _P, _DP, _DP]),
     "cannikin_gns_stats_async": (_I, [_P, _P, _P]),
     "cannikin_device_status": (_I, [_P]),
@@ -218,6 +220,9 @@ class Context:
 
     def weighted_allreduce(self, ptr: int, n: int, dtype: int, r_i: float, stream=None):
         _check(lib().cannikin_weighted_allreduce(self._h, ptr, n, dtype, r_i, _stream(stream)))
+
+    def weighted_allreduce_nccl(self, ptr: int, n: int, dtype: int, r_i: float, stream=None):
+        _check(lib().cannikin_weighted_allreduce_nccl(self._h, ptr, n, dtype, r_i, _stream(stream)))
 
     def weighted_allreduce_nvls(self, ptr: int, mc_ptr: int, n: int, dtype: int, r_i: float,
                                 stream=None):

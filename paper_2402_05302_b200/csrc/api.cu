@@ -51,6 +51,7 @@ static cannikin_status destroy_partial(cannikin_ctx* ctx) {
     if (j != ctx->rank && ctx->peer_base[j] && !ctx->in_process) cudaIpcCloseMemHandle(ctx->peer_base[j]);
   if (ctx->nccl_comm) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl_comm));
   if (ctx->base) cudaFree(ctx->base);
+  if (ctx->k4_buf) cudaFree(ctx->k4_buf);
   if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
   delete ctx;
   return CANNIKIN_OK;
@@ -424,6 +425,34 @@ extern "C" cannikin_status cannikin_ddp_allreduce_mean(cannikin_ctx* ctx, void* 
   CK_NCCL(ncclAllReduce(bucket, bucket, n, dt == CANNIKIN_F32 ? ncclFloat32 : ncclBfloat16, ncclAvg,
                         static_cast<ncclComm_t>(ctx->nccl_comm), S(stream)));
   return CANNIKIN_OK;
+}
+
+extern "C" cannikin_status cannikin_weighted_allreduce_nccl(cannikin_ctx* ctx, void* bucket,
+                                                            size_t n, cannikin_dtype dt,
+                                                            double r_i, void* stream) {
+  if (!ctx) return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_nccl: ctx == NULL");
+  ctx->last_launches = 0;
+  if (dt != CANNIKIN_F32 && dt != CANNIKIN_BF16)
+    return fail(CANNIKIN_ERR_UNSUPPORTED, "weighted_allreduce_nccl: dtype %d", (int)dt);
+  if (n == 0) return CANNIKIN_OK;
+  if (!bucket) return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_nccl: bucket == NULL");
+  if (reinterpret_cast<uintptr_t>(bucket) % 16)
+    return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_nccl: bucket not 16-byte aligned");
+  if (!(r_i == r_i)) return fail(CANNIKIN_ERR_DOMAIN, "weighted_allreduce_nccl: r_i is NaN");
+  if (ctx->world == 1) return cannikin_weighted_allreduce(ctx, bucket, n, dt, r_i, stream);
+  if (!ctx->nccl_comm)
+    return fail(CANNIKIN_ERR_UNSUPPORTED, "weighted_allreduce_nccl: no NCCL communicator (in-process group)");
+  CK_CUDA(cudaSetDevice(ctx->device));
+  const size_t need = cannikin::k4_buffer_bytes(ctx->world, n);
+  if (need > ctx->k4_bytes) {  // grow (synchronises the device: first use or a larger bucket)
+    CK_CUDA(cudaDeviceSynchronize());
+    if (ctx->k4_buf) CK_CUDA(cudaFree(ctx->k4_buf));
+    ctx->k4_buf = nullptr;
+    ctx->k4_bytes = 0;
+    CK_CUDA(cudaMalloc(&ctx->k4_buf, need));
+    ctx->k4_bytes = need;
+  }
+  return cannikin::launch_k4(ctx, bucket, n, dt, r_i, S(stream));
 }
 
 extern "C" int cannikin_last_launch_count(cannikin_ctx* ctx) { return ctx ? ctx->last_launches : 0; }

@@ -48,5 +48,8 @@ size_t ll128_region_bytes(int world, size_t max_bytes);
 bool ll128_eligible(const cannikin_ctx* ctx, size_t bytes);
 cudaError_t launch_ll128(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt, double r_i,
                          cudaStream_t st);
+size_t k4_buffer_bytes(int world, size_t n);
+cannikin_status launch_k4(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt, double r_i,
+                          cudaStream_t st);
 
 }  // namespace cannikin

@@ -51,6 +51,14 @@ def weighted_allreduce(ctx: Context, bucket: torch.Tensor, r_i: float, stream=No
                            _cur(stream))
 
 
+def weighted_allreduce_nccl(ctx: Context, bucket: torch.Tensor, r_i: float, stream=None):
+    """As weighted_allreduce, through NCCL reduce-scatter / all-gather with fused pre/post kernels
+    (K4): any device tensor, no peer mapping."""
+    assert bucket.is_cuda and bucket.is_contiguous()
+    ctx.weighted_allreduce_nccl(bucket.data_ptr(), bucket.numel(), dtype_code(bucket.dtype), r_i,
+                                _cur(stream))
+
+
 def weighted_sum_local(ctx: Context, grads, r, out: torch.Tensor, local_sq: torch.Tensor,
                        global_sq: torch.Tensor, accumulate: bool = False, stream=None,
                        variant=None):

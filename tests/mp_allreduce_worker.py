@@ -163,6 +163,8 @@ def main():
         dist.destroy_process_group()
         return
     ctx = ta.init_distributed_context(heap_bytes=maxN * 4 + 4096, grid=args.grid)
+    # CANNIKIN_TEST_PATH=nccl: the cases go through the NCCL path (K4) instead of the P2P kernels
+    AR = ta.weighted_allreduce_nccl if os.environ.get("CANNIKIN_TEST_PATH") == "nccl" else ta.weighted_allreduce
     tdt = {"f32": torch.float32, "bf16": torch.bfloat16}
     for name, N, dtype, seed in CASES:
         b = b_for(world, seed)
@@ -171,25 +173,25 @@ def main():
         # (1) zero-copy bucket in the symmetric heap
         bucket = ta.bucket_tensor(ctx, N, tdt[dtype])
         bucket.copy_(to_dev(gs[rank], dtype))
-        ta.weighted_allreduce(ctx, bucket, b[rank] / B)
+        AR(ctx, bucket, b[rank] / B)
         loc, glob = ctx.gns_stats()
         out1 = from_dev(bucket, dtype)
         # (2) again (determinism, flag epochs advance)
         bucket.copy_(to_dev(gs[rank], dtype))
-        ta.weighted_allreduce(ctx, bucket, b[rank] / B)
+        AR(ctx, bucket, b[rank] / B)
         loc2, glob2 = ctx.gns_stats()
         out2 = from_dev(bucket, dtype)
         ta.free_bucket_tensor(ctx, bucket)
         # (3) ordinary (non-peer-mapped) torch tensor: staged through the heap scratch
         t = to_dev(gs[rank], dtype)
-        ta.weighted_allreduce(ctx, t, b[rank] / B)
+        AR(ctx, t, b[rank] / B)
         loc3, glob3 = ctx.gns_stats()
         out3 = from_dev(t, dtype)
         # (4) the same gradient as 3 buckets of different sizes; stats accumulate over buckets
         t = to_dev(gs[rank], dtype)
         cuts = sorted({0, N // 3 - (N // 3) % 8, (2 * N) // 3 - ((2 * N) // 3) % 8, N})
         for a, c in zip(cuts[:-1], cuts[1:]):
-            ta.weighted_allreduce(ctx, t[a:c], b[rank] / B)
+            AR(ctx, t[a:c], b[rank] / B)
         loc4, glob4 = ctx.gns_stats()
         out4 = from_dev(t, dtype)
         np.savez(os.path.join(args.out, f"rank{rank}_{name}.npz"), out1=out1, out2=out2,

@@ -1,4 +1,5 @@
-"""Multi-GPU parity of cannikin_weighted_allreduce (two-shot / one-shot NVLink kernels) against the oracle,
+"""Multi-GPU parity of cannikin_weighted_allreduce (every NVLink kernel variant) and of
+cannikin_weighted_allreduce_nccl (K4) against the oracle,
 bitwise identity across ranks, run-to-run determinism, staging path, multi-bucket stats.
 Runs tests/mp_allreduce_worker.py under torchrun on every visible GPU (2..8)."""
 import os
@@ -30,7 +31,7 @@ def _port():
     return p
 
 
-@pytest.fixture(scope="module", params=["static", "dyn", "push", "pushdyn", "oneshot", "ll", "ll128"])
+@pytest.fixture(scope="module", params=["static", "dyn", "push", "pushdyn", "oneshot", "ll", "ll128", "nccl"])
 def results(request):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -50,7 +51,10 @@ def results(request):
                CANNIKIN_AR_LL="1" if request.param == "ll" else "0",
                # "ll128": every bucket up to 64 MiB (all but the 355M full-size case) through the
                # flag-in-line two-shot kernel
-               CANNIKIN_AR_LL128="1" if request.param == "ll128" else "0")
+               CANNIKIN_AR_LL128="1" if request.param == "ll128" else "0",
+               # "nccl": the cases through cannikin_weighted_allreduce_nccl (K4: NCCL
+               # reduce-scatter / all-gather with fused pre/post kernels)
+               CANNIKIN_TEST_PATH="nccl" if request.param == "nccl" else "p2p")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     return world, d

@@ -49,7 +49,7 @@ def main():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--grids", default="0")
     ap.add_argument("--variants", default="0",
-                    help="CANNIKIN_AR_DYN values (two-shot), 'push', 'oneshot' (2 vectors per thread), 'oneshot1', 'pushdyn[:chunk_kb]', 'll', 'll128' or 'auto'")
+                    help="CANNIKIN_AR_DYN values (two-shot), 'push', 'oneshot' (2 vectors per thread), 'oneshot1', 'pushdyn[:chunk_kb]', 'll', 'll128', 'k4' (NCCL path) or 'auto'")
     ap.add_argument("--sizes-mb", default="1,4,16,64,256,1024")
     ap.add_argument("--total", type=int, default=TOTAL)
     ap.add_argument("--nvls", action="store_true", help="also time the NVLS kernel (fp32)")
@@ -71,7 +71,7 @@ def main():
             for k in ("CANNIKIN_AR_PUSH", "CANNIKIN_AR_DYN", "CANNIKIN_AR_ONESHOT", "CANNIKIN_AR_LL",
                       "CANNIKIN_AR_LL128"):
                 os.environ.pop(k, None)
-        elif var in ("ll", "ll128"):
+        elif var in ("ll", "ll128", "k4"):
             os.environ.update(CANNIKIN_AR_PUSH="0", CANNIKIN_AR_DYN="0", CANNIKIN_AR_ONESHOT="0")
         elif var.startswith("pushdyn"):
             os.environ["CANNIKIN_AR_PUSH"] = "2"
@@ -96,9 +96,11 @@ def main():
             nb = len(cuts) - 1
             reps = max(1, min(20, int(2e9 // (N * s)), 4096 // nb))
 
+            AR = ta.weighted_allreduce_nccl if var == "k4" else ta.weighted_allreduce
+
             def ours():
                 for a, c in zip(cuts[:-1], cuts[1:]):
-                    ta.weighted_allreduce(ctx, bucket[a:c], r)
+                    AR(ctx, bucket[a:c], r)
                 ctx.gns_stats_async(stats.data_ptr(), torch.cuda.current_stream())
 
             def nccl():
