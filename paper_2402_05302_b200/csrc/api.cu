@@ -110,11 +110,14 @@ static cannikin_status create_local(cannikin_ctx** out, int rank, int world, int
   // LL128 buffers (flag-in-line two-shot for mid-size buckets): 2 parities x {scatter, gather} x
   // W source slots of the largest shard, plus headers; zeroed (flags start at epoch 0)
   if (const char* t = std::getenv("CANNIKIN_AR_LL128")) ctx->ar_ll128 = std::atoi(t) != 0 ? 1 : 0;
-  if (const char* t = std::getenv("CANNIKIN_LL128_FUSE")) ctx->ll128_fuse = std::atoi(t) != 0;
-  if (world > 1 && ctx->ar_ll128 != 0) {
+  if (const char* t = std::getenv("CANNIKIN_AR_LL128OS")) ctx->ar_ll128os = std::atoi(t) != 0 ? 1 : 0;
+  if (world > 1 && (ctx->ar_ll128 != 0 || ctx->ar_ll128os != 0)) {
     size_t mb = 64;
     if (const char* t = std::getenv("CANNIKIN_LL128_MAX_MB")) mb = (size_t)std::max(1, std::atoi(t));
     ctx->ll128_max_bytes = mb << 20;
+    ctx->ll128os_auto_bytes = cannikin::ll128os_auto_bytes(world);
+    if (const char* t = std::getenv("CANNIKIN_LL128OS_AUTO_KB"))
+      ctx->ll128os_auto_bytes = (size_t)std::max(0, std::atoi(t)) << 10;
     ctx->ll128_off = ctx->total_bytes;
     ctx->total_bytes += align_up(cannikin::ll128_region_bytes(world, ctx->ll128_max_bytes), 4096);
   }
@@ -297,6 +300,12 @@ extern "C" cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* 
     const double r[1] = {r_i};
     CK_CUDA(cannikin::launch_wsum_local(ctx, in, 1, r, bucket, n, dt, &ctx->ctrl->stats[0],
                                         &ctx->ctrl->stats[1], true, 0, S(stream)));
+    ctx->last_launches = 1;
+    return CANNIKIN_OK;
+  }
+  if (cannikin::ll128os_eligible(ctx, bytes)) {
+    // one-shot LL128: the whole bucket to every peer, every rank reduces it by itself
+    CK_CUDA(cannikin::launch_ll128os(ctx, bucket, n, dt, r_i, S(stream)));
     ctx->last_launches = 1;
     return CANNIKIN_OK;
   }

@@ -61,7 +61,8 @@ struct cannikin_ctx {
   int ar_ll = -1;           // CANNIKIN_AR_LL=0|1 forbids/prefers the LL kernel; -1 = by size
   size_t ll_max_bytes = 0;  // largest LL bucket = its slot payload: 2 MiB / (W - 1), 64 KiB steps
   int ar_ll128 = -1;        // CANNIKIN_AR_LL128=0|1 forbids/prefers the LL128 kernel; -1 = by size
-  int ll128_fuse = 0;       // CANNIKIN_LL128_FUSE: scatter inside the reduction loop
+  int ar_ll128os = -1;      // CANNIKIN_AR_LL128OS=0|1 forbids/prefers the one-shot LL128 kernel
+  size_t ll128os_auto_bytes = 0;  // its automatic limit (CANNIKIN_LL128OS_AUTO_KB overrides)
   size_t ll128_max_bytes = 0;  // largest LL128 bucket (CANNIKIN_LL128_MAX_MB), sizes its slots
   int ar_oneshot = -1;      // CANNIKIN_AR_ONESHOT=0|1 forbids/prefers one-shot; -1 = by size
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2

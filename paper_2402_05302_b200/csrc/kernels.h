@@ -48,6 +48,10 @@ size_t ll128_region_bytes(int world, size_t max_bytes);
 bool ll128_eligible(const cannikin_ctx* ctx, size_t bytes);
 cudaError_t launch_ll128(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt, double r_i,
                          cudaStream_t st);
+size_t ll128os_auto_bytes(int world);
+bool ll128os_eligible(const cannikin_ctx* ctx, size_t bytes);
+cudaError_t launch_ll128os(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt,
+                           double r_i, cudaStream_t st);
 size_t k4_buffer_bytes(int world, size_t n);
 cannikin_status launch_k4(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt, double r_i,
                           cudaStream_t st);

@@ -132,13 +132,14 @@ def main():
         return
     if args.variants:
         # the same inputs through every K3 variant: the result bits must not depend on it
-        VARS = {"static": ("0", "0", "0", "0", "0"), "dyn": ("1", "0", "0", "0", "0"),
-                "push": ("0", "1", "0", "0", "0"), "pushdyn": ("0", "2", "0", "0", "0"),
-                "oneshot": ("0", "0", "1", "0", "0"), "ll": ("0", "0", "0", "1", "0"),
-                "ll128": ("0", "0", "0", "0", "1")}
-        for name, (dyn, push, one, ll, ll128) in VARS.items():
+        VARS = {"static": ("0", "0", "0", "0", "0", "0"), "dyn": ("1", "0", "0", "0", "0", "0"),
+                "push": ("0", "1", "0", "0", "0", "0"), "pushdyn": ("0", "2", "0", "0", "0", "0"),
+                "oneshot": ("0", "0", "1", "0", "0", "0"), "ll": ("0", "0", "0", "1", "0", "0"),
+                "ll128": ("0", "0", "0", "0", "1", "0"), "ll128os": ("0", "0", "0", "0", "0", "1")}
+        for name, (dyn, push, one, ll, ll128, ll128os) in VARS.items():
             os.environ.update(CANNIKIN_AR_DYN=dyn, CANNIKIN_AR_PUSH=push, CANNIKIN_AR_ONESHOT=one,
-                              CANNIKIN_AR_LL=ll, CANNIKIN_AR_LL128=ll128, CANNIKIN_PD_CHUNK_KB="16")
+                              CANNIKIN_AR_LL=ll, CANNIKIN_AR_LL128=ll128,
+                              CANNIKIN_AR_LL128OS=ll128os, CANNIKIN_PD_CHUNK_KB="16")
             ctx = ta.init_distributed_context(heap_bytes=(1 << 22), grid=args.grid)
             for N, dtype in ((100_003, "f32"), (200_011, "bf16")):
                 b = b_for(world, 21)

@@ -22,12 +22,16 @@ from paper_2402_05302_b200 import torch_api as ta  # noqa: E402
 
 TOL = {"f32": 1e-5, "bf16": 1e-2}
 TDT = {"f32": torch.float32, "bf16": torch.bfloat16}
-VARIANTS = {  # CANNIKIN_AR_DYN, _PUSH, _ONESHOT, _LL, _LL128
-    "static": ("0", "0", "0", "0", "0"), "dyn": ("1", "0", "0", "0", "0"),
-    "push": ("0", "1", "0", "0", "0"), "pushdyn": ("0", "2", "0", "0", "0"),
-    "oneshot": ("0", "0", "1", "0", "0"), "ll": ("0", "0", "0", "1", "0"),
-    "ll128": ("0", "0", "0", "0", "1"),
+VARIANTS = {  # CANNIKIN_AR_DYN, _PUSH, _ONESHOT, _LL, _LL128, _LL128OS
+    "static": ("0", "0", "0", "0", "0", "0"), "dyn": ("1", "0", "0", "0", "0", "0"),
+    "push": ("0", "1", "0", "0", "0", "0"), "pushdyn": ("0", "2", "0", "0", "0", "0"),
+    "oneshot": ("0", "0", "1", "0", "0", "0"), "ll": ("0", "0", "0", "1", "0", "0"),
+    "ll128": ("0", "0", "0", "0", "1", "0"), "ll128os": ("0", "0", "0", "0", "0", "1"),
 }
+# automatic LL128 choice with the one-shot limit lowered to 256 KiB: one-shot and two-shot LL128
+# calls interleave on the same region, epoch and parity sequence
+MIXED_ENV = dict(CANNIKIN_AR_DYN="0", CANNIKIN_AR_PUSH="0", CANNIKIN_AR_ONESHOT="0",
+                 CANNIKIN_AR_LL="0", CANNIKIN_LL128OS_AUTO_KB="256")
 CASES = [(1, "f32", 1), (7, "bf16", 2), (4099, "f32", 3), (300_001, "f32", 4),
          ((1 << 20) + 5, "bf16", 5), (3_000_011, "f32", 6)]
 
@@ -38,10 +42,13 @@ def _need_gpu():
 
 
 def _group(world, variant, check_ratios=False):
-    dyn, push, one, ll, ll128 = VARIANTS[variant]
-    os.environ.update(CANNIKIN_AR_DYN=dyn, CANNIKIN_AR_PUSH=push, CANNIKIN_AR_ONESHOT=one,
-                      CANNIKIN_AR_LL=ll, CANNIKIN_AR_LL128=ll128, CANNIKIN_PD_CHUNK_KB="16",
-                      CANNIKIN_SPIN_TIMEOUT_MS="20000")
+    if variant == "mixed":
+        os.environ.update(MIXED_ENV, CANNIKIN_SPIN_TIMEOUT_MS="20000")
+    else:
+        dyn, push, one, ll, ll128, ll128os = VARIANTS[variant]
+        os.environ.update(CANNIKIN_AR_DYN=dyn, CANNIKIN_AR_PUSH=push, CANNIKIN_AR_ONESHOT=one,
+                          CANNIKIN_AR_LL=ll, CANNIKIN_AR_LL128=ll128, CANNIKIN_AR_LL128OS=ll128os,
+                          CANNIKIN_PD_CHUNK_KB="16", CANNIKIN_SPIN_TIMEOUT_MS="20000")
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     grid = min(32, sms // world)  # W = 8: 18 CTAs per rank, 144 co-resident
     try:
@@ -49,7 +56,8 @@ def _group(world, variant, check_ratios=False):
                                       check_ratios=check_ratios)
     finally:
         for k in ("CANNIKIN_AR_DYN", "CANNIKIN_AR_PUSH", "CANNIKIN_AR_ONESHOT", "CANNIKIN_AR_LL",
-                  "CANNIKIN_AR_LL128", "CANNIKIN_PD_CHUNK_KB"):
+                  "CANNIKIN_AR_LL128", "CANNIKIN_AR_LL128OS", "CANNIKIN_PD_CHUNK_KB",
+                  "CANNIKIN_LL128OS_AUTO_KB"):
             os.environ.pop(k, None)
 
 
@@ -127,7 +135,7 @@ def test_group_local_bits_identical_across_variants():
             assert np.array_equal(out, ref), (key, variant)
 
 
-@pytest.mark.parametrize("variant", ["static", "ll", "ll128"])
+@pytest.mark.parametrize("variant", ["static", "ll", "ll128", "ll128os", "mixed"])
 @pytest.mark.parametrize("world", [2, 4])
 def test_group_local_back_to_back(world, variant):
     """40 calls of mixed sizes and dtypes enqueued back to back (no host sync in between), each on
@@ -168,7 +176,7 @@ def test_group_local_back_to_back(world, variant):
 def test_group_local_check_ratios():
     _need_gpu()
     world = 2
-    for variant in ("static", "ll", "ll128"):
+    for variant in ("static", "ll", "ll128", "ll128os"):
         ctxs = _group(world, variant, check_ratios=True)
         streams = [torch.cuda.Stream() for _ in range(world)]
         try:

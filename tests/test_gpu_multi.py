@@ -31,7 +31,8 @@ def _port():
     return p
 
 
-@pytest.fixture(scope="module", params=["static", "dyn", "push", "pushdyn", "oneshot", "ll", "ll128", "nccl"])
+@pytest.fixture(scope="module", params=["static", "dyn", "push", "pushdyn", "oneshot", "ll", "ll128", "ll128os",
+                                               "nccl"])
 def results(request):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -52,6 +53,8 @@ def results(request):
                # "ll128": every bucket up to 64 MiB (all but the 355M full-size case) through the
                # flag-in-line two-shot kernel
                CANNIKIN_AR_LL128="1" if request.param == "ll128" else "0",
+               # "ll128os": its one-shot form for every bucket its slots hold (all but C5 full)
+               CANNIKIN_AR_LL128OS="1" if request.param == "ll128os" else "0",
                # "nccl": the cases through cannikin_weighted_allreduce_nccl (K4: NCCL
                # reduce-scatter / all-gather with fused pre/post kernels)
                CANNIKIN_TEST_PATH="nccl" if request.param == "nccl" else "p2p")
@@ -132,7 +135,7 @@ def test_result_bits_independent_of_variant():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for dtype in ("f32", "bf16"):
         ref = np.load(os.path.join(d, f"rank0_var_static_{dtype}.npy"))
-        for name in ("static", "dyn", "push", "pushdyn", "oneshot", "ll", "ll128"):
+        for name in ("static", "dyn", "push", "pushdyn", "oneshot", "ll", "ll128", "ll128os"):
             for k in range(world):
                 got = np.load(os.path.join(d, f"rank{k}_var_{name}_{dtype}.npy"))
                 assert np.array_equal(got, ref), (name, dtype, k)

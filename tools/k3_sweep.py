@@ -67,11 +67,12 @@ def main():
     for grid, var in combos:
         os.environ["CANNIKIN_AR_LL"] = "1" if var == "ll" else "0"
         os.environ["CANNIKIN_AR_LL128"] = "1" if var == "ll128" else "0"
+        os.environ["CANNIKIN_AR_LL128OS"] = "1" if var == "ll128os" else "0"
         if var == "auto":
             for k in ("CANNIKIN_AR_PUSH", "CANNIKIN_AR_DYN", "CANNIKIN_AR_ONESHOT", "CANNIKIN_AR_LL",
-                      "CANNIKIN_AR_LL128"):
+                      "CANNIKIN_AR_LL128", "CANNIKIN_AR_LL128OS"):
                 os.environ.pop(k, None)
-        elif var in ("ll", "ll128", "k4"):
+        elif var in ("ll", "ll128", "ll128os", "k4"):
             os.environ.update(CANNIKIN_AR_PUSH="0", CANNIKIN_AR_DYN="0", CANNIKIN_AR_ONESHOT="0")
         elif var.startswith("pushdyn"):
             os.environ["CANNIKIN_AR_PUSH"] = "2"
