@@ -129,9 +129,9 @@ cannikin_status cannikin_free_bucket(cannikin_ctx* ctx, void* dptr);
  * with the scaling, the fp32 accumulation in rank order, both norms and the partial exchange
  * fused (DESIGN.md §6 K3).  Variant by size (a function of n, dt, world and grid only, so every
  * rank picks the same): low-latency LL (<= 2 MiB / (world-1): data and flag in one 8-byte NVLink
- * store, no barrier; the bucket may then be any device memory), LL128 (above that, up to 32 MiB
- * at world 2 and 16 MiB from world 4: two-shot with the epoch flag inside every 128-byte line,
- * no barrier, any device memory), two-shot pull (static, or
+ * store, no barrier; the bucket may then be any device memory), LL128 (above that, up to
+ * 32 MiB: two-shot with the epoch flag inside every 128-byte line, no barrier, any device memory),
+ * two-shot pull (static, or
  * dynamic chunks for shards >= 64 MiB), two-shot push (world >= 4, buckets >= 128 MiB: every
  * NVLink transfer a write); one-shot and dynamic push on request.  CANNIKIN_AR_* environment
  * knobs force one (CANNIKIN_AR_LL128=1: every bucket up to CANNIKIN_LL128_MAX_MB, default 64).

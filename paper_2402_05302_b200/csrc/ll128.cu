@@ -678,10 +678,13 @@ size_t ll128os_max_bytes(int world, size_t max_bytes) {
 }
 
 // Automatic range (measured, profiles/r01/k3_ll128c_*): above the LL kernel's limit and up to
-// 32 MiB at W = 2 (two-shot wins from 64 MiB: 567 vs 549 GB/s; 32 MiB 516 vs 504), 16 MiB from
-// W = 4 (32 MiB: 540 vs 544, a tie; 16 MiB 504 vs 478).  CANNIKIN_AR_LL128=1 extends it to the
-// buffer size (CANNIKIN_LL128_MAX_MB, default 64).
-size_t ll128_auto_bytes(int world) { return world <= 2 ? (size_t)32 << 20 : (size_t)16 << 20; }
+// 32 MiB: at W = 2 the two-shot wins from 64 MiB (567 vs 549 GB/s; 32 MiB 516 vs 504), at W = 4
+// 32 MiB is a tie for heap buckets (540 vs 544; 16 MiB 504 vs 478) -- and a bucket outside the
+// heap would cost the two-shot two staging copies, the LL128 kernel none (DDP's 25 MB buckets).
+// The choice depends only on (bytes, world), never on where the bucket lives, so every rank
+// picks the same kernel.  CANNIKIN_AR_LL128=1 extends it to the buffer size
+// (CANNIKIN_LL128_MAX_MB, default 64).
+size_t ll128_auto_bytes(int) { return (size_t)32 << 20; }
 
 bool ll128_eligible(const cannikin_ctx* ctx, size_t bytes) {
   if (ctx->world < 2 || !ctx->ll128_off || ctx->ar_ll128 == 0) return false;
