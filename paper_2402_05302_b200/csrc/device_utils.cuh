@@ -85,6 +85,57 @@ struct Vec<__nv_bfloat16> {
   }
 };
 
+// ------------------------------------------------------------------ packed fp32x2 arithmetic
+// sm_100's FFMA2: two independent fp32 FMAs (each rounded exactly as fmaf) in one instruction.
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  return ((uint64_t)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ float f2lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+// The emulated-rank pass over one 16-byte vector index (K2, both variants): out = sum_j r_j x_j in
+// rank order from 0 (fp32 fma: the same bits as a scalar fmaf chain), |x_j|^2 and |out|^2 of the
+// vector in fp32 (even and odd elements in two chains, then added), accumulated in fp64.
+template <typename T, int NR>
+__device__ __forceinline__ void wsum16(const uint4 (&x)[NR], const float (&r)[NR], char* dst,
+                                       double (&lsq)[NR], double& gsq) {
+  using V = Vec<T>;
+  constexpr int E = V::E;
+  constexpr int P = E / 2;
+  uint64_t acc[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) acc[p] = 0ull;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    float g[E];
+    V::unpack(x[j], g);
+    const uint64_t rr = f2pack(r[j], r[j]);
+    uint64_t sq = 0ull;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const uint64_t gp = f2pack(g[2 * p], g[2 * p + 1]);
+      acc[p] = ffma2(rr, gp, acc[p]);
+      sq = ffma2(gp, gp, sq);
+    }
+    lsq[j] += (double)(f2lo(sq) + f2hi(sq));
+  }
+  uint64_t gs = 0ull;
+  float out[E];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    gs = ffma2(acc[p], acc[p], gs);
+    out[2 * p] = f2lo(acc[p]);
+    out[2 * p + 1] = f2hi(acc[p]);
+  }
+  gsq += (double)(f2lo(gs) + f2hi(gs));
+  st16(dst, V::pack(out));
+}
+
 // ------------------------------------------------------------------ deterministic reductions
 // Butterfly over the 32 lanes: every lane ends with the same, order-fixed sum.
 __device__ __forceinline__ double warp_sum(double v) {

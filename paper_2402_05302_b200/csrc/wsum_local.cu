@@ -20,33 +20,6 @@
 namespace cannikin {
 
 
-template <typename T, int NR>
-__device__ __forceinline__ void wsum_vec(const uint4 (&x)[NR], const float (&r)[NR], char* dst,
-                                         double (&lsq)[NR], double& gsq) {
-  using V = dev::Vec<T>;
-  constexpr int E = V::E;
-  float acc[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) acc[e] = 0.0f;
-#pragma unroll
-  for (int j = 0; j < NR; ++j) {
-    float g[E];
-    V::unpack(x[j], g);
-    float sq = 0.0f;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      acc[e] = fmaf(r[j], g[e], acc[e]);
-      sq = fmaf(g[e], g[e], sq);
-    }
-    lsq[j] += (double)sq;
-  }
-  float gs = 0.0f;
-#pragma unroll
-  for (int e = 0; e < E; ++e) gs = fmaf(acc[e], acc[e], gs);
-  gsq += (double)gs;
-  dev::st16(dst, V::pack(acc));
-}
-
 template <typename T, int NR, int U, int NT>
 __global__ void __launch_bounds__(NT) wsum_local_kernel(const LocalArgs a) {
   using V = dev::Vec<T>;
@@ -81,13 +54,13 @@ __global__ void __launch_bounds__(NT) wsum_local_kernel(const LocalArgs a) {
 #pragma unroll
       for (int j = 0; j < NR; ++j) x[u][j] = dev::ld16(in[j] + (v + u * stride) * 16);
 #pragma unroll
-    for (int u = 0; u < U; ++u) wsum_vec<T, NR>(x[u], r, a.out + (v + u * stride) * 16, lsq, gsq);
+    for (int u = 0; u < U; ++u) dev::wsum16<T, NR>(x[u], r, a.out + (v + u * stride) * 16, lsq, gsq);
   }
   for (; v < a.nvec; v += stride) {
     uint4 x[NR];
 #pragma unroll
     for (int j = 0; j < NR; ++j) x[j] = dev::ld16(in[j] + v * 16);
-    wsum_vec<T, NR>(x, r, a.out + v * 16, lsq, gsq);
+    dev::wsum16<T, NR>(x, r, a.out + v * 16, lsq, gsq);
   }
   // ragged tail (< one vector of elements) -- scalar, block 0
   if (blockIdx.x == 0) {

@@ -59,33 +59,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 }  // namespace tma
 
-template <typename T, int NR>
-__device__ __forceinline__ void tma_vec(const uint4 (&x)[NR], const float (&r)[NR], char* dst,
-                                        double (&lsq)[NR], double& gsq) {
-  using V = dev::Vec<T>;
-  constexpr int E = V::E;
-  float acc[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) acc[e] = 0.0f;
-#pragma unroll
-  for (int j = 0; j < NR; ++j) {
-    float g[E];
-    V::unpack(x[j], g);
-    float sq = 0.0f;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      acc[e] = fmaf(r[j], g[e], acc[e]);
-      sq = fmaf(g[e], g[e], sq);
-    }
-    lsq[j] += (double)sq;
-  }
-  float gs = 0.0f;
-#pragma unroll
-  for (int e = 0; e < E; ++e) gs = fmaf(acc[e], acc[e], gs);
-  gsq += (double)gs;
-  dev::st16(dst, V::pack(acc));
-}
-
 // tile_vec: 16-byte vectors per rank per tile; stages: ring depth.
 template <typename T, int NR>
 __global__ void __launch_bounds__(tma::kThreads, 1)
@@ -155,7 +128,7 @@ __global__ void __launch_bounds__(tma::kThreads, 1)
 #pragma unroll
         for (int j = 0; j < NR; ++j)
           x[j] = *reinterpret_cast<const uint4*>(st + ((size_t)j * tile_vec + v) * 16);
-        tma_vec<T, NR>(x, r, a.out + (v0 + v) * 16, lsq, gsq);
+        dev::wsum16<T, NR>(x, r, a.out + (v0 + v) * 16, lsq, gsq);
       }
       __syncwarp();
       if (lane == 0) tma::mbar_arrive(&empty[s]);
