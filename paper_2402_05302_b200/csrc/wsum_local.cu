@@ -20,8 +20,16 @@
 namespace cannikin {
 
 
+// Register budget (n <= 8 ranks): 4 resident 256-thread CTAs per SM (<= 64 registers).  With it ptxas keeps the
+// loads of a vector batch closer together (5 of 8 issued ahead of the arithmetic); A/B on one box
+// (profiles/r01/k2_minb_ab.jsonl): C4 0.3256 -> 0.3195 ms, C5 1.970 -> 1.848 ms, against no
+// minimum (60 registers) and 3 CTAs (74 registers, all 8 loads ahead: between the two).
+#ifndef CANNIKIN_K2_MINB
+#define CANNIKIN_K2_MINB 4
+#endif
 template <typename T, int NR, int U, int NT>
-__global__ void __launch_bounds__(NT) wsum_local_kernel(const LocalArgs a) {
+__global__ void __launch_bounds__(NT, NT == 256 && NR <= 8 ? CANNIKIN_K2_MINB : 1)
+    wsum_local_kernel(const LocalArgs a) {
   using V = dev::Vec<T>;
   constexpr int E = V::E;
   __shared__ double red[32 * (NR + 1)];

@@ -1,15 +1,17 @@
-# A/B of the K2 kernel: build/ab/old.so vs build/ab/new.so, interleaved, same box.
+# A/B of K2 builds (build/ab/*.so), interleaved on one box.
 L=paper_2402_05302_b200/libcannikin.so
+cp $L /tmp/keep.so
 for k in 1 2; do
-for v in old new; do
+for v in new mb3 mb4 mb2u2; do
 cp build/ab/$v.so $L
-timeout 600 python tools/k2_sweep.py --shapes c4,c4x2,c4f32,c5 --grids 0 --tma 0 --reps 10 2>/dev/null | grep '^{' | sed "s/^{/{\"build\": \"$v\", /" >> gpurun_out/k2_ab.jsonl
+timeout 600 python tools/k2_sweep.py --shapes c4,c4f32,c5 --grids 0 --tma 0 --reps 10 2>/dev/null | grep '^{' | sed "s/^{/{\"build\": \"$v\", /" >> gpurun_out/k2_ab2.jsonl
 done
 done
-cp build/ab/new.so $L
+cp /tmp/keep.so $L
 python - <<'PY'
-import json
-for l in open("gpurun_out/k2_ab.jsonl"):
-    d=json.loads(l); print(d["build"], d["shape"], d["variant"], d["grid"], d["ms"], d["GBps"])
+import json, collections
+d=collections.defaultdict(list)
+for l in open("gpurun_out/k2_ab2.jsonl"):
+    r=json.loads(l); d[(r["shape"], r["build"])].append(r["ms"])
+for k in sorted(d): print(k, sorted(d[k]))
 PY
-timeout 900 python -m pytest tests/test_gpu_local.py -x -q > gpurun_out/pytest_local.log 2>&1; echo "local tests exit $?"; tail -1 gpurun_out/pytest_local.log
