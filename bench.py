@@ -196,6 +196,27 @@ def nvls_sidecar(ctx, N, rank, world, r_i, steps, dist, ta, torch):
     return res
 
 
+def k4_sidecar(ctx, bucket, N, s, r_i, world, steps, barrier, stream, dist, ta, torch):
+    """cannikin_weighted_allreduce_nccl (K4) on the bench bucket: kernel-path time, max over ranks."""
+    for _ in range(3):
+        ta.weighted_allreduce_nccl(ctx, bucket, r_i)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        ta.weighted_allreduce_nccl(ctx, bucket, r_i)
+    e1.record(stream)
+    barrier()
+    km = torch.tensor([e0.elapsed_time(e1) / steps], device="cuda", dtype=torch.float64)
+    dist.all_reduce(km, op=dist.ReduceOp.MAX)
+    ctx.gns_stats()
+    k4ms = float(km.item())
+    return {"ms": round(k4ms, 4),
+            "busbw": round(N * s / (k4ms * 1e-3) * 2 * (world - 1) / world / 1e9, 1),
+            "note": "cannikin_weighted_allreduce_nccl: fp32 pre-kernel + ncclReduceScatter + "
+                    "post-kernel + ncclAllGather, same bucket, statistics included"}
+
+
 def esize(dtype):
     return 4 if dtype == "f32" else 2
 
@@ -621,24 +642,11 @@ def main():
 
     # ---- the same weighted all-reduce through NCCL reduce-scatter / all-gather (K4), N > 1
     if world > 1:
-        for _ in range(3):
-            ta.weighted_allreduce_nccl(ctx, bucket, r[rank])
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            ta.weighted_allreduce_nccl(ctx, bucket, r[rank])
-        e1.record(stream)
-        barrier()
-        km = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda", dtype=torch.float64)
-        dist.all_reduce(km, op=dist.ReduceOp.MAX)
-        ctx.gns_stats()
-        k4ms = float(km.item())
-        ddp["k4_nccl_path"] = {
-            "ms": round(k4ms, 4),
-            "busbw": round(N * s / (k4ms * 1e-3) * 2 * (world - 1) / world / 1e9, 1),
-            "note": "cannikin_weighted_allreduce_nccl: fp32 pre-kernel + ncclReduceScatter + "
-                    "post-kernel + ncclAllGather, same bucket, statistics included"}
+        try:
+            ddp["k4_nccl_path"] = k4_sidecar(ctx, bucket, N, s, r[rank], world, args.steps,
+                                             barrier, stream, dist, ta, torch)
+        except Exception as e:  # a sidecar must not sink the bench line
+            ddp["k4_nccl_path"] = {"unavailable": str(e)[:200]}
 
     # ---- NVSwitch-multicast (NVLS) variant, fp32 sidecar on the same element count (K6)
     nvls = None
