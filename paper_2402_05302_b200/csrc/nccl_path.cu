@@ -4,7 +4,8 @@
 // baseline next to the fused P2P kernels, and as the path that needs no peer mapping (it runs on
 // anything NCCL connects, including ranks on different nodes).
 //
-//   pre  (K1):  y[e] = r_i g_i[e] in fp32 (bf16 widened exactly), zero padding to W*L;
+//   pre  (K1):  y[e] = r_i g_i[e] in fp32 (bf16 widened exactly), zero padding to W*L (an fp32
+//               bucket of exactly W shards skips y: NCCL's PreMulSum scales in place);
 //               per-CTA partials of |g_i|^2 on the UNSCALED gradient (Eq. 10 input)
 //   ncclReduceScatter(y, sum, fp32), in place: rank k owns y[k L, (k+1) L)      (Eq. 9)
 //   post:       round the owned shard once to the bucket dtype; per-CTA partials of |g|^2 from
@@ -32,6 +33,7 @@ constexpr int kK4Threads = 256;
 constexpr int kK4MaxBlocks = 1024;
 
 // y <- r g (fp32) over 16-byte vectors of g, zero padding up to `padded` elements; partial |g|^2
+// (y == nullptr: the norm only -- the fp32 fast path scales inside NCCL)
 template <typename T>
 __global__ void __launch_bounds__(kK4Threads) k4_pre_kernel(const char* g, size_t n, size_t padded,
                                                             float r, float* y, double* part) {
@@ -51,6 +53,7 @@ __global__ void __launch_bounds__(kK4Threads) k4_pre_kernel(const char* g, size_
       o[q] = r * f[q];
     }
     sq += (double)s;
+    if (y == nullptr) continue;
 #pragma unroll
     for (int q = 0; q < E; q += 4)
       dev::st16(y + v * E + q, make_uint4(__float_as_uint(o[q]), __float_as_uint(o[q + 1]),
@@ -61,8 +64,8 @@ __global__ void __launch_bounds__(kK4Threads) k4_pre_kernel(const char* g, size_
     if (e < n) {
       const float f = V::load1(g + e * sizeof(T));
       sq += (double)(f * f);
-      y[e] = r * f;
-    } else {
+      if (y != nullptr) y[e] = r * f;
+    } else if (y != nullptr) {
       y[e] = 0.0f;
     }
   }
@@ -71,7 +74,8 @@ __global__ void __launch_bounds__(kK4Threads) k4_pre_kernel(const char* g, size_
   if (threadIdx.x == 0) part[blockIdx.x] = v1[0];
 }
 
-// dst[e] <- round(shard[e]) for e < cnt; partial |g|^2 from the fp32 values
+// dst[e] <- round(shard[e]) for e < cnt; partial |g|^2 from the fp32 values (dst == nullptr:
+// the norm only, the shard already is the result)
 template <typename T>
 __global__ void __launch_bounds__(kK4Threads) k4_post_kernel(const float* shard, size_t cnt,
                                                              char* dst, double* part) {
@@ -94,12 +98,12 @@ __global__ void __launch_bounds__(kK4Threads) k4_post_kernel(const float* shard,
 #pragma unroll
     for (int q = 0; q < E; ++q) s = fmaf(f[q], f[q], s);
     sq += (double)s;
-    dev::st16(dst + v * 16, V::pack(f));
+    if (dst != nullptr) dev::st16(dst + v * 16, V::pack(f));
   }
   for (size_t e = nvec * E + (size_t)blockIdx.x * kK4Threads + threadIdx.x; e < cnt; e += stride) {
     const float f = shard[e];
     sq += (double)(f * f);
-    V::store1(dst + e * sizeof(T), f);
+    if (dst != nullptr) V::store1(dst + e * sizeof(T), f);
   }
   double v1[1] = {sq};
   dev::block_sum(v1, red);
@@ -183,18 +187,34 @@ cannikin_status launch_k4(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dt
 
   const int gpre = k4_grid(ctx, padded / 4);
   const int gpost = k4_grid(ctx, L / 4);
-  if (dt == CANNIKIN_F32)
-    k4_pre_kernel<float><<<gpre, kK4Threads, 0, st>>>(static_cast<const char*>(bucket), n, padded,
-                                                       (float)r_i, y, pre);
-  else
-    k4_pre_kernel<__nv_bfloat16><<<gpre, kK4Threads, 0, st>>>(static_cast<const char*>(bucket), n,
-                                                               padded, (float)r_i, y, pre);
-  K4_CUDA(cudaGetLastError());
-  K4_NCCL(ncclReduceScatter(y, y + me * L, L, ncclFloat32, ncclSum, comm, st));
-  if (dt == CANNIKIN_F32)
-    k4_post_kernel<float><<<gpost, kK4Threads, 0, st>>>(y + me * L, cnt, dst, post);
-  else
-    k4_post_kernel<__nv_bfloat16><<<gpost, kK4Threads, 0, st>>>(y + me * L, cnt, dst, post);
+  if (dt == CANNIKIN_F32 && direct) {
+    // fp32 bucket of exactly W shards: NCCL scales (PreMulSum, r_i as a host immediate) and sums
+    // in place; the pre/post kernels only read (norms).  Same arithmetic as the general path.
+    float* gb = static_cast<float*>(bucket);
+    k4_pre_kernel<float><<<gpre, kK4Threads, 0, st>>>(static_cast<const char*>(bucket), n, n,
+                                                       0.0f, nullptr, pre);
+    K4_CUDA(cudaGetLastError());
+    float rf = (float)r_i;
+    ncclRedOp_t op;
+    K4_NCCL(ncclRedOpCreatePreMulSum(&op, &rf, ncclFloat32, ncclScalarHostImmediate, comm));
+    const ncclResult_t rs = ncclReduceScatter(gb, gb + me * L, L, ncclFloat32, op, comm, st);
+    ncclRedOpDestroy(op, comm);
+    K4_NCCL(rs);
+    k4_post_kernel<float><<<gpost, kK4Threads, 0, st>>>(gb + me * L, cnt, nullptr, post);
+  } else {
+    if (dt == CANNIKIN_F32)
+      k4_pre_kernel<float><<<gpre, kK4Threads, 0, st>>>(static_cast<const char*>(bucket), n,
+                                                         padded, (float)r_i, y, pre);
+    else
+      k4_pre_kernel<__nv_bfloat16><<<gpre, kK4Threads, 0, st>>>(static_cast<const char*>(bucket),
+                                                                 n, padded, (float)r_i, y, pre);
+    K4_CUDA(cudaGetLastError());
+    K4_NCCL(ncclReduceScatter(y, y + me * L, L, ncclFloat32, ncclSum, comm, st));
+    if (dt == CANNIKIN_F32)
+      k4_post_kernel<float><<<gpost, kK4Threads, 0, st>>>(y + me * L, cnt, dst, post);
+    else
+      k4_post_kernel<__nv_bfloat16><<<gpost, kK4Threads, 0, st>>>(y + me * L, cnt, dst, post);
+  }
   k4_stats_kernel<<<1, kK4Threads, 0, st>>>(pre, gpre, post, gpost, xs);
   K4_CUDA(cudaGetLastError());
   K4_NCCL(ncclGroupStart());

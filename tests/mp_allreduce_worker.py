@@ -31,6 +31,9 @@ CASES = [  # (name, N, dtype, seed)
     ("resnet50", 25_557_032, "f32", 11),   # configs[2]
     ("os_f32", 300_001, "f32", 8),     # one-shot sized: several CTAs, ragged tail
     ("os_bf16", 600_007, "bf16", 10),
+    # multiples of 64 elements: every shard full (the NCCL path's in-place fast paths)
+    ("pow2_f32", 1 << 20, "f32", 12),
+    ("pow2_bf16", 1 << 21, "bf16", 13),
 ]
 
 

@@ -12,6 +12,9 @@ import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from launch import run_torchrun  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 
 import cannikin_synth as synth  # noqa: E402
@@ -58,7 +61,7 @@ def results(request):
                # "nccl": the cases through cannikin_weighted_allreduce_nccl (K4: NCCL
                # reduce-scatter / all-gather with fused pre/post kernels)
                CANNIKIN_TEST_PATH="nccl" if request.param == "nccl" else "p2p")
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    r = run_torchrun(cmd, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     return world, d
 
@@ -130,7 +133,7 @@ def test_result_bits_independent_of_variant():
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
            os.path.join(os.path.dirname(__file__), "mp_allreduce_worker.py"), "--out", d,
            "--variants"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+    r = run_torchrun(cmd, capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000"))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for dtype in ("f32", "bf16"):
@@ -152,7 +155,7 @@ def test_mixed_sequence_of_sizes_dtypes_and_variants():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
            os.path.join(os.path.dirname(__file__), "mp_allreduce_worker.py"), "--out", d, "--mixed"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,
+    r = run_torchrun(cmd, capture_output=True, text=True, timeout=900,
                        env=dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000"))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for t in range(W.MIXED_CALLS):

@@ -14,6 +14,9 @@ import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from launch import run_torchrun  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 
 from oracle import aggregate as agg  # noqa: E402
@@ -46,7 +49,7 @@ def _run_and_check(cfg, world, d):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
            os.path.join(os.path.dirname(__file__), "mp_allreduce_worker.py"), "--out", d, "--full", cfg]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,
+    r = run_torchrun(cmd, capture_output=True, text=True, timeout=900,
                        env=dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000"))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     ranks = [dict(np.load(os.path.join(d, f"rank{k}_full.npz"))) for k in range(world)]

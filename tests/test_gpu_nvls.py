@@ -10,6 +10,9 @@ import numpy as np
 import pytest
 
 torch = pytest.importorskip("torch")
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from launch import run_torchrun  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 
 import cannikin_synth as synth  # noqa: E402
@@ -39,7 +42,7 @@ def results():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
            os.path.join(os.path.dirname(__file__), "mp_nvls_worker.py"), "--out", d]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,
+    r = run_torchrun(cmd, capture_output=True, text=True, timeout=900,
                        env=dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000"))
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     return world, d
