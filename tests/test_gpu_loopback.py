@@ -296,3 +296,44 @@ def test_group_local_config3_eight_ranks_full_size():
     finally:
         for c in ctxs:
             c.close()
+
+
+@pytest.mark.parametrize("variant", ["ll128", "ll128os"])
+def test_group_local_ll128_size_limit(variant):
+    """The LL128 kernels at their buffer limit (CANNIKIN_LL128_MAX_MB, 64 MiB: 16,777,216 fp32
+    elements) and 4 KiB past it (past the one-shot slot's few extra groups too: the two-shot takes
+    over through the staging copy), W = 2: parity with the oracle and identical bits on both
+    ranks on either side of the boundary."""
+    _need_gpu()
+    world = 2
+    dyn, push, one, ll, ll128, ll128os = VARIANTS[variant]
+    os.environ.update(CANNIKIN_AR_DYN="0", CANNIKIN_AR_PUSH="0", CANNIKIN_AR_ONESHOT="0",
+                      CANNIKIN_AR_LL="0", CANNIKIN_AR_LL128=ll128, CANNIKIN_AR_LL128OS=ll128os,
+                      CANNIKIN_SPIN_TIMEOUT_MS="20000")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    try:
+        ctxs = ck.Context.group_local(world, device=0, heap_bytes=(64 << 20) + 4096,
+                                      grid=sms // world)
+    finally:
+        for k in ("CANNIKIN_AR_DYN", "CANNIKIN_AR_PUSH", "CANNIKIN_AR_ONESHOT", "CANNIKIN_AR_LL",
+                  "CANNIKIN_AR_LL128", "CANNIKIN_AR_LL128OS"):
+            os.environ.pop(k, None)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    try:
+        for N in ((64 << 20) // 4, (64 << 20) // 4 + 1024):
+            b = [37, 91]
+            gs = synth.gns_gradients(world, N, b, seed=N % 1000, dtype="f32")
+            r = agg.ratios(b)
+            ts = [_to_dev(gs[k], "f32") for k in range(world)]
+            _reduce(ctxs, ts, r, streams)
+            st = _stats(ctxs, streams)
+            outs = [_from_dev(t, "f32") for t in ts]
+            g_ref, ls_ref, gsq_ref = agg.aggregate(gs, r, "f32")
+            scale = np.maximum(agg.elementwise_scale([agg.to_f64(g, "f32") for g in gs], r), 1e-30)
+            assert np.max(np.abs(outs[0].astype(np.float64) - g_ref) / scale) <= 1e-5, N
+            assert np.array_equal(outs[0], outs[1]) and st[0] == st[1], N
+            assert np.allclose(st[0][0], ls_ref, rtol=1e-4, atol=0), N
+            assert abs(st[0][1] - gsq_ref) <= 1e-4 * gsq_ref, N
+    finally:
+        for c in ctxs:
+            c.close()
