@@ -178,8 +178,8 @@ __global__ void __launch_bounds__(kL8Threads, 1) ll128_kernel(const LL128Args a)
   __shared__ float s_r[W];
   __shared__ uint32_t s_row[W][NS];
   __shared__ uint64_t s_e;
-  __shared__ char* s_reg[W];
-  __shared__ size_t s_h0[W], s_h1[W], s_lo[W];  // peer regions (indexed by runtime rank: shared, not param space)
+  __shared__ char* s_reg[W];  // peer regions (indexed by runtime rank: shared, not param space)
+  __shared__ size_t s_h0[W], s_h1[W], s_lo[W];  // CTA b's piece of every shard, shard starts
   const int b = blockIdx.x, tid = threadIdx.x, me = a.rank, G = gridDim.x;
   const int lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
@@ -243,7 +243,8 @@ __global__ void __launch_bounds__(kL8Threads, 1) ll128_kernel(const LL128Args a)
         for (int jj = 1; jj < W; ++jj) {
           const int k = (me + jj) % W;
           const size_t g = s_h0[k] + warp + (size_t)(ns + u) * kL8Warps;
-          if (u < nu && g < s_h1[k]) v[u][jj] = load_payload(a.bucket, a.bytes, g * kGroupPayload + poff, pb);
+          if (u < nu && g < s_h1[k])
+            v[u][jj] = load_payload(a.bucket, a.bytes, g * kGroupPayload + poff, pb);
         }
 #pragma unroll
       for (int u = 0; u < kGU; ++u)
@@ -261,8 +262,8 @@ __global__ void __launch_bounds__(kL8Threads, 1) ll128_kernel(const LL128Args a)
       ns += nu;
     }
   };
-  // (sending only a few steps ahead of the reduction instead -- scatter inside the reduction loop
-  // -- measured no faster in the automatic range and costs registers: DESIGN.md §6)
+  // the whole scatter first (sending only a few steps ahead of the reduction instead was measured
+  // no faster in the automatic range and cost registers: DESIGN.md §6)
   if (tid < W && tid != me)
     st_word(hdr(tid, me), ((uint64_t)e32 << 32) | __float_as_uint(a.r_me));
   scatter_to(Tmax);
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(kL8Threads, 1) ll128_kernel(const LL128Args a)
         for (int jj = 1; jj < W; ++jj) st_vol16(dst[jj] + (gu - l) * kGroupWire, y);
       }
     };
-    // ---- 3. (fused) gather the other shards' results into the own bucket, LAG steps behind the
+    // ---- 3. (fused) gather the other shards' results into the own bucket, kLag steps behind the
     // reduction: the peers reduce their pieces at the same pace, so their groups have landed by
     // the time they are copied and the copy overlaps the NVLink traffic instead of following it.
     // Warp-sequence index t: this warp's t-th group of a piece is g0 + warp + t * 16.
