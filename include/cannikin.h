@@ -128,7 +128,7 @@ cannikin_status cannikin_free_bucket(cannikin_ctx* ctx, void* dptr);
  * accumulator that cannikin_gns_stats reads.  Implementation: one kernel over NVLink peer memory
  * with the scaling, the fp32 accumulation in rank order, both norms and the partial exchange
  * fused (DESIGN.md §6 K3).  Variant by size (a function of n, dt, world and grid only, so every
- * rank picks the same): low-latency LL (<= 2 MiB / (world-1): data and flag in one 8-byte NVLink
+ * rank picks the same): low-latency LL (<= 1 MiB / (world-1): data and flag in one 8-byte NVLink
  * store, no barrier; the bucket may then be any device memory), LL128 (above that, up to
  * 32 MiB: two-shot with the epoch flag inside every 128-byte line, no barrier, any device memory),
  * two-shot pull (static, or

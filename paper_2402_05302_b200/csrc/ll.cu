@@ -241,10 +241,12 @@ static cudaError_t dispatch_ll(int W, const LLArgs& a, int grid, cudaStream_t st
 }
 
 // The LL kernel's NVLink bytes, 2 (W-1) N s per direction, grow with W while the two-shot's do
-// not; it wins up to about 2 MiB / (W-1) (measured crossover: above 1 MiB at W = 2, ~0.75 MiB at
-// W = 4; profiles/r01/k3_ll_n{2,4}.jsonl), which also sizes its buffers.
+// not.  Against the barrier two-shot it won up to ~2 MiB / (W-1) (profiles/r01/k3_ll_n{2,4}.jsonl);
+// against the LL128 two-shot (no barrier either, 1.07 N s) only up to ~1 MiB / (W-1): W = 2
+// 1 MB 10.3 vs 9.9 us, 2 MB 13.9 vs 11.2; W = 4 0.25 MB 11.8 vs 13.9, 0.5 MB 14.6 vs 14.3
+// (profiles/r01/k3_ll128os_f32_n{2,4}.jsonl).  The limit also sizes the LL buffers.
 size_t ll_max_bytes(int world) {
-  size_t m = ((size_t)2 << 20) / (size_t)(world > 1 ? world - 1 : 1);
+  size_t m = ((size_t)1 << 20) / (size_t)(world > 1 ? world - 1 : 1);
   return m / (64u << 10) * (64u << 10);
 }
 

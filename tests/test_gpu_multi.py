@@ -51,7 +51,7 @@ def results(request):
                # "oneshot": every bucket that fits the one-shot kernel uses it (larger ones, and
                # the larger pieces of case (4), fall back to two-shot: mixed sequences)
                CANNIKIN_AR_ONESHOT="1" if request.param == "oneshot" else "0",
-               # "ll": buckets <= 256 KiB through the low-latency kernel (no heap bucket needed)
+               # "ll": buckets <= 1 MiB / (W-1) through the low-latency kernel (no heap bucket needed)
                CANNIKIN_AR_LL="1" if request.param == "ll" else "0",
                # "ll128": every bucket up to 64 MiB (all but the 355M full-size case) through the
                # flag-in-line two-shot kernel
