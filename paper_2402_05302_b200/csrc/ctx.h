@@ -59,7 +59,7 @@ struct cannikin_ctx {
   int os_vpt = 2;           // CANNIKIN_OS_VPT=1|2: one-shot vectors per thread (sets its grid)
   int ar_chunk_max = 512 * 16;  // CANNIKIN_AR_CHUNK: dynamic two-shot max chunk (16-B vectors)
   int ar_ll = -1;           // CANNIKIN_AR_LL=0|1 forbids/prefers the LL kernel; -1 = by size
-  size_t ll_max_bytes = 0;  // largest LL bucket = its slot payload: 2 MiB / (W - 1), 64 KiB steps
+  size_t ll_max_bytes = 0;  // largest LL bucket = its slot payload: 1 MiB / (W - 1), 64 KiB steps
   int ar_ll128 = -1;        // CANNIKIN_AR_LL128=0|1 forbids/prefers the LL128 kernel; -1 = by size
   int ar_ll128os = -1;      // CANNIKIN_AR_LL128OS=0|1 forbids/prefers the one-shot LL128 kernel
   size_t ll128os_auto_bytes = 0;  // its automatic limit (CANNIKIN_LL128OS_AUTO_KB overrides)
