@@ -1,3 +1,4 @@
+# (historical: CANNIKIN_LL128_MODE existed only for this experiment and was removed after it)
 # LL128 experiments: store flavour / poll backoff (CANNIKIN_LL128_MODE) and a phase trace.
 export CANNIKIN_SPIN_TIMEOUT_MS=15000
 NG=$(nvidia-smi -L | wc -l)

@@ -1,3 +1,4 @@
+# (historical: CANNIKIN_LL128_FUSE existed only for this experiment and was removed after it)
 # LL128 scatter fused into the reduction loop (CANNIKIN_LL128_FUSE=1) vs separate scatter phase.
 export CANNIKIN_SPIN_TIMEOUT_MS=15000
 NG=$(nvidia-smi -L | wc -l)
