@@ -744,9 +744,13 @@ cudaError_t launch_ll128(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dty
   a.r_me = (float)r_i;
   a.rank = ctx->rank;
   a.check_r = ctx->check_ratios;
-  // about two groups per warp and phase; every rank derives the same grid from (n, W)
+  // about one group per warp and phase (profiles/r01/k3_ll128_gpw_ab_n2.jsonl: 2 MB 192 vs 177
+  // GB/s with two, 4-16 MB equal); every rank derives the same grid from (n, W)
+#ifndef CANNIKIN_LL128_GPW
+#define CANNIKIN_LL128_GPW 1
+#endif
   const size_t per_shard = (a.ngroups + W - 1) / W;
-  size_t g = (per_shard + 2 * kL8Warps - 1) / (2 * kL8Warps);
+  size_t g = (per_shard + CANNIKIN_LL128_GPW * kL8Warps - 1) / (CANNIKIN_LL128_GPW * kL8Warps);
   if (g < 1) g = 1;
   if (g > (size_t)ctx->grid_ar) g = (size_t)ctx->grid_ar;
   if (dt == CANNIKIN_F32) return dispatch_ll128<float>(W, a, (int)g, st);

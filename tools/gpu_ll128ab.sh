@@ -4,9 +4,9 @@ TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-add
 L=paper_2402_05302_b200/libcannikin.so
 cp $L /tmp/keep.so
 for k in 1 2; do
-for v in u2 u4; do
+for v in u2 u4 g4; do
 cp build/ab/$v.so $L
-CANNIKIN_SPIN_TIMEOUT_MS=15000 timeout 600 $TR --master-port 2967$k tools/k3_sweep.py --dtype f32 --variants ll128 --sizes-mb 2,4,8,16,32,64 2>/dev/null | grep '^{' | sed "s/^{/{\"build\": \"$v\", /" >> gpurun_out/ll128_ab.jsonl
+CANNIKIN_SPIN_TIMEOUT_MS=15000 timeout 600 $TR --master-port 2967$k tools/k3_sweep.py --dtype f32 --variants ll128 --sizes-mb 1,2,4,8,16 2>/dev/null | grep '^{' | sed "s/^{/{\"build\": \"$v\", /" >> gpurun_out/ll128_ab.jsonl
 done
 done
 cp /tmp/keep.so $L
