@@ -94,14 +94,36 @@ cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world, const voi
 
 /* In-process group on ONE device (test and single-GPU use of the multi-GPU kernels): creates
  * `world` contexts out[0..world-1], ranks 0..world-1, in this process, each with its own region
- * and the others' regions as its "peers" (same address space: no IPC, no NCCL).  The ranks'
- * reductions must run CONCURRENTLY (one stream per rank) and their kernels must be co-resident,
- * so `grid` is required and world * grid must not exceed the SM count (the kernels spin on their
- * peer CTAs; a violation traps after CANNIKIN_SPIN_TIMEOUT_MS instead of hanging).
+ * and the others' regions as its "peers" (same address space: no IPC, no NCCL).  `grid` is
+ * required and world * grid must not exceed the SM count (the ranks' kernels spin on their peer
+ * CTAs, so all must be resident at once).  Two ways to reduce:
+ *   - cannikin_weighted_allreduce_group (preferred): all ranks in ONE kernel launch, co-resident
+ *     by construction -- also under a profiler that serialises kernels;
+ *   - cannikin_weighted_allreduce per ctx, each rank on its own stream, issued concurrently (as
+ *     W processes would); relies on the W kernels running at the same time (a serialising
+ *     profiler breaks that: the first kernel waits for its peers until CANNIKIN_SPIN_TIMEOUT_MS).
  * cannikin_ddp_allreduce_mean is UNSUPPORTED on such contexts; each is destroyed separately.
  * Errors: INVALID (world outside 2..CANNIKIN_MAX_WORLD, grid <= 0, unknown flag), CUDA. */
 cannikin_status cannikin_init_group_local(cannikin_ctx** out, int world, int device,
                                           size_t heap_bytes, int grid, unsigned flags);
+
+/* cannikin_weighted_allreduce for ALL ranks of an in-process group in one call (Eq. 9,
+ * P:328-331; the Eq. 10 norm inputs, accumulated in every rank's ctx):
+ *   ctxs[k]    : rank k's ctx of ONE cannikin_init_group_local group, k = 0..world-1
+ *   buckets[k] : rank k's bucket (device pointer, n elements of dt, 16-byte aligned); each is
+ *                overwritten with g = sum_j r[j] buckets[j], identical bits in every bucket
+ *   r[k]       : rank k's share b_k / B (host array)
+ * The variant (LL, LL128, two-shot pull / dynamic / push) is chosen from (n, dt, world) exactly as
+ * cannikin_weighted_allreduce chooses it, and its kernel runs as ONE grid of world x G CTAs (CTA
+ * c plays rank c / G's CTA c % G), enqueued on `stream`.  The result bits and statistics are those
+ * of world separate per-rank calls.  Buckets at the same heap offset of every rank are reduced
+ * zero-copy, others staged through each rank's scratch (two copies per rank).  Errors: INVALID
+ * (NULL, misaligned, too large, ctxs not one group in rank order), UNSUPPORTED (dtype), DOMAIN
+ * (NaN share), CUDA. */
+cannikin_status cannikin_weighted_allreduce_group(cannikin_ctx* const* ctxs, int world,
+                                                  void* const* buckets, size_t n,
+                                                  cannikin_dtype dt, const double* r,
+                                                  void* stream);
 
 /* Destroy a ctx (synchronises its device first).  NULL is accepted and ignored. */
 cannikin_status cannikin_destroy(cannikin_ctx* ctx);
@@ -131,10 +153,10 @@ cannikin_status cannikin_free_bucket(cannikin_ctx* ctx, void* dptr);
  * rank picks the same): low-latency LL (<= 1 MiB / (world-1): data and flag in one 8-byte NVLink
  * store, no barrier; the bucket may then be any device memory), LL128 (above that, up to
  * 32 MiB: two-shot with the epoch flag inside every 128-byte line, no barrier, any device memory),
- * two-shot pull (static, or
- * dynamic chunks for shards >= 64 MiB), two-shot push (world >= 4, buckets >= 128 MiB: every
- * NVLink transfer a write); one-shot and dynamic push on request.  CANNIKIN_AR_* environment
- * knobs force one (CANNIKIN_AR_LL128=1: every bucket up to CANNIKIN_LL128_MAX_MB, default 64).
+ * two-shot pull (static, or dynamic chunks for shards >= 64 MiB), two-shot push (world >= 4,
+ * buckets >= 128 MiB: every NVLink transfer a write).  CANNIKIN_AR_{LL,LL128,DYN,PUSH}=0|1
+ * environment knobs force or forbid one (CANNIKIN_AR_LL128=1: every bucket up to
+ * CANNIKIN_LL128_MAX_MB, default 32).
  * The result bits do not depend on the variant; the statistics' summation grouping does.
  * world == 1: g = r_0 g_0 in place.
  * Errors: INVALID (NULL, misaligned, too large), UNSUPPORTED (dtype), CUDA. */
@@ -212,7 +234,7 @@ cannikin_status cannikin_weighted_sum_local(cannikin_ctx* ctx, const void* const
                                             void* stream);
 
 /* Baseline for the step-time comparison: equal-split DDP semantics (Eq. 2) -- an NCCL
- * sum all-reduce of the bucket followed by a division by world (scale kernel).  In place. */
+ * all-reduce of the bucket with ncclAvg (sum, then division by world, inside NCCL).  In place. */
 cannikin_status cannikin_ddp_allreduce_mean(cannikin_ctx* ctx, void* bucket, size_t n,
                                             cannikin_dtype dt, void* stream);
 
@@ -229,7 +251,9 @@ cannikin_status cannikin_emulate_compute(double seconds, void* stream);
  * Errors: INVALID, CUDA. */
 cannikin_status cannikin_trace(cannikin_ctx* ctx, uint64_t* out, int max_ctas, int* n_ctas);
 
-/* Number of CUDA kernels the last hot-path call on this ctx enqueued (for launch accounting). */
+/* Number of device operations (kernels and copies) the last hot-path call on this ctx enqueued,
+ * for launch accounting: 1 for a zero-copy or LL/LL128 reduction, 3 for a staged one (copy in,
+ * kernel, copy out); for cannikin_weighted_allreduce_group it is recorded on ctxs[0]. */
 int cannikin_last_launch_count(cannikin_ctx* ctx);
 
 /* ------------------------------------------------------------------------------------------

@@ -7,6 +7,7 @@ Entry points mirror include/cannikin.h:
     Context(...)                      cannikin_init / cannikin_destroy
     Context.alloc_bucket / free_bucket
     Context.weighted_allreduce        Eq. 9 + fused |g_i|^2, |g|^2
+    weighted_allreduce_group          the same for every rank of an in-process group, one launch
     Context.weighted_allreduce_nccl   the same through NCCL reduce-scatter / all-gather (K4)
     Context.gns_stats                 finalise the norm statistics
     Context.weighted_sum_local        emulated ranks on one GPU
@@ -23,6 +24,7 @@ import os
 __all__ = [
     "CannikinError", "Context", "F32", "BF16", "ACCUMULATE", "ROUND_PAPER", "lib", "lib_path",
     "get_unique_id", "gns_estimate", "opt_split", "node_time", "warmup_split", "MAX_WORLD",
+    "weighted_allreduce_group",
     "MAX_EMULATED",
 ]
 
@@ -91,6 +93,8 @@ SIGNATURES = {
     "cannikin_alloc_bucket": (_I, [_P, _Z, ctypes.POINTER(_P)]),
     "cannikin_free_bucket": (_I, [_P, _P]),
     "cannikin_weighted_allreduce": (_I, [_P, _P, _Z, _I, _D, _P]),
+    "cannikin_weighted_allreduce_group": (_I, [ctypes.POINTER(_P), _I, ctypes.POINTER(_P), _Z, _I,
+                                               _DP, _P]),
     "cannikin_weighted_allreduce_nvls": (_I, [_P, _P, _P, _Z, _I, _D, _P]),
     "cannikin_weighted_allreduce_nccl": (_I, [_P, _P, _Z, _I, _D, _P]),
     "cannikin_gns_stats": (_I, [_P, _P, _DP, _DP]),
@@ -268,6 +272,15 @@ class Context:
 
     def last_launch_count(self) -> int:
         return int(lib().cannikin_last_launch_count(self._h))
+
+
+def weighted_allreduce_group(ctxs, ptrs, n: int, dtype: int, r, stream=None):
+    """cannikin_weighted_allreduce_group: every rank of an in-process group (Context.group_local,
+    in rank order) reduced by ONE kernel launch on `stream`."""
+    w = len(ctxs)
+    hs = (_P * w)(*[c._h.value for c in ctxs])
+    ps = (_P * w)(*ptrs)
+    _check(lib().cannikin_weighted_allreduce_group(hs, w, ps, n, dtype, _dbl(r), _stream(stream)))
 
 
 def emulate_compute(seconds: float, stream=None):

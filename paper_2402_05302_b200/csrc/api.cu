@@ -88,15 +88,11 @@ static cannikin_status create_local(cannikin_ctx** out, int rank, int world, int
   ctx->scratch_off = ctx->user_off + ctx->heap_bytes;
   ctx->total_bytes = ctx->scratch_off + (world > 1 ? ctx->heap_bytes : 0);
   if (const char* t = std::getenv("CANNIKIN_AR_CHUNK")) ctx->ar_chunk_max = std::max(512, std::atoi(t));
-  if (const char* t = std::getenv("CANNIKIN_OS_VPT")) ctx->os_vpt = std::atoi(t) >= 2 ? 2 : 1;
-  if (const char* t = std::getenv("CANNIKIN_AR_ONESHOT")) ctx->ar_oneshot = std::atoi(t) != 0;
-  if (const char* t = std::getenv("CANNIKIN_AR_PUSH")) {
-    const int v = std::atoi(t);
-    ctx->ar_push = v <= 0 ? 0 : (v == 1 ? 1 : 2);
-  }
-  if (const char* t = std::getenv("CANNIKIN_PD_CHUNK_KB")) ctx->pd_chunk_kb = std::max(16, std::atoi(t));
-  // staging for the push variant (W slots of the largest shard): by default from 4 ranks up
-  if (world > 1 && (ctx->ar_push >= 1 || (ctx->ar_push < 0 && world >= 4))) {
+  if (const char* t = std::getenv("CANNIKIN_AR_PUSH")) ctx->ar_push = std::atoi(t) > 0 ? 1 : 0;
+  // staging for the push variant (W slots of the largest shard): only where push can be chosen --
+  // forced, or automatically (W >= 4, buckets >= 128 MiB, so the heap must hold one)
+  if (world > 1 && (ctx->ar_push == 1 ||
+                    (ctx->ar_push < 0 && world >= 4 && ctx->heap_bytes >= cannikin::kPushAutoBytes))) {
     ctx->stage_off = ctx->total_bytes;
     ctx->total_bytes += align_up(ctx->heap_bytes + (size_t)world * world * 64 * 16 + 4096, 4096);
   }
@@ -108,16 +104,15 @@ static cannikin_status create_local(cannikin_ctx** out, int rank, int world, int
     ctx->total_bytes += align_up(cannikin::ll_region_bytes(world), 4096);
   }
   // LL128 buffers (flag-in-line two-shot for mid-size buckets): 2 parities x {scatter, gather} x
-  // W source slots of the largest shard, plus headers; zeroed (flags start at epoch 0)
+  // W source slots of the largest shard, plus headers; zeroed (flags start at epoch 0).  Sized for
+  // the automatic range (ll128_auto_bytes) unless CANNIKIN_LL128_MAX_MB asks for more (e.g. with
+  // CANNIKIN_AR_LL128=1, which sends every bucket up to that size through LL128).
   if (const char* t = std::getenv("CANNIKIN_AR_LL128")) ctx->ar_ll128 = std::atoi(t) != 0 ? 1 : 0;
-  if (const char* t = std::getenv("CANNIKIN_AR_LL128OS")) ctx->ar_ll128os = std::atoi(t) != 0 ? 1 : 0;
-  if (world > 1 && (ctx->ar_ll128 != 0 || ctx->ar_ll128os != 0)) {
-    size_t mb = 64;
-    if (const char* t = std::getenv("CANNIKIN_LL128_MAX_MB")) mb = (size_t)std::max(1, std::atoi(t));
-    ctx->ll128_max_bytes = mb << 20;
-    ctx->ll128os_auto_bytes = cannikin::ll128os_auto_bytes(world);
-    if (const char* t = std::getenv("CANNIKIN_LL128OS_AUTO_KB"))
-      ctx->ll128os_auto_bytes = (size_t)std::max(0, std::atoi(t)) << 10;
+  if (world > 1 && ctx->ar_ll128 != 0) {
+    size_t max_bytes = cannikin::ll128_auto_bytes(world);
+    if (const char* t = std::getenv("CANNIKIN_LL128_MAX_MB"))
+      max_bytes = (size_t)std::max(1, std::atoi(t)) << 20;
+    ctx->ll128_max_bytes = max_bytes;
     ctx->ll128_off = ctx->total_bytes;
     ctx->total_bytes += align_up(cannikin::ll128_region_bytes(world, ctx->ll128_max_bytes), 4096);
   }
@@ -303,12 +298,6 @@ extern "C" cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* 
     ctx->last_launches = 1;
     return CANNIKIN_OK;
   }
-  if (cannikin::ll128os_eligible(ctx, bytes)) {
-    // one-shot LL128: the whole bucket to every peer, every rank reduces it by itself
-    CK_CUDA(cannikin::launch_ll128os(ctx, bucket, n, dt, r_i, S(stream)));
-    ctx->last_launches = 1;
-    return CANNIKIN_OK;
-  }
   if (cannikin::ll128_eligible(ctx, bytes)) {
     // mid-size bucket: flag-in-line two-shot, no barrier; touches only this rank's bucket
     CK_CUDA(cannikin::launch_ll128(ctx, bucket, n, dt, r_i, S(stream)));
@@ -336,7 +325,76 @@ extern "C" cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* 
   CK_CUDA(cudaMemcpyAsync(scratch, bucket, bytes, cudaMemcpyDeviceToDevice, S(stream)));
   CK_CUDA(cannikin::launch_twoshot(ctx, ctx->scratch_off, n, dt, r_i, S(stream)));
   CK_CUDA(cudaMemcpyAsync(bucket, scratch, bytes, cudaMemcpyDeviceToDevice, S(stream)));
-  ctx->last_launches = 1;
+  ctx->last_launches = 3;  // copy in, kernel, copy out
+  return CANNIKIN_OK;
+}
+
+extern "C" cannikin_status cannikin_weighted_allreduce_group(cannikin_ctx* const* ctxs, int world,
+                                                             void* const* buckets, size_t n,
+                                                             cannikin_dtype dt, const double* r,
+                                                             void* stream) {
+  if (!ctxs || !buckets || !r) return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_group: NULL argument");
+  if (world < 2 || world > CANNIKIN_MAX_WORLD)
+    return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_group: world=%d", world);
+  for (int k = 0; k < world; ++k) {
+    const cannikin_ctx* c = ctxs[k];
+    if (!c || !c->in_process || c->rank != k || c->world != world || c->device != ctxs[0]->device ||
+        c->grid_ar != ctxs[0]->grid_ar)
+      return fail(CANNIKIN_ERR_INVALID,
+                  "weighted_allreduce_group: ctxs[%d] is not rank %d of one in-process group", k, k);
+    for (int j = 0; j < world; ++j)
+      if (c->peer_base[j] != ctxs[j]->base)
+        return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_group: ctxs are not one group");
+    ctxs[k]->last_launches = 0;
+  }
+  if (dt != CANNIKIN_F32 && dt != CANNIKIN_BF16)
+    return fail(CANNIKIN_ERR_UNSUPPORTED, "weighted_allreduce_group: dtype %d", (int)dt);
+  if (n == 0) return CANNIKIN_OK;
+  for (int k = 0; k < world; ++k) {
+    if (!buckets[k]) return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_group: buckets[%d] == NULL", k);
+    if (reinterpret_cast<uintptr_t>(buckets[k]) % 16)
+      return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_group: buckets[%d] not 16-byte aligned", k);
+    if (!(r[k] == r[k])) return fail(CANNIKIN_ERR_DOMAIN, "weighted_allreduce_group: r[%d] is NaN", k);
+  }
+  cannikin_ctx* c0 = ctxs[0];
+  const size_t bytes = n * elem_size(dt);
+  CK_CUDA(cudaSetDevice(c0->device));
+  if (cannikin::ll128_eligible(c0, bytes)) {
+    CK_CUDA(cannikin::launch_ll128_group(ctxs, world, buckets, n, dt, r, S(stream)));
+    ctxs[0]->last_launches = 1;
+    return CANNIKIN_OK;
+  }
+  if (cannikin::ll_eligible(c0, bytes)) {
+    CK_CUDA(cannikin::launch_ll_group(ctxs, world, buckets, n, dt, r, S(stream)));
+    ctxs[0]->last_launches = 1;
+    return CANNIKIN_OK;
+  }
+  if (bytes > c0->heap_bytes)
+    return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_group: %zu bytes > heap %zu", bytes,
+                c0->heap_bytes);
+  // zero-copy when every bucket sits at the same offset of its rank's heap
+  bool same = true;
+  size_t off = 0;
+  for (int k = 0; k < world && same; ++k) {
+    const char* p = static_cast<const char*>(buckets[k]);
+    const char* lo = ctxs[k]->base + ctxs[k]->user_off;
+    if (p < lo || p + bytes > lo + ctxs[k]->heap_bytes) same = false;
+    else if (k == 0) off = p - ctxs[k]->base;
+    else if ((size_t)(p - ctxs[k]->base) != off) same = false;
+  }
+  if (same) {
+    CK_CUDA(cannikin::launch_twoshot_group(ctxs, world, off, n, dt, r, S(stream)));
+    ctxs[0]->last_launches = 1;
+    return CANNIKIN_OK;
+  }
+  for (int k = 0; k < world; ++k)
+    CK_CUDA(cudaMemcpyAsync(ctxs[k]->base + ctxs[k]->scratch_off, buckets[k], bytes,
+                            cudaMemcpyDeviceToDevice, S(stream)));
+  CK_CUDA(cannikin::launch_twoshot_group(ctxs, world, c0->scratch_off, n, dt, r, S(stream)));
+  for (int k = 0; k < world; ++k)
+    CK_CUDA(cudaMemcpyAsync(buckets[k], ctxs[k]->base + ctxs[k]->scratch_off, bytes,
+                            cudaMemcpyDeviceToDevice, S(stream)));
+  ctxs[0]->last_launches = 1 + 2 * world;
   return CANNIKIN_OK;
 }
 

@@ -12,6 +12,7 @@ namespace cannikin {
 
 constexpr int kMaxWorld = CANNIKIN_MAX_WORLD;
 constexpr int kMaxArBlocks = 256;      // grid cap of the two-shot kernel
+constexpr size_t kPushAutoBytes = (size_t)128 << 20;  // push two-shot from this bucket size (W >= 4)
 constexpr int kMaxArChunks = 2048;     // partial-table rows per source rank (dynamic two-shot)
 constexpr int kMaxLocalBlocks = 2048;  // grid cap of the emulated-rank kernel
 constexpr int kMaxEmu = CANNIKIN_MAX_EMULATED;
@@ -27,8 +28,6 @@ struct Ctrl {
   uint64_t rv_word[kMaxArBlocks][kMaxWorld];                 // [peer] entry: (float r_src, epoch32)
   uint64_t meta_word[kMaxArBlocks][kMaxWorld];               // [peer] entry: (bucket hash32, epoch32)
   uint64_t pmid[kMaxArBlocks][kMaxWorld];                    // [peer] push variant: (r_src, epoch32)
-  uint64_t sflag[kMaxWorld][kMaxArChunks];                   // [peer] dynamic push: chunk landed
-  uint64_t pd_epoch;                                         // [local] dynamic-push call counter
   uint64_t ll_epoch;                                         // [local] LL-kernel call counter
   unsigned ticket_ll;                                        // [local] LL last-CTA ticket
   uint64_t ll128_epoch;                                      // [local] LL128-kernel call counter
@@ -53,18 +52,13 @@ struct cannikin_ctx {
   int rank = 0, world = 1, device = 0;
   int grid_ar = 148;
   int ar_dyn = -1;          // CANNIKIN_AR_DYN=0|1 forces static/dynamic chunks; -1 = by size
-  int ar_push = -1;         // CANNIKIN_AR_PUSH=0|1|2 forces pull / static push / dynamic push
-  int pd_chunk_kb = 256;    // CANNIKIN_PD_CHUNK_KB: dynamic-push chunk (grown to fit the row table)
+  int ar_push = -1;         // CANNIKIN_AR_PUSH=0|1 forces pull / push; -1 = by size
   int check_ratios = 0;     // CANNIKIN_INIT_CHECK_RATIOS
-  int os_vpt = 2;           // CANNIKIN_OS_VPT=1|2: one-shot vectors per thread (sets its grid)
   int ar_chunk_max = 512 * 16;  // CANNIKIN_AR_CHUNK: dynamic two-shot max chunk (16-B vectors)
   int ar_ll = -1;           // CANNIKIN_AR_LL=0|1 forbids/prefers the LL kernel; -1 = by size
   size_t ll_max_bytes = 0;  // largest LL bucket = its slot payload: 1 MiB / (W - 1), 64 KiB steps
   int ar_ll128 = -1;        // CANNIKIN_AR_LL128=0|1 forbids/prefers the LL128 kernel; -1 = by size
-  int ar_ll128os = -1;      // CANNIKIN_AR_LL128OS=0|1 forbids/prefers the one-shot LL128 kernel
-  size_t ll128os_auto_bytes = 0;  // its automatic limit (CANNIKIN_LL128OS_AUTO_KB overrides)
   size_t ll128_max_bytes = 0;  // largest LL128 bucket (CANNIKIN_LL128_MAX_MB), sizes its slots
-  int ar_oneshot = -1;      // CANNIKIN_AR_ONESHOT=0|1 forbids/prefers one-shot; -1 = by size
   int grid_local = 0;       // 0 = occupancy-derived grid for the LDG variant of K2
   bool local_tma = false;   // default variant of K2 (CANNIKIN_K2_IMPL=tma|ldg)
   int local_nt = 256;       // CANNIKIN_K2_NT: CTA size of K2 (256, or one big CTA per SM)

@@ -207,4 +207,20 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 
 }  // namespace dev
+
+// Two entry points for one kernel body BODY<TARGS>(args, cta, grid): KERNEL, the per-rank launch
+// (one grid per rank), and GKERNEL, the in-process group launch over GroupArgs<ARGS> (kernels.h):
+// world x grid CTAs in ONE grid, CTA c running BODY for rank c / grid as its CTA c % grid.
+#define CANNIKIN_UNPAREN(...) __VA_ARGS__
+#define CANNIKIN_GROUP_ENTRY(TPARAMS, TARGS, BOUNDS, KERNEL, GKERNEL, BODY, ARGS)      \
+  template <CANNIKIN_UNPAREN TPARAMS>                                                 \
+  __global__ void __launch_bounds__ BOUNDS KERNEL(const ARGS a) {                     \
+    BODY<CANNIKIN_UNPAREN TARGS>(a, blockIdx.x, gridDim.x);                           \
+  }                                                                                   \
+  template <CANNIKIN_UNPAREN TPARAMS>                                                 \
+  __global__ void __launch_bounds__ BOUNDS GKERNEL(const GroupArgs<ARGS> g) {         \
+    const int rk = blockIdx.x / g.grid;                                               \
+    BODY<CANNIKIN_UNPAREN TARGS>(g.a[rk], blockIdx.x - rk * g.grid, g.grid);          \
+  }
+
 }  // namespace cannikin

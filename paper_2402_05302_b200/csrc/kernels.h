@@ -7,6 +7,15 @@
 
 namespace cannikin {
 
+// Arguments of a single-launch in-process group (cannikin_weighted_allreduce_group): the per-rank
+// arguments of every rank, one grid of world x grid CTAs; CTA c serves rank c / grid as its CTA
+// c % grid, so the ranks' CTAs are co-resident by construction (one kernel).
+template <typename A>
+struct GroupArgs {
+  A a[kMaxWorld];
+  int grid;
+};
+
 // Arguments of the emulated-rank kernels (K2, both variants).
 struct LocalArgs {
   const char* in[kMaxEmu];
@@ -34,10 +43,15 @@ cudaError_t launch_wsum_local_tma(cannikin_ctx* ctx, const void* const* in, int 
 cudaError_t launch_emulate(double seconds, cudaStream_t st);
 cudaError_t launch_nvls(cannikin_ctx* ctx, void* local, void* mc, size_t n, cannikin_dtype dt,
                         double r_i, cudaStream_t st);
-cudaError_t launch_twoshot_push(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt,
-                                double r_i, cudaStream_t st);
 cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
                            cudaStream_t st);
+// in-process group (cannikin_weighted_allreduce_group): all W ranks' kernels in ONE launch
+cudaError_t launch_twoshot_group(cannikin_ctx* const* ctxs, int W, size_t off, size_t n,
+                                 cannikin_dtype dt, const double* r, cudaStream_t st);
+cudaError_t launch_ll_group(cannikin_ctx* const* ctxs, int W, void* const* buckets, size_t n,
+                            cannikin_dtype dt, const double* r, cudaStream_t st);
+cudaError_t launch_ll128_group(cannikin_ctx* const* ctxs, int W, void* const* buckets, size_t n,
+                               cannikin_dtype dt, const double* r, cudaStream_t st);
 cudaError_t launch_stats_finalize(cannikin_ctx* ctx, double* out, cudaStream_t st);
 size_t ll_max_bytes(int world);
 size_t ll_region_bytes(int world);
@@ -45,13 +59,10 @@ bool ll_eligible(const cannikin_ctx* ctx, size_t bytes);
 cudaError_t launch_ll(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt, double r_i,
                       cudaStream_t st);
 size_t ll128_region_bytes(int world, size_t max_bytes);
+size_t ll128_auto_bytes(int world);
 bool ll128_eligible(const cannikin_ctx* ctx, size_t bytes);
 cudaError_t launch_ll128(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt, double r_i,
                          cudaStream_t st);
-size_t ll128os_auto_bytes(int world);
-bool ll128os_eligible(const cannikin_ctx* ctx, size_t bytes);
-cudaError_t launch_ll128os(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt,
-                           double r_i, cudaStream_t st);
 size_t k4_buffer_bytes(int world, size_t n);
 cannikin_status launch_k4(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt, double r_i,
                           cudaStream_t st);

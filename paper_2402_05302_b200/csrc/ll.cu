@@ -98,13 +98,13 @@ struct Word<__nv_bfloat16> {
 };
 
 template <typename T, int W>
-__global__ void __launch_bounds__(kLLThreads, 1) ll_kernel(const LLArgs a) {
+__device__ __forceinline__ void ll_body(const LLArgs& a, const int b, const int G) {
   using Wd = Word<T>;
   constexpr int E = Wd::E;
   __shared__ double red[32 * (W + 1)];
   __shared__ float s_r[W];
   __shared__ uint32_t s_e;
-  const int b = blockIdx.x, tid = threadIdx.x, me = a.rank;
+  const int tid = threadIdx.x, me = a.rank;
   if (tid == 0) {
     s_e = (uint32_t)(__ldcg(&a.ctrl->ll_epoch) + 1);
     a.ctrl->trace[b][0] = dev::globaltimer_ns();
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_kernel(const LLArgs a) {
   // slot (parity, source s) in rank k's region
   auto slot = [&](int k, int s) -> char* { return a.ll[k] + (par * W + s) * a.slot_bytes; };
   const bool half_tail = sizeof(T) == 2 && (a.n & 1);  // last word holds one bf16
-  const size_t stride = (size_t)gridDim.x * kLLThreads;
+  const size_t stride = (size_t)G * kLLThreads;
 
   // per-thread slot pointers, resolved once (the loops below index them statically)
   char* dstp[W];        // dstp[jj]: my slot in rank (me + jj) % W's region, jj = 1..W-1
@@ -217,20 +217,31 @@ __global__ void __launch_bounds__(kLLThreads, 1) ll_kernel(const LLArgs a) {
     for (int j = 0; j <= W; ++j) acc[j] = __ldcg(&acc[j]) + vals[j];
     a.ctrl->trace[b][2] = a.ctrl->trace[b][3] = a.ctrl->trace[b][4] = dev::globaltimer_ns();
     __threadfence();
-    if (atomicAdd(&a.ctrl->ticket_ll, 1u) == gridDim.x - 1) {
+    if (atomicAdd(&a.ctrl->ticket_ll, 1u) == G - 1) {
       a.ctrl->ticket_ll = 0u;
       a.ctrl->ll_epoch = a.ctrl->ll_epoch + 1;
-      a.ctrl->trace_grid = gridDim.x;
+      a.ctrl->trace_grid = G;
     }
   }
 }
 
+CANNIKIN_GROUP_ENTRY((typename T, int W), (T, W), (kLLThreads, 1), ll_kernel, ll_group_kernel,
+                     ll_body, LLArgs)
+
+// a[0] (single launch) or a[0..W-1] (in-process group: one launch of W x grid CTAs)
 template <typename T>
-static cudaError_t dispatch_ll(int W, const LLArgs& a, int grid, cudaStream_t st) {
+static cudaError_t dispatch_ll(int W, const LLArgs* a, int grid, bool group, cudaStream_t st) {
   switch (W) {
-#define CANNIKIN_CASE(K) \
-  case K:                \
-    ll_kernel<T, K><<<grid, kLLThreads, 0, st>>>(a); \
+#define CANNIKIN_CASE(K)                                                     \
+  case K:                                                                    \
+    if (group) {                                                             \
+      GroupArgs<LLArgs> g{};                                                 \
+      for (int k = 0; k < K; ++k) g.a[k] = a[k];                             \
+      g.grid = grid;                                                         \
+      ll_group_kernel<T, K><<<K * grid, kLLThreads, 0, st>>>(g);             \
+    } else {                                                                 \
+      ll_kernel<T, K><<<grid, kLLThreads, 0, st>>>(a[0]);                    \
+    }                                                                        \
     return cudaGetLastError();
     CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5) CANNIKIN_CASE(6)
     CANNIKIN_CASE(7) CANNIKIN_CASE(8)
@@ -244,7 +255,8 @@ static cudaError_t dispatch_ll(int W, const LLArgs& a, int grid, cudaStream_t st
 // not.  Against the barrier two-shot it won up to ~2 MiB / (W-1) (profiles/r01/k3_ll_n{2,4}.jsonl);
 // against the LL128 two-shot (no barrier either, 1.07 N s) only up to ~1 MiB / (W-1): W = 2
 // 1 MB 10.3 vs 9.9 us, 2 MB 13.9 vs 11.2; W = 4 0.25 MB 11.8 vs 13.9, 0.5 MB 14.6 vs 14.3
-// (profiles/r01/k3_ll128os_f32_n{2,4}.jsonl).  The limit also sizes the LL buffers.
+// (profiles/r01/k3_ll128os_f32_n{2,4}.jsonl, measured alongside the since-removed one-shot LL128
+// variant).  The limit also sizes the LL buffers.
 size_t ll_max_bytes(int world) {
   size_t m = ((size_t)1 << 20) / (size_t)(world > 1 ? world - 1 : 1);
   return m / (64u << 10) * (64u << 10);
@@ -259,10 +271,11 @@ bool ll_eligible(const cannikin_ctx* ctx, size_t bytes) {
   return bytes <= ctx->ll_max_bytes;
 }
 
-cudaError_t launch_ll(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt, double r_i,
-                      cudaStream_t st) {
+static int plan_ll(const cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt, double r_i,
+                   LLArgs* out) {
   const int W = ctx->world;
-  LLArgs a{};
+  LLArgs& a = *out;
+  a = LLArgs{};
   a.bucket = static_cast<char*>(bucket);
   for (int j = 0; j < W; ++j) a.ll[j] = ctx->peer_base[j] + ctx->ll_off;
   a.ctrl = ctx->ctrl;
@@ -277,8 +290,24 @@ cudaError_t launch_ll(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype 
   size_t g = (a.nwords + kLLThreads - 1) / kLLThreads;
   if (g < 1) g = 1;
   if (g > (size_t)ctx->grid_ar) g = (size_t)ctx->grid_ar;
-  if (dt == CANNIKIN_F32) return dispatch_ll<float>(W, a, (int)g, st);
-  return dispatch_ll<__nv_bfloat16>(W, a, (int)g, st);
+  return (int)g;
+}
+
+cudaError_t launch_ll(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt, double r_i,
+                      cudaStream_t st) {
+  LLArgs a;
+  const int g = plan_ll(ctx, bucket, n, dt, r_i, &a);
+  if (dt == CANNIKIN_F32) return dispatch_ll<float>(ctx->world, &a, g, false, st);
+  return dispatch_ll<__nv_bfloat16>(ctx->world, &a, g, false, st);
+}
+
+cudaError_t launch_ll_group(cannikin_ctx* const* ctxs, int W, void* const* buckets, size_t n,
+                            cannikin_dtype dt, const double* r, cudaStream_t st) {
+  LLArgs a[kMaxWorld];
+  int g = 0;
+  for (int k = 0; k < W; ++k) g = plan_ll(ctxs[k], buckets[k], n, dt, r[k], &a[k]);
+  if (dt == CANNIKIN_F32) return dispatch_ll<float>(W, a, g, true, st);
+  return dispatch_ll<__nv_bfloat16>(W, a, g, true, st);
 }
 
 }  // namespace cannikin

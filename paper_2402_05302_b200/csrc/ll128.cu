@@ -170,7 +170,7 @@ __device__ __forceinline__ void store_payload(char* bucket, size_t bytes, size_t
 }
 
 template <typename T, int W>
-__global__ void __launch_bounds__(kL8Threads, 1) ll128_kernel(const LL128Args a) {
+__device__ __forceinline__ void ll128_body(const LL128Args& a, const int b, const int G) {
   using V = dev::Vec<T>;
   constexpr int E = V::E;
   constexpr int NS = 2 * (W + 1);  // statistics words per row
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kL8Threads, 1) ll128_kernel(const LL128Args a)
   __shared__ uint64_t s_e;
   __shared__ char* s_reg[W];  // peer regions (indexed by runtime rank: shared, not param space)
   __shared__ size_t s_h0[W], s_h1[W], s_lo[W];  // CTA b's piece of every shard, shard starts
-  const int b = blockIdx.x, tid = threadIdx.x, me = a.rank, G = gridDim.x;
+  const int tid = threadIdx.x, me = a.rank;
   const int lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
     s_e = __ldcg(&a.ctrl->ll128_epoch) + 1;
@@ -457,199 +457,24 @@ __global__ void __launch_bounds__(kL8Threads, 1) ll128_kernel(const LL128Args a)
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// One-shot LL128 (world 2, and small buckets at any world): every rank sends its WHOLE bucket in
-// LL128 groups into its slot of every peer's region, and every rank reduces the whole bucket by
-// itself from its own copy and the W-1 received ones (rank order, fp32 fmaf, one rounding -- the
-// same bits as every variant).  One NVLink hop instead of two and no statistics exchange: every
-// rank computes every CTA's statistics row from the same data in the same order, so the rows are
-// identical without being sent.  NVLink bytes per direction (W-1) N s x 512/480: at W = 2 the
-// same as the two-shot's, which it therefore dominates; above, only for small buckets.
-// It shares the LL128 region (and its epoch and parity sequence) with the two-shot kernel: slot
-// (parity p, source s) = data bytes [(p W + s) S, (p W + s + 1) S) -- parity p covers the same
-// bytes in both layouts, so the reuse argument holds for any mix of the two.
-template <typename T, int W>
-__global__ void __launch_bounds__(kL8Threads, 1) ll128os_kernel(const LL128Args a) {
-  using V = dev::Vec<T>;
-  constexpr int E = V::E;
-  __shared__ double red[32 * (W + 1)];
-  __shared__ float s_r[W];
-  __shared__ uint64_t s_e;
-  __shared__ char* s_reg[W];
-  const int b = blockIdx.x, tid = threadIdx.x, me = a.rank, G = gridDim.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    s_e = __ldcg(&a.ctrl->ll128_epoch) + 1;
-    a.ctrl->trace[b][0] = dev::globaltimer_ns();
-  }
-#pragma unroll
-  for (int j = 0; j < W; ++j)
-    if (tid == j) s_reg[j] = a.reg[j];
-  __syncthreads();
-  const uint64_t e = s_e;
-  const uint32_t e32 = (uint32_t)e;
-  const size_t par = e & 1u;
-  const bool fl = (lane & 7) == 7;
-  const size_t poff = fl ? 448 + 8 * (lane >> 3) : 16 * ((lane >> 3) * 7 + (lane & 7));
-  const int pb = fl ? 8 : 16;
-  auto slot = [&](int k, int src) -> char* {
-    return s_reg[k] + kL8HeaderBytes + (par * W + src) * a.slot_bytes + (size_t)lane * 16;
-  };
-  auto hdr = [&](int k, int src) -> char* {
-    return s_reg[k] + (((par * kMaxWorld + src) * kMaxArBlocks) + b) * (size_t)(kHdrWords * 8);
-  };
-  const size_t g0 = a.ngroups * (size_t)b / G, g1 = a.ngroups * (size_t)(b + 1) / G;
-  const long Tn = g0 + warp < g1 ? (long)((g1 - g0 - warp + kL8Warps - 1) / kL8Warps) : 0;
-  constexpr int kU = W <= 4 ? 2 : 1;
-  auto grp = [&](long t) -> size_t { return g0 + warp + (size_t)t * kL8Warps; };
+CANNIKIN_GROUP_ENTRY((typename T, int W), (T, W), (kL8Threads, 1), ll128_kernel, ll128_group_kernel,
+                     ll128_body, LL128Args)
 
-  // ---- send: every group of CTA b's piece to every peer, kLagS steps ahead of the reduction
-  long ns = 0;
-  auto send_to = [&](long tend) {
-    while (ns < tend) {
-      const int nu = (ns + kU <= tend) ? kU : 1;
-      uint4 v[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u)
-        if (u < nu) v[u] = load_payload(a.bucket, a.bytes, grp(ns + u) * kGroupPayload + poff, pb);
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        if (u >= nu) continue;
-        if (fl) {
-          v[u].z = e32;
-          v[u].w = (uint32_t)(e >> 32);
-        }
-#pragma unroll
-        for (int jj = 1; jj < W; ++jj)
-          st_vol16(slot((me + jj) % W, me) + grp(ns + u) * kGroupWire, v[u]);
-      }
-      ns += nu;
-    }
-  };
-  constexpr long kLagS = 2 * kU;
-  if (tid < W && tid != me)
-    st_word(hdr(tid, me), ((uint64_t)e32 << 32) | __float_as_uint(a.r_me));
-  send_to(kLagS < Tn ? kLagS : Tn);
-  if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
-  if (tid < W) {
-    if (tid == me) {
-      s_r[tid] = a.r_me;
-    } else {
-      const uint64_t h = wait_word(hdr(me, tid), e32, a.ctrl, a.timeout_ns);
-      s_r[tid] = __uint_as_float((uint32_t)h);
-    }
-  }
-  __syncthreads();
-  if (a.check_r && b == 0 && tid == 0) {
-    double sr = 0.0;
-#pragma unroll
-    for (int j = 0; j < W; ++j) sr += (double)s_r[j];
-    if (fabs(sr - 1.0) > 0x1p-23) {
-      a.ctrl->rsum_bad = sr;
-      atomicCAS(&a.ctrl->error_code, 0, 7);
-    }
-  }
-  float r[W];
-#pragma unroll
-  for (int j = 0; j < W; ++j) r[j] = s_r[j];
-
-  // ---- reduce every group of the piece from the W copies; the result stays local
-  double lsq[W];
-#pragma unroll
-  for (int j = 0; j < W; ++j) lsq[j] = 0.0;
-  double gsq = 0.0;
-  auto step = [&](long t, auto uc) {
-    constexpr int U = decltype(uc)::value;
-    uint4 x[U][W];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int j = 0; j < W; ++j)
-        x[u][j] = j != me ? ld_vol16(slot(me, j) + grp(t + u) * kGroupWire)
-                          : load_payload(a.bucket, a.bytes, grp(t + u) * kGroupPayload + poff, pb);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-#pragma unroll
-      for (int j = 0; j < W; ++j) {
-        if (j == me) continue;
-        x[u][j] = wait_group(slot(me, j) + grp(t + u) * kGroupWire, x[u][j], fl, e, a.ctrl,
-                             a.timeout_ns);
-        if (fl) x[u][j].z = x[u][j].w = 0u;
-      }
-      float acc[E];
-#pragma unroll
-      for (int q = 0; q < E; ++q) acc[q] = 0.0f;
-#pragma unroll
-      for (int j = 0; j < W; ++j) {
-        float f[E];
-        V::unpack(x[u][j], f);
-        float sq = 0.0f;
-#pragma unroll
-        for (int q = 0; q < E; ++q) {
-          acc[q] = fmaf(r[j], f[q], acc[q]);
-          sq = fmaf(f[q], f[q], sq);
-        }
-        lsq[j] += (double)sq;
-      }
-      float sg = 0.0f;
-#pragma unroll
-      for (int q = 0; q < E; ++q) sg = fmaf(acc[q], acc[q], sg);
-      gsq += (double)sg;
-      store_payload(a.bucket, a.bytes, grp(t + u) * kGroupPayload + poff, pb, V::pack(acc));
-    }
-  };
-  long t = 0;
-  for (; t + kU <= Tn; t += kU) {
-    send_to(t + kU + kLagS < Tn ? t + kU + kLagS : Tn);
-    step(t, std::integral_constant<int, kU>{});
-  }
-  for (; t < Tn; ++t) {
-    send_to(Tn);
-    step(t, std::integral_constant<int, 1>{});
-  }
-  if (tid == 0) a.ctrl->trace[b][2] = a.ctrl->trace[b][3] = dev::globaltimer_ns();
-
-  // ---- statistics: CTA b's row, identical on every rank without an exchange
-  double vals[W + 1];
-#pragma unroll
-  for (int j = 0; j < W; ++j) vals[j] = lsq[j];
-  vals[W] = gsq;
-  dev::block_sum(vals, red);
-  if (tid == 0) {
-    double* acc = a.ctrl->cta_acc[b];
-#pragma unroll
-    for (int j = 0; j <= W; ++j) acc[j] = __ldcg(&acc[j]) + vals[j];
-    a.ctrl->trace[b][4] = dev::globaltimer_ns();
-    __threadfence();
-    if (atomicAdd(&a.ctrl->ticket_ll128, 1u) == (unsigned)G - 1) {
-      a.ctrl->ticket_ll128 = 0u;
-      a.ctrl->ll128_epoch = a.ctrl->ll128_epoch + 1;
-      a.ctrl->trace_grid = G;
-    }
-  }
-}
-
+// a[0] (single launch) or a[0..W-1] (in-process group: one launch of W x grid CTAs)
 template <typename T>
-static cudaError_t dispatch_ll128(int W, const LL128Args& a, int grid, cudaStream_t st) {
+static cudaError_t dispatch_ll128(int W, const LL128Args* a, int grid, bool group,
+                                  cudaStream_t st) {
   switch (W) {
-#define CANNIKIN_CASE(K) \
-  case K:                \
-    ll128_kernel<T, K><<<grid, kL8Threads, 0, st>>>(a); \
-    return cudaGetLastError();
-    CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5) CANNIKIN_CASE(6)
-    CANNIKIN_CASE(7) CANNIKIN_CASE(8)
-#undef CANNIKIN_CASE
-    default:
-      return cudaErrorInvalidValue;
-  }
-}
-
-template <typename T>
-static cudaError_t dispatch_ll128os(int W, const LL128Args& a, int grid, cudaStream_t st) {
-  switch (W) {
-#define CANNIKIN_CASE(K) \
-  case K:                \
-    ll128os_kernel<T, K><<<grid, kL8Threads, 0, st>>>(a); \
+#define CANNIKIN_CASE(K)                                                     \
+  case K:                                                                    \
+    if (group) {                                                             \
+      GroupArgs<LL128Args> g{};                                              \
+      for (int k = 0; k < K; ++k) g.a[k] = a[k];                             \
+      g.grid = grid;                                                         \
+      ll128_group_kernel<T, K><<<K * grid, kL8Threads, 0, st>>>(g);          \
+    } else {                                                                 \
+      ll128_kernel<T, K><<<grid, kL8Threads, 0, st>>>(a[0]);                 \
+    }                                                                        \
     return cudaGetLastError();
     CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5) CANNIKIN_CASE(6)
     CANNIKIN_CASE(7) CANNIKIN_CASE(8)
@@ -668,23 +493,13 @@ size_t ll128_region_bytes(int world, size_t max_bytes) {
   return kL8HeaderBytes + (size_t)2 * 2 * world * ll128_slot_bytes(world, max_bytes);
 }
 
-// One-shot slot (parity, source): the same data bytes as the two-shot layout, cut into 2 W slots.
-static size_t ll128os_slot_bytes(int world, size_t max_bytes) {
-  const size_t data = (size_t)2 * 2 * world * ll128_slot_bytes(world, max_bytes);
-  return data / (2 * (size_t)world) / kGroupWire * kGroupWire;
-}
-
-size_t ll128os_max_bytes(int world, size_t max_bytes) {
-  return ll128os_slot_bytes(world, max_bytes) / kGroupWire * kGroupPayload;
-}
-
 // Automatic range (measured, profiles/r01/k3_ll128c_*): above the LL kernel's limit and up to
 // 32 MiB: at W = 2 the two-shot wins from 64 MiB (567 vs 549 GB/s; 32 MiB 516 vs 504), at W = 4
 // 32 MiB is a tie for heap buckets (540 vs 544; 16 MiB 504 vs 478) -- and a bucket outside the
 // heap would cost the two-shot two staging copies, the LL128 kernel none (DDP's 25 MB buckets).
 // The choice depends only on (bytes, world), never on where the bucket lives, so every rank
 // picks the same kernel.  CANNIKIN_AR_LL128=1 extends it to the buffer size
-// (CANNIKIN_LL128_MAX_MB, default 64).
+// (CANNIKIN_LL128_MAX_MB, default: this range).
 size_t ll128_auto_bytes(int) { return (size_t)32 << 20; }
 
 bool ll128_eligible(const cannikin_ctx* ctx, size_t bytes) {
@@ -694,46 +509,11 @@ bool ll128_eligible(const cannikin_ctx* ctx, size_t bytes) {
   return bytes <= ll128_auto_bytes(ctx->world) && (bytes > ctx->ll_max_bytes || ctx->ar_ll == 0);
 }
 
-// Automatic one-shot range: none (opt-in, CANNIKIN_AR_LL128OS=1).  Measured
-// (profiles/r01/k3_ll128os_*): at W = 2 within 2% of the two-shot LL128 at every size (1 MB 9.8 vs
-// 9.9 us, 8 MB 21.8 vs 20.7) -- the saved hop is not visible under the per-call fixed cost; at
-// W = 4 it wins only around 0.5 MB (12.9 us vs LL 14.6, LL128 14.3) and loses from 1 MB (twice
-// the wire bytes).  CANNIKIN_LL128OS_AUTO_KB sets a range (tests use it to mix the two layouts).
-size_t ll128os_auto_bytes(int) { return 0; }
-
-bool ll128os_eligible(const cannikin_ctx* ctx, size_t bytes) {
-  if (ctx->world < 2 || !ctx->ll128_off || ctx->ar_ll128os == 0) return false;
-  if (bytes > ll128os_max_bytes(ctx->world, ctx->ll128_max_bytes)) return false;
-  if (ctx->ar_ll128os == 1) return true;
-  return bytes <= ctx->ll128os_auto_bytes && (bytes > ctx->ll_max_bytes || ctx->ar_ll == 0);
-}
-
-cudaError_t launch_ll128os(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt,
-                           double r_i, cudaStream_t st) {
+static int plan_ll128(const cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt,
+                      double r_i, LL128Args* out) {
   const int W = ctx->world;
-  LL128Args a{};
-  a.bucket = static_cast<char*>(bucket);
-  for (int j = 0; j < W; ++j) a.reg[j] = ctx->peer_base[j] + ctx->ll128_off;
-  a.ctrl = ctx->ctrl;
-  a.bytes = n * (dt == CANNIKIN_F32 ? 4 : 2);
-  a.ngroups = (a.bytes + kGroupPayload - 1) / kGroupPayload;
-  a.slot_bytes = ll128os_slot_bytes(W, ctx->ll128_max_bytes);
-  a.timeout_ns = ctx->spin_timeout_ns;
-  a.r_me = (float)r_i;
-  a.rank = ctx->rank;
-  a.check_r = ctx->check_ratios;
-  // about four groups per warp; every rank derives the same grid from (n, W)
-  size_t g = (a.ngroups + 4 * kL8Warps - 1) / (4 * kL8Warps);
-  if (g < 1) g = 1;
-  if (g > (size_t)ctx->grid_ar) g = (size_t)ctx->grid_ar;
-  if (dt == CANNIKIN_F32) return dispatch_ll128os<float>(W, a, (int)g, st);
-  return dispatch_ll128os<__nv_bfloat16>(W, a, (int)g, st);
-}
-
-cudaError_t launch_ll128(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt, double r_i,
-                         cudaStream_t st) {
-  const int W = ctx->world;
-  LL128Args a{};
+  LL128Args& a = *out;
+  a = LL128Args{};
   a.bucket = static_cast<char*>(bucket);
   for (int j = 0; j < W; ++j) a.reg[j] = ctx->peer_base[j] + ctx->ll128_off;
   a.ctrl = ctx->ctrl;
@@ -746,15 +526,28 @@ cudaError_t launch_ll128(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dty
   a.check_r = ctx->check_ratios;
   // about one group per warp and phase (profiles/r01/k3_ll128_gpw_ab_n2.jsonl: 2 MB 192 vs 177
   // GB/s with two, 4-16 MB equal); every rank derives the same grid from (n, W)
-#ifndef CANNIKIN_LL128_GPW
-#define CANNIKIN_LL128_GPW 1
-#endif
   const size_t per_shard = (a.ngroups + W - 1) / W;
-  size_t g = (per_shard + CANNIKIN_LL128_GPW * kL8Warps - 1) / (CANNIKIN_LL128_GPW * kL8Warps);
+  size_t g = (per_shard + kL8Warps - 1) / kL8Warps;
   if (g < 1) g = 1;
   if (g > (size_t)ctx->grid_ar) g = (size_t)ctx->grid_ar;
-  if (dt == CANNIKIN_F32) return dispatch_ll128<float>(W, a, (int)g, st);
-  return dispatch_ll128<__nv_bfloat16>(W, a, (int)g, st);
+  return (int)g;
+}
+
+cudaError_t launch_ll128(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dtype dt, double r_i,
+                         cudaStream_t st) {
+  LL128Args a;
+  const int g = plan_ll128(ctx, bucket, n, dt, r_i, &a);
+  if (dt == CANNIKIN_F32) return dispatch_ll128<float>(ctx->world, &a, g, false, st);
+  return dispatch_ll128<__nv_bfloat16>(ctx->world, &a, g, false, st);
+}
+
+cudaError_t launch_ll128_group(cannikin_ctx* const* ctxs, int W, void* const* buckets, size_t n,
+                               cannikin_dtype dt, const double* r, cudaStream_t st) {
+  LL128Args a[kMaxWorld];
+  int g = 0;
+  for (int k = 0; k < W; ++k) g = plan_ll128(ctxs[k], buckets[k], n, dt, r[k], &a[k]);
+  if (dt == CANNIKIN_F32) return dispatch_ll128<float>(W, a, g, true, st);
+  return dispatch_ll128<__nv_bfloat16>(W, a, g, true, st);
 }
 
 }  // namespace cannikin

@@ -158,14 +158,14 @@ __device__ __forceinline__ void reduce_vec(const uint4 (&x)[W], const float (&r)
 }
 
 template <typename T, int W, int U, int NT>
-__global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
+__device__ __forceinline__ void twoshot_body(const ArArgs& a, const int b, const int G) {
   using V = dev::Vec<T>;
   constexpr int E = V::E;
   __shared__ double red[32 * (W + 1)];
   __shared__ double s_part[W + 1];
   __shared__ float s_r[W];
   __shared__ uint64_t s_ep;
-  const int b = blockIdx.x, tid = threadIdx.x;
+  const int tid = threadIdx.x;
 
   if (tid == 0) {
     s_ep = a.ctrl->epoch[b] + 1;
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
   double gsq = 0.0;
 
   // ---- 1+2. reduce-scatter on S_rank, fused norms, push to every peer
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t stride = (size_t)G * blockDim.x;
   size_t v = a.shard_lo + (size_t)b * blockDim.x + tid;
   for (; v + (U - 1) * stride < a.shard_hi; v += U * stride) {
     uint4 x[U][W];
@@ -265,10 +265,12 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
       acc[j] = __ldcg(&acc[j]) + t;
     }
     a.ctrl->trace[b][4] = dev::globaltimer_ns();
-    if (b == 0) a.ctrl->trace_grid = gridDim.x;
+    if (b == 0) a.ctrl->trace_grid = G;
   }
 }
 
+CANNIKIN_GROUP_ENTRY((typename T, int W, int U, int NT), (T, W, U, NT), (NT, 1), twoshot_kernel,
+                     twoshot_group_kernel, twoshot_body, ArArgs)
 
 // Dynamic variant of K3: identical protocol and arithmetic; the shard is cut into chunks that CTAs
 // claim from a per-rank counter, and every chunk's W+1 norm partials form one row of the peers'
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(NT, 1) twoshot_kernel(const ArArgs a) {
 // did which chunk.  The exit barrier still pairs CTA b with CTA b of every peer: when all CTAs of
 // this rank have passed it, every peer CTA -- hence every peer chunk and row -- is complete.
 template <typename T, int W, int U>
-__global__ void __launch_bounds__(kArThreads, 1) twoshot_dyn_kernel(const ArArgs a) {
+__device__ __forceinline__ void twoshot_dyn_body(const ArArgs& a, const int b, const int G) {
   using V = dev::Vec<T>;
   constexpr int E = V::E;
   constexpr int NT = kArThreads;
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(kArThreads, 1) twoshot_dyn_kernel(const ArArgs
   __shared__ uint64_t s_ep;
   __shared__ unsigned s_chunk[2];
   __shared__ bool s_last;
-  const int b = blockIdx.x, tid = threadIdx.x;
+  const int tid = threadIdx.x;
   const bool has_tail = a.n > a.nvec * E;
   auto nchunks_of = [&](int src) -> unsigned {
     const size_t len = (src == W - 1) ? a.shard_len_last : a.shard_len;
@@ -386,7 +388,7 @@ __global__ void __launch_bounds__(kArThreads, 1) twoshot_dyn_kernel(const ArArgs
     a.ctrl->epoch[b] = ep;
     a.ctrl->trace[b][3] = dev::globaltimer_ns();
     __threadfence();
-    s_last = (atomicAdd(&a.ctrl->ticket_ar, 1u) == gridDim.x - 1);
+    s_last = (atomicAdd(&a.ctrl->ticket_ar, 1u) == G - 1);
   }
   __syncthreads();
   if (!s_last) return;
@@ -412,222 +414,17 @@ __global__ void __launch_bounds__(kArThreads, 1) twoshot_dyn_kernel(const ArArgs
     a.ctrl->ticket_ar = 0u;
     a.ctrl->ar_counter = 0u;
     a.ctrl->trace[b][4] = dev::globaltimer_ns();
-    a.ctrl->trace_grid = gridDim.x;
+    a.ctrl->trace_grid = G;
   }
 }
+CANNIKIN_GROUP_ENTRY((typename T, int W, int U), (T, W, U), (kArThreads, 1), twoshot_dyn_kernel,
+                     twoshot_dyn_group_kernel, twoshot_dyn_body, ArArgs)
 
 template <int W>
 constexpr int u_default_ar() {
   return W <= 2 ? 4 : (W <= 4 ? 2 : 1);
 }
 
-template <typename T, int W>
-static cudaError_t launch_w(const ArArgs& a, int grid, bool dyn, cudaStream_t st) {
-  constexpr int U = u_default_ar<W>();
-  if (dyn) twoshot_dyn_kernel<T, W, U><<<grid, kArThreads, 0, st>>>(a);
-  else twoshot_kernel<T, W, U, kArThreads><<<grid, kArThreads, 0, st>>>(a);
-  return cudaGetLastError();
-}
-
-template <typename T>
-static cudaError_t dispatch_w(int W, const ArArgs& a, int grid, bool dyn, cudaStream_t st) {
-  switch (W) {
-    case 2: return launch_w<T, 2>(a, grid, dyn, st);
-    case 3: return launch_w<T, 3>(a, grid, dyn, st);
-    case 4: return launch_w<T, 4>(a, grid, dyn, st);
-    case 5: return launch_w<T, 5>(a, grid, dyn, st);
-    case 6: return launch_w<T, 6>(a, grid, dyn, st);
-    case 7: return launch_w<T, 7>(a, grid, dyn, st);
-    case 8: return launch_w<T, 8>(a, grid, dyn, st);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
-
-// ============================================================================================
-// One-shot variant of K3 for small buckets (below ~W x 256 KiB): every rank reads the
-// WHOLE bucket of every peer and sums in the same fixed rank order, so every rank computes the
-// identical g (and identical norm partials) by itself -- no all-gather, no partial exchange.
-//   0. entry barrier (as the two-shot): r_j and the bucket identity;
-//   1. CTA b loads its (same on every rank) vectors of all W buckets, reduces in fp32 in rank
-//      order and keeps the result in registers (<= MV vectors per thread), with |g_j|^2 and |g|^2;
-//   2. "done reading" barrier: CTA b tells CTA b of every peer that it has read its part of the
-//      peer's bucket, and waits for the same from every peer;
-//   3. CTA b writes its result into its OWN bucket only (local stores) -- all of that region has
-//      been read by every peer;
-//   4. CTA b adds its partials to its running statistics row (the same on every rank).
-// Nobody writes into a peer's memory except the flag words, so no exit barrier is needed.
-// NVLink bytes per rank, inbound: (W-1) N s (reads); the latency is one entry handshake, one read
-// round trip and one flag handshake.
-// ============================================================================================
-template <typename T, int W, int MV>
-__global__ void __launch_bounds__(kArThreads, 1) oneshot_kernel(const ArArgs a) {
-  using V = dev::Vec<T>;
-  constexpr int E = V::E;
-  __shared__ double red[32 * (W + 1)];
-  __shared__ float s_r[W];
-  __shared__ uint64_t s_ep;
-  const int b = blockIdx.x, tid = threadIdx.x;
-
-  if (tid == 0) {
-    s_ep = a.ctrl->epoch[b] + 1;
-    a.ctrl->trace[b][0] = dev::globaltimer_ns();
-  }
-  __syncthreads();
-  const uint64_t ep = s_ep;
-  if (tid < W) entry_barrier_thread<W>(a, b, ep, s_r);
-  __syncthreads();
-  if (a.check_r && b == 0 && tid == 0) check_ratios<W>(s_r, a.ctrl);
-  if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
-
-  float r[W];
-#pragma unroll
-  for (int j = 0; j < W; ++j) r[j] = s_r[j];
-  double lsq[W];
-#pragma unroll
-  for (int j = 0; j < W; ++j) lsq[j] = 0.0;
-  double gsq = 0.0;
-
-  // ---- 1. loads of every bucket (all issued before any use), fp32 reduction in rank order
-  const size_t stride = (size_t)gridDim.x * kArThreads;
-  const size_t v0 = (size_t)b * kArThreads + tid;
-  uint4 x[MV][W];
-#pragma unroll
-  for (int u = 0; u < MV; ++u) {
-    const size_t v = v0 + u * stride;
-    if (v < a.nvec) {
-#pragma unroll
-      for (int j = 0; j < W; ++j) x[u][j] = dev::ld16(a.bucket[j] + v * 16);
-    }
-  }
-  uint4 y[MV];
-#pragma unroll
-  for (int u = 0; u < MV; ++u) {
-    if (v0 + u * stride < a.nvec) {
-      float acc[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) acc[e] = 0.0f;
-#pragma unroll
-      for (int j = 0; j < W; ++j) {
-        float g[E];
-        V::unpack(x[u][j], g);
-        float sq = 0.0f;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          acc[e] = fmaf(r[j], g[e], acc[e]);
-          sq = fmaf(g[e], g[e], sq);
-        }
-        lsq[j] += (double)sq;
-      }
-      float gs = 0.0f;
-#pragma unroll
-      for (int e = 0; e < E; ++e) gs = fmaf(acc[e], acc[e], gs);
-      gsq += (double)gs;
-      y[u] = V::pack(acc);
-    }
-  }
-  // ragged tail (< one vector of elements): CTA 0 of every rank
-  const size_t et = a.nvec * E + tid;
-  const bool has_t = b == 0 && tid < E && et < a.n;
-  float acc_t = 0.0f;
-  if (has_t) {
-#pragma unroll
-    for (int j = 0; j < W; ++j) {
-      const float g = V::load1(a.bucket[j] + et * sizeof(T));
-      acc_t = fmaf(r[j], g, acc_t);
-      lsq[j] += (double)(g * g);
-    }
-    gsq += (double)(acc_t * acc_t);
-  }
-  double vals[W + 1];
-#pragma unroll
-  for (int j = 0; j < W; ++j) vals[j] = lsq[j];
-  vals[W] = gsq;
-  dev::block_sum(vals, red);  // ends with __syncthreads: every load of the CTA is consumed
-  if (tid == 0) a.ctrl->trace[b][2] = dev::globaltimer_ns();
-
-  // ---- 2. done-reading barrier with CTA b of every peer
-  if (tid < W) {
-    dev::st_release_sys(&a.pctrl[tid]->exit_[b][a.rank], ep);
-    spin_until(&a.ctrl->exit_[b][tid], ep, a.ctrl, a.timeout_ns, 3);
-  }
-  __syncthreads();
-
-  // ---- 3. local stores of the result
-  char* own = a.bucket[a.rank];
-#pragma unroll
-  for (int u = 0; u < MV; ++u) {
-    const size_t v = v0 + u * stride;
-    if (v < a.nvec) dev::st16(own + v * 16, y[u]);
-  }
-  if (has_t) V::store1(own + et * sizeof(T), acc_t);
-
-  // ---- 4. add the CTA's partials to its running row (identical on every rank)
-  if (tid == 0) {
-    double* acc = a.ctrl->cta_acc[b];
-#pragma unroll
-    for (int j = 0; j <= W; ++j) acc[j] = __ldcg(&acc[j]) + vals[j];
-    a.ctrl->epoch[b] = ep;
-    a.ctrl->trace[b][3] = a.ctrl->trace[b][4] = dev::globaltimer_ns();
-    if (b == 0) a.ctrl->trace_grid = gridDim.x;
-  }
-}
-
-constexpr int kOneShotMV = 2;  // result vectors held per thread across the done-reading barrier
-
-template <typename T>
-static cudaError_t dispatch_oneshot(int W, const ArArgs& a, int grid, cudaStream_t st) {
-  switch (W) {
-#define CANNIKIN_CASE(K) \
-  case K:                \
-    oneshot_kernel<T, K, kOneShotMV><<<grid, kArThreads, 0, st>>>(a); \
-    return cudaGetLastError();
-    CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5) CANNIKIN_CASE(6)
-    CANNIKIN_CASE(7) CANNIKIN_CASE(8)
-#undef CANNIKIN_CASE
-    default:
-      return cudaErrorInvalidValue;
-  }
-}
-
-// One-shot launch if the bucket qualifies (returns true and sets *err), else false.
-static bool try_oneshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
-                        cudaStream_t st, cudaError_t* err) {
-  const int W = ctx->world;
-  const size_t esz = dt == CANNIKIN_F32 ? 4 : 2;
-  const size_t bytes = n * esz, nvec = bytes / 16;
-  if (ctx->ar_oneshot == 0) return false;
-  // not chosen automatically any more: the LL kernel (ll.cu) is faster wherever one-shot beat
-  // two-shot (W = 2, <= 512 KiB; profiles/r01/k3_ll_n2.jsonl), and at W = 4 one-shot loses to
-  // two-shot at every size (k3_os_n4.jsonl).  CANNIKIN_AR_ONESHOT=1 still selects it.
-  if (ctx->ar_oneshot != 1) return false;
-  // os_vpt vectors per thread where the grid allows, up to kOneShotMV
-  const size_t per_cta = (size_t)kArThreads * (size_t)ctx->os_vpt;
-  size_t g = (nvec + per_cta - 1) / per_cta;
-  if (g < 1) g = 1;
-  if (g > (size_t)ctx->grid_ar) g = (size_t)ctx->grid_ar;
-  if (nvec > g * kArThreads * kOneShotMV) return false;
-  const int grid = (int)g;
-  ArArgs a{};
-  for (int j = 0; j < W; ++j) {
-    a.bucket[j] = ctx->peer_base[j] + off;
-    a.pctrl[j] = reinterpret_cast<Ctrl*>(ctx->peer_base[j]);
-  }
-  a.ctrl = ctx->ctrl;
-  a.n = n;
-  a.nvec = nvec;
-  uint64_t meta = (uint64_t)off * 0x9E3779B97F4A7C15ull;
-  meta ^= (uint64_t)n * 0xC2B2AE3D27D4EB4Full;
-  meta ^= ((uint64_t)grid << 8) ^ (uint64_t)dt ^ 0x6f6e65ull;
-  a.meta = meta;
-  a.timeout_ns = ctx->spin_timeout_ns;
-  a.r_me = r_i;
-  a.rank = ctx->rank;
-  a.check_r = ctx->check_ratios;
-  *err = dt == CANNIKIN_F32 ? dispatch_oneshot<float>(W, a, grid, st)
-                            : dispatch_oneshot<__nv_bfloat16>(W, a, grid, st);
-  return true;
-}
 
 // ============================================================================================
 // Push variant of K3 (CANNIKIN_AR_PUSH=1): every NVLink transfer is a write.
@@ -657,7 +454,7 @@ struct PushArgs {
 };
 
 template <typename T, int W, int U>
-__global__ void __launch_bounds__(512, 1) twoshot_push_kernel(const PushArgs a) {
+__device__ __forceinline__ void twoshot_push_body(const PushArgs& a, const int b, const int G) {
   using V = dev::Vec<T>;
   constexpr int E = V::E;
   __shared__ double red[32 * (kMaxWorld + 1)];
@@ -665,7 +462,7 @@ __global__ void __launch_bounds__(512, 1) twoshot_push_kernel(const PushArgs a) 
   __shared__ float s_r[W];
   __shared__ uint64_t s_ep;
   __shared__ bool s_last;
-  const int b = blockIdx.x, tid = threadIdx.x, G = gridDim.x, NT = blockDim.x;
+  const int tid = threadIdx.x, NT = blockDim.x;
   auto shard_lo = [&](int k) -> size_t { return a.L * k; };
   auto shard_hi = [&](int k) -> size_t { return (k == W - 1) ? a.nvec : a.L * (k + 1); };
   if (tid == 0) {
@@ -842,7 +639,7 @@ __global__ void __launch_bounds__(512, 1) twoshot_push_kernel(const PushArgs a) 
     a.ctrl->epoch[b] = ep;
     a.ctrl->trace[b][3] = dev::globaltimer_ns();
     __threadfence();
-    s_last = (atomicAdd(&a.ctrl->ticket_ar, 1u) == gridDim.x - 1);
+    s_last = (atomicAdd(&a.ctrl->ticket_ar, 1u) == G - 1);
   }
   __syncthreads();
   if (!s_last) return;
@@ -865,26 +662,30 @@ __global__ void __launch_bounds__(512, 1) twoshot_push_kernel(const PushArgs a) 
     a.ctrl->trace_grid = G;
   }
 }
+CANNIKIN_GROUP_ENTRY((typename T, int W, int U), (T, W, U), (kArThreads, 1), twoshot_push_kernel,
+                     twoshot_push_group_kernel, twoshot_push_body, PushArgs)
 
-template <typename T>
-static cudaError_t dispatch_push(int W, const PushArgs& a, int grid, cudaStream_t st) {
-  switch (W) {
-#define CANNIKIN_CASE(K) \
-  case K:                \
-    twoshot_push_kernel<T, K, K <= 2 ? 4 : 2><<<grid, kArThreads, 0, st>>>(a); \
-    return cudaGetLastError();
-    CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5) CANNIKIN_CASE(6)
-    CANNIKIN_CASE(7) CANNIKIN_CASE(8)
-#undef CANNIKIN_CASE
-    default:
-      return cudaErrorInvalidValue;
-  }
+// Per-rank plan of a two-shot call: variant, grid and kernel arguments.  The variant and grid
+// are functions of (n, dt, W, grid_ar) only, so every rank -- and every rank of an in-process
+// group -- derives the same.
+struct ArPlan {
+  int kind;  // 0 static pull, 1 dynamic pull, 2 push
+  int grid;
+  ArArgs ar;
+  PushArgs push;
+};
+
+static uint64_t bucket_meta(size_t off, size_t n, int grid, cannikin_dtype dt, uint64_t salt) {
+  uint64_t meta = (uint64_t)off * 0x9E3779B97F4A7C15ull;
+  meta ^= (uint64_t)n * 0xC2B2AE3D27D4EB4Full;
+  return meta ^ ((uint64_t)grid << 8) ^ (uint64_t)dt ^ salt;
 }
 
-cudaError_t launch_twoshot_push(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt,
-                                double r_i, cudaStream_t st) {
+static void plan_push(const cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
+                      ArPlan* p) {
   const int W = ctx->world;
-  PushArgs a{};
+  PushArgs& a = p->push;
+  a = PushArgs{};
   for (int j = 0; j < W; ++j) {
     a.bucket[j] = ctx->peer_base[j] + off;
     a.stage[j] = ctx->peer_base[j] + ctx->stage_off;
@@ -901,344 +702,18 @@ cudaError_t launch_twoshot_push(cannikin_ctx* ctx, size_t off, size_t n, canniki
   int grid = ctx->grid_ar;
   const size_t want = (L + (size_t)kArThreads * 2 - 1) / ((size_t)kArThreads * 2);
   if (want < (size_t)grid) grid = want < 1 ? 1 : (int)want;
-  uint64_t meta = (uint64_t)off * 0x9E3779B97F4A7C15ull;
-  meta ^= (uint64_t)n * 0xC2B2AE3D27D4EB4Full;
-  meta ^= ((uint64_t)grid << 8) ^ (uint64_t)dt ^ 0x70757368ull;
-  a.meta = meta;
+  a.meta = bucket_meta(off, n, grid, dt, 0x70757368ull);
   a.timeout_ns = ctx->spin_timeout_ns;
   a.r_me = (float)r_i;
   a.rank = ctx->rank;
   a.check_r = ctx->check_ratios;
-  if (dt == CANNIKIN_F32) return dispatch_push<float>(W, a, grid, st);
-  return dispatch_push<__nv_bfloat16>(W, a, grid, st);
+  p->kind = 2;
+  p->grid = grid;
 }
 
-// ============================================================================================
-// Dynamic push variant of K3 (CANNIKIN_AR_PUSH=2): the push protocol with work items claimed from
-// a per-rank counter, so no CTA waits for a static piece and the two phases overlap.
-//   items 0..S-1 (scatter): chunk c of my part of peer shard S_k -> slot `rank` of k's staging,
-//     chunk-major over the peers, |g_me|^2 on the way; then a per-(source, chunk) flag
-//     (r_rank | call epoch) with release semantics at the owner;
-//   items S..S+R-1 (reduce): chunk c of my own shard, once every peer's flag for c has arrived:
-//     sum own bucket + W-1 staging slots (all LOCAL reads) in rank order (fp32), |g|^2, push the
-//     result into every bucket;
-//   every item's {|g_me|^2, |g|^2} piece is one row of every rank's partial table (so the
-//     statistics do not depend on which CTA did which item); exit barrier (CTA b <-> CTA b: when
-//     all CTAs of this rank pass it, every peer item is done); the last CTA sums all rows in
-//     (rank, row) order.
-// Scatter items never wait, and a CTA claims items in increasing order, so every awaited flag is
-// raised unconditionally: no deadlock for any grid.  NVLink bytes as the other variants.
-// ============================================================================================
-struct PushDynArgs {
-  char* bucket[kMaxWorld];
-  char* stage[kMaxWorld];
-  Ctrl* pctrl[kMaxWorld];
-  Ctrl* ctrl;
-  size_t nvec, n, L, slot_vec, chunk;
-  unsigned C;               // chunks of the largest (last) shard
-  uint64_t meta;
-  uint64_t timeout_ns;
-  float r_me;
-  int rank;
-  int check_r;
-};
-
-template <typename T, int W, int U>
-__global__ void __launch_bounds__(kArThreads, 1) pushdyn_kernel(const PushDynArgs a) {
-  using V = dev::Vec<T>;
-  constexpr int E = V::E;
-  constexpr int NT = kArThreads;
-  __shared__ double red[32 * (W + 1)];
-  __shared__ double s_row[2];
-  __shared__ float s_r[W];
-  __shared__ uint64_t s_ep;
-  __shared__ uint32_t s_ce;
-  __shared__ unsigned s_item[2];
-  __shared__ bool s_last;
-  const int b = blockIdx.x, tid = threadIdx.x, me = a.rank;
-  const bool has_tail = a.n > a.nvec * E;
-  auto lo_of = [&](int k) -> size_t { return a.L * (size_t)k; };
-  auto hi_of = [&](int k) -> size_t { return k == W - 1 ? a.nvec : a.L * (size_t)(k + 1); };
-  auto nck = [&](int k) -> unsigned {
-    unsigned c = (unsigned)((hi_of(k) - lo_of(k) + a.chunk - 1) / a.chunk);
-    if (k == W - 1 && c == 0 && has_tail) c = 1;
-    return c;
-  };
-  const unsigned S = a.C * (W - 1), R = nck(me);
-  const uint32_t m32 = (uint32_t)(a.meta ^ (a.meta >> 32));
-
-  if (tid == 0) {
-    s_ep = a.ctrl->epoch[b] + 1;
-    s_ce = (uint32_t)(a.ctrl->pd_epoch + 1);
-    a.ctrl->trace[b][0] = dev::globaltimer_ns();
-    a.ctrl->trace[b][1] = 0;
-    s_item[0] = atomicAdd(&a.ctrl->ar_counter, 1u);
-    s_item[1] = atomicAdd(&a.ctrl->ar_counter, 1u);
-  }
-  __syncthreads();
-  const uint64_t ep = s_ep;
-  const uint32_t ce = s_ce;
-  if (tid < W)  // bucket identity, checked at the exit barrier
-    dev::st_relaxed_sys_u64(&a.pctrl[tid]->meta_word[b][me], ((uint64_t)m32 << 32) | (uint32_t)ep);
-  const char* mine = a.bucket[me];
-
-  for (unsigned it = 0;; ++it) {
-    const unsigned i = s_item[it & 1];
-    if (i >= S + R) break;
-    double lsq = 0.0, gsq = 0.0;
-    if (i < S) {
-      // ---- scatter item
-      const unsigned c = i / (W - 1);
-      const int k = (me + 1 + (int)(i % (W - 1))) % W;
-      if (c < nck(k)) {
-        const size_t lo = lo_of(k) + (size_t)c * a.chunk;
-        const size_t hi = (lo + a.chunk < hi_of(k)) ? lo + a.chunk : hi_of(k);
-        char* dst = a.stage[k] + ((size_t)me * a.slot_vec - lo_of(k)) * 16;
-        size_t v = lo + tid;
-        for (; v + (U - 1) * NT < hi; v += U * NT) {
-          uint4 x[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) x[u] = dev::ld16(mine + (v + u * NT) * 16);
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            float g[E];
-            V::unpack(x[u], g);
-            float sq = 0.0f;
-#pragma unroll
-            for (int e = 0; e < E; ++e) sq = fmaf(g[e], g[e], sq);
-            lsq += (double)sq;
-            dev::st16(dst + (v + u * NT) * 16, x[u]);
-          }
-        }
-        for (; v < hi; v += NT) {
-          const uint4 x = dev::ld16(mine + v * 16);
-          float g[E];
-          V::unpack(x, g);
-          float sq = 0.0f;
-#pragma unroll
-          for (int e = 0; e < E; ++e) sq = fmaf(g[e], g[e], sq);
-          lsq += (double)sq;
-          dev::st16(dst + v * 16, x);
-        }
-        // my own ragged tail (in shard W-1): its |g_me|^2 goes with the last chunk of that shard,
-        // read before the flag that lets the owner overwrite it
-        if (k == W - 1 && c == nck(k) - 1 && has_tail) {
-          const size_t e = a.nvec * E + tid;
-          if (e < a.n) {
-            const float g = V::load1(mine + e * sizeof(T));
-            lsq += (double)(g * g);
-          }
-        }
-        __syncthreads();  // every store of the chunk has been issued
-        if (tid == 0) {
-          __threadfence_system();
-          dev::st_release_sys(&a.pctrl[k]->sflag[me][c],
-                              ((uint64_t)__float_as_uint(a.r_me) << 32) | ce);
-        }
-      }
-    } else {
-      // ---- reduce item
-      const unsigned c = i - S;
-      if (tid == 0 && a.ctrl->trace[b][1] == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();
-      if (tid < W) {
-        if (tid == me) {
-          s_r[tid] = a.r_me;
-        } else {
-          const uint64_t w = spin_word(&a.ctrl->sflag[tid][c], ce, a.ctrl, a.timeout_ns, 6);
-          s_r[tid] = __uint_as_float((uint32_t)(w >> 32));
-        }
-      }
-      __syncthreads();
-      if (a.check_r && c == 0 && tid == 0) check_ratios<W>(s_r, a.ctrl);
-      float r[W];
-      const char* src[W];
-      char* dst_rot[W];  // staggered destination order, rotated once (static index in the loop)
-      const size_t slo = lo_of(me);
-#pragma unroll
-      for (int j = 0; j < W; ++j) {
-        r[j] = s_r[j];
-        src[j] = (j == me) ? mine + slo * 16 : a.stage[me] + (size_t)j * a.slot_vec * 16;
-        dst_rot[j] = a.bucket[(me + j) % W];
-      }
-      const size_t lo = slo + (size_t)c * a.chunk;
-      const size_t hi = (lo + a.chunk < hi_of(me)) ? lo + a.chunk : hi_of(me);
-      for (size_t v = lo + tid; v < hi; v += NT) {
-        const size_t rel = v - slo;
-        uint4 x[W];
-#pragma unroll
-        for (int j = 0; j < W; ++j) x[j] = dev::ld16(src[j] + rel * 16);
-        float acc[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e) acc[e] = 0.0f;
-#pragma unroll
-        for (int j = 0; j < W; ++j) {
-          float g[E];
-          V::unpack(x[j], g);
-#pragma unroll
-          for (int e = 0; e < E; ++e) acc[e] = fmaf(r[j], g[e], acc[e]);
-          if (j == me) {
-            float sq = 0.0f;
-#pragma unroll
-            for (int e = 0; e < E; ++e) sq = fmaf(g[e], g[e], sq);
-            lsq += (double)sq;
-          }
-        }
-        float gs = 0.0f;
-#pragma unroll
-        for (int e = 0; e < E; ++e) gs = fmaf(acc[e], acc[e], gs);
-        gsq += (double)gs;
-        const uint4 y = V::pack(acc);
-#pragma unroll
-        for (int jj = 0; jj < W; ++jj) dev::st16(dst_rot[jj] + v * 16, y);
-      }
-      // the ragged element tail: owned by the last rank, with its last chunk; every peer's flag
-      // for that chunk has arrived, so every peer has read its own tail (and its bucket is ready)
-      if (me == W - 1 && c == R - 1 && has_tail) {
-        const size_t e = a.nvec * E + tid;
-        if (e < a.n) {
-          float acc = 0.0f;
-#pragma unroll
-          for (int j = 0; j < W; ++j) {
-            const float g = V::load1(a.bucket[j] + e * sizeof(T));
-            acc = fmaf(r[j], g, acc);
-            if (j == me) lsq += (double)(g * g);
-          }
-          gsq += (double)(acc * acc);
-#pragma unroll
-          for (int j = 0; j < W; ++j) V::store1(a.bucket[j] + e * sizeof(T), acc);
-        }
-      }
-    }
-    // ---- this item's row {|g_me|^2, |g|^2} -> every rank's table (zero rows for empty items)
-    double vals[2] = {lsq, gsq};
-    dev::block_sum(vals, red);
-    if (tid == 0) {
-      s_row[0] = vals[0];
-      s_row[1] = vals[1];
-      s_item[it & 1] = atomicAdd(&a.ctrl->ar_counter, 1u);
-    }
-    __syncthreads();
-    if (tid < W) {
-      double* row = &a.pctrl[tid]->part[me][i][0];
-#pragma unroll
-      for (int j = 0; j <= W; ++j)
-        dev::st_relaxed_sys_f64(row + j, j == me ? s_row[0] : (j == W ? s_row[1] : 0.0));
-    }
-  }
-  if (tid == 0) {
-    a.ctrl->trace[b][2] = dev::globaltimer_ns();
-    if (a.ctrl->trace[b][1] == 0) a.ctrl->trace[b][1] = a.ctrl->trace[b][2];
-  }
-  __syncthreads();  // every data, flag and row store of this CTA has been issued
-
-  // ---- exit barrier (+ the bucket-identity check)
-  if (tid < W) {
-    __threadfence_system();
-    dev::st_release_sys(&a.pctrl[tid]->exit_[b][me], ep);
-    spin_until(&a.ctrl->exit_[b][tid], ep, a.ctrl, a.timeout_ns, 3);
-    const uint64_t wm = spin_word(&a.ctrl->meta_word[b][tid], (uint32_t)ep, a.ctrl, a.timeout_ns, 2);
-    if ((uint32_t)(wm >> 32) != m32) {
-      atomicExch(&a.ctrl->error_code, 2);
-      __trap();
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    a.ctrl->epoch[b] = ep;
-    a.ctrl->trace[b][3] = dev::globaltimer_ns();
-    __threadfence();
-    s_last = (atomicAdd(&a.ctrl->ticket_ar, 1u) == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  double tot[W + 1];
-#pragma unroll
-  for (int j = 0; j <= W; ++j) tot[j] = 0.0;
-  for (int src = 0; src < W; ++src) {
-    const unsigned nrows = S + nck(src);
-    for (unsigned i = tid; i < nrows; i += NT) {
-      const double* row = &a.ctrl->part[src][i][0];
-#pragma unroll
-      for (int j = 0; j <= W; ++j) tot[j] += __ldcg(row + j);
-    }
-  }
-  dev::block_sum(tot, red);
-  if (tid == 0) {
-#pragma unroll
-    for (int j = 0; j <= W; ++j) a.ctrl->stats[j] += tot[j];
-    a.ctrl->ticket_ar = 0u;
-    a.ctrl->ar_counter = 0u;
-    a.ctrl->pd_epoch = a.ctrl->pd_epoch + 1;
-    a.ctrl->trace[b][4] = dev::globaltimer_ns();
-    a.ctrl->trace_grid = gridDim.x;
-  }
-}
-
-template <typename T>
-static cudaError_t dispatch_pushdyn(int W, const PushDynArgs& a, int grid, cudaStream_t st) {
-  switch (W) {
-#define CANNIKIN_CASE(K) \
-  case K:                \
-    pushdyn_kernel<T, K, K <= 2 ? 4 : 2><<<grid, kArThreads, 0, st>>>(a); \
-    return cudaGetLastError();
-    CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5) CANNIKIN_CASE(6)
-    CANNIKIN_CASE(7) CANNIKIN_CASE(8)
-#undef CANNIKIN_CASE
-    default:
-      return cudaErrorInvalidValue;
-  }
-}
-
-cudaError_t launch_pushdyn(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
-                           cudaStream_t st) {
+static void plan_twoshot(const cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt,
+                         double r_i, ArPlan* p) {
   const int W = ctx->world;
-  PushDynArgs a{};
-  for (int j = 0; j < W; ++j) {
-    a.bucket[j] = ctx->peer_base[j] + off;
-    a.stage[j] = ctx->peer_base[j] + ctx->stage_off;
-    a.pctrl[j] = reinterpret_cast<Ctrl*>(ctx->peer_base[j]);
-  }
-  a.ctrl = ctx->ctrl;
-  const size_t esz = dt == CANNIKIN_F32 ? 4 : 2;
-  a.n = n;
-  a.nvec = n * esz / 16;
-  size_t L = a.nvec / W;
-  L -= L % 64;
-  a.L = L;
-  const size_t last = a.nvec - L * (size_t)(W - 1);
-  a.slot_vec = last;
-  // chunk: the preferred size, grown so that W x (chunks of the largest shard) rows fit the table
-  size_t chunk = (size_t)ctx->pd_chunk_kb * 1024 / 16;
-  const size_t cmax = (size_t)(kMaxArChunks - 1) / (size_t)W;
-  const size_t need = (last + cmax - 1) / cmax;
-  if (need > chunk) chunk = need;
-  chunk = (chunk + kArThreads - 1) / kArThreads * kArThreads;
-  a.chunk = chunk;
-  unsigned C = (unsigned)((last + chunk - 1) / chunk);
-  if (C == 0 && n * esz > a.nvec * 16) C = 1;
-  a.C = C;
-  int grid = ctx->grid_ar;
-  uint64_t meta = (uint64_t)off * 0x9E3779B97F4A7C15ull;
-  meta ^= (uint64_t)n * 0xC2B2AE3D27D4EB4Full;
-  meta ^= ((uint64_t)grid << 8) ^ (uint64_t)dt ^ ((uint64_t)chunk * 0x94D049BB133111EBull) ^ 0x7064ull;
-  a.meta = meta;
-  a.timeout_ns = ctx->spin_timeout_ns;
-  a.r_me = (float)r_i;
-  a.rank = ctx->rank;
-  a.check_r = ctx->check_ratios;
-  if (dt == CANNIKIN_F32) return dispatch_pushdyn<float>(W, a, grid, st);
-  return dispatch_pushdyn<__nv_bfloat16>(W, a, grid, st);
-}
-
-// Launch K3 on the bucket at byte offset `off` of every rank's allocation.
-cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
-                           cudaStream_t st) {
-  const int W = ctx->world;
-  {
-    cudaError_t err;
-    if (try_oneshot(ctx, off, n, dt, r_i, st, &err)) return err;
-  }
   {
     // push (all-write) pays for large buckets from 4 ranks up (W = 4: equal at 64 MB, +5% at
     // 256 MB-1 GB; profiles/r01/k3_pull_dyn_push_n4.jsonl); pull is better for small buckets and at
@@ -1246,11 +721,11 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
     // sends C4's 220 MB bucket through the all-write pattern, which held up best under all-to-all
     // load at W = 4 (profiles/r01/nvlink_bw_n4.jsonl)
     const size_t bucket_bytes = n * (dt == CANNIKIN_F32 ? 4 : 2);
-    if (ctx->ar_push == 2 && ctx->stage_off) return launch_pushdyn(ctx, off, n, dt, r_i, st);
-    const bool push = ctx->ar_push == 1 || (ctx->ar_push < 0 && W >= 4 && bucket_bytes >= (128ull << 20));
-    if (push && ctx->stage_off) return launch_twoshot_push(ctx, off, n, dt, r_i, st);
+    const bool push = ctx->ar_push == 1 || (ctx->ar_push < 0 && W >= 4 && bucket_bytes >= kPushAutoBytes);
+    if (push && ctx->stage_off) return plan_push(ctx, off, n, dt, r_i, p);
   }
-  ArArgs a{};
+  ArArgs& a = p->ar;
+  a = ArArgs{};
   for (int j = 0; j < W; ++j) {
     a.bucket[j] = ctx->peer_base[j] + off;
     a.pctrl[j] = reinterpret_cast<Ctrl*>(ctx->peer_base[j]);
@@ -1269,9 +744,6 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
   const size_t per_cta = (size_t)kArThreads * 2;
   const size_t want = (L + per_cta - 1) / per_cta;
   if (want < (size_t)grid) grid = want < 1 ? 1 : (int)want;
-  uint64_t meta = (uint64_t)off * 0x9E3779B97F4A7C15ull;
-  meta ^= (uint64_t)n * 0xC2B2AE3D27D4EB4Full;
-  meta ^= ((uint64_t)grid << 8) ^ (uint64_t)dt;
   a.timeout_ns = ctx->spin_timeout_ns;
   a.r_me = r_i;
   a.rank = ctx->rank;
@@ -1290,14 +762,77 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
   a.chunk = chunk;
   a.shard_len_last = a.nvec - L * (size_t)(W - 1);
   a.shard_len = L;
-  if (dyn) meta ^= (uint64_t)chunk * 0x94D049BB133111EBull;
-  a.meta = meta;
-  if (dt == CANNIKIN_F32) return dispatch_w<float>(W, a, grid, dyn, st);
-  return dispatch_w<__nv_bfloat16>(W, a, grid, dyn, st);
+  a.meta = bucket_meta(off, n, grid, dt, dyn ? (uint64_t)chunk * 0x94D049BB133111EBull : 0);
+  p->kind = dyn ? 1 : 0;
+  p->grid = grid;
+}
+
+template <typename T, int W>
+static cudaError_t launch_plan(const ArPlan& p, cudaStream_t st) {
+  constexpr int U = u_default_ar<W>();
+  constexpr int UP = W <= 2 ? 4 : 2;
+  if (p.kind == 0) twoshot_kernel<T, W, U, kArThreads><<<p.grid, kArThreads, 0, st>>>(p.ar);
+  else if (p.kind == 1) twoshot_dyn_kernel<T, W, U><<<p.grid, kArThreads, 0, st>>>(p.ar);
+  else twoshot_push_kernel<T, W, UP><<<p.grid, kArThreads, 0, st>>>(p.push);
+  return cudaGetLastError();
+}
+
+// p[0..W-1]: the plans of ranks 0..W-1 of an in-process group, one launch of W x grid CTAs
+template <typename T, int W>
+static cudaError_t launch_plan_group(const ArPlan* p, cudaStream_t st) {
+  constexpr int U = u_default_ar<W>();
+  constexpr int UP = W <= 2 ? 4 : 2;
+  const int G = p[0].grid;
+  if (p[0].kind == 2) {
+    GroupArgs<PushArgs> g{};
+    for (int k = 0; k < W; ++k) g.a[k] = p[k].push;
+    g.grid = G;
+    twoshot_push_group_kernel<T, W, UP><<<W * G, kArThreads, 0, st>>>(g);
+  } else {
+    GroupArgs<ArArgs> g{};
+    for (int k = 0; k < W; ++k) g.a[k] = p[k].ar;
+    g.grid = G;
+    if (p[0].kind == 0) twoshot_group_kernel<T, W, U, kArThreads><<<W * G, kArThreads, 0, st>>>(g);
+    else twoshot_dyn_group_kernel<T, W, U><<<W * G, kArThreads, 0, st>>>(g);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t dispatch_plan(int W, const ArPlan* p, bool group, cudaStream_t st) {
+  switch (W) {
+#define CANNIKIN_CASE(K) \
+  case K:                \
+    return group ? launch_plan_group<T, K>(p, st) : launch_plan<T, K>(*p, st);
+    CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5) CANNIKIN_CASE(6)
+    CANNIKIN_CASE(7) CANNIKIN_CASE(8)
+#undef CANNIKIN_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+// Launch K3 on the bucket at byte offset `off` of every rank's allocation.
+cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dtype dt, double r_i,
+                           cudaStream_t st) {
+  ArPlan p;
+  plan_twoshot(ctx, off, n, dt, r_i, &p);
+  if (dt == CANNIKIN_F32) return dispatch_plan<float>(ctx->world, &p, false, st);
+  return dispatch_plan<__nv_bfloat16>(ctx->world, &p, false, st);
+}
+
+// The same for all W ranks of an in-process group in ONE launch (bucket at byte offset `off` of
+// every rank's region; r[k] = rank k's share).
+cudaError_t launch_twoshot_group(cannikin_ctx* const* ctxs, int W, size_t off, size_t n,
+                                 cannikin_dtype dt, const double* r, cudaStream_t st) {
+  ArPlan p[kMaxWorld];
+  for (int k = 0; k < W; ++k) plan_twoshot(ctxs[k], off, n, dt, r[k], &p[k]);
+  if (dt == CANNIKIN_F32) return dispatch_plan<float>(W, p, true, st);
+  return dispatch_plan<__nv_bfloat16>(W, p, true, st);
 }
 
 // Finalize the statistics of all calls since the last finalize: out[j] = stats[j] (dynamic / push
-// two-shot, NVLS, world 1) + sum over b of cta_acc[b][j] (static two-shot, one-shot) in ascending
+// two-shot, NVLS, world 1) + sum over b of cta_acc[b][j] (static two-shot, LL, LL128) in ascending
 // b, then zero both.  One warp; `out` may be device or pinned host memory.
 __global__ void stats_finalize_kernel(Ctrl* c, int W, double* out) {
   const int j = threadIdx.x;

@@ -8,6 +8,7 @@ from __future__ import annotations
 import torch
 
 from . import BF16, F32, Context, get_unique_id
+from . import weighted_allreduce_group as _group_ar
 
 _CODES = {torch.float32: F32, torch.bfloat16: BF16}
 
@@ -49,6 +50,15 @@ def weighted_allreduce(ctx: Context, bucket: torch.Tensor, r_i: float, stream=No
     assert bucket.is_cuda and bucket.is_contiguous()
     ctx.weighted_allreduce(bucket.data_ptr(), bucket.numel(), dtype_code(bucket.dtype), r_i,
                            _cur(stream))
+
+
+def weighted_allreduce_group(ctxs, buckets, r, stream=None):
+    """Every rank of an in-process group (Context.group_local) in ONE kernel launch: buckets[k]
+    <- sum_j r[j] buckets[j] (Eq. 9), norms accumulated in every rank's ctx."""
+    n, dt = buckets[0].numel(), buckets[0].dtype
+    for b in buckets:
+        assert b.is_cuda and b.is_contiguous() and b.numel() == n and b.dtype == dt
+    _group_ar(ctxs, [b.data_ptr() for b in buckets], n, dtype_code(dt), list(r), _cur(stream))
 
 
 def weighted_allreduce_nccl(ctx: Context, bucket: torch.Tensor, r_i: float, stream=None):

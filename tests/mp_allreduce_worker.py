@@ -15,6 +15,7 @@ import torch.distributed as dist
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import cannikin_synth as synth  # noqa: E402
 import paper_2402_05302_b200 as ck  # noqa: E402
@@ -29,7 +30,7 @@ CASES = [  # (name, N, dtype, seed)
     ("big_bf16", 3_000_011, "bf16", 6),
     ("resnet18", 11_689_512, "f32", 7),    # configs[1]
     ("resnet50", 25_557_032, "f32", 11),   # configs[2]
-    ("os_f32", 300_001, "f32", 8),     # one-shot sized: several CTAs, ragged tail
+    ("os_f32", 300_001, "f32", 8),     # LL sized: several CTAs, ragged tail
     ("os_bf16", 600_007, "bf16", 10),
     # multiples of 64 elements: every shard full (the NCCL path's in-place fast paths)
     ("pow2_f32", 1 << 20, "f32", 12),
@@ -65,8 +66,12 @@ FULL = {  # BASELINE configs at full size in the bench launch configuration: (N,
 
 def full_case(ctx, rank, world, out, cfg):
     """One BASELINE config at full size in the bench launch configuration (one zero-copy bucket,
-    default grid): saves sampled elements of every rank's input and of the result, the whole
-    inputs (rank 0, chunked, for the oracle norms) and the statistics."""
+    default grid).  Every rank's input of record and result are gathered to rank 0 (plumbing),
+    which compares EVERY element of rank 0's result with the oracle chunk by chunk and every other
+    rank's result bitwise with rank 0's (tests/parity.py), and saves the oracle's whole-vector
+    norms; every rank saves its statistics."""
+    import parity
+
     N, dt, seed = FULL[cfg]
     tdt = torch.bfloat16 if dt == "bf16" else torch.float32
     b = b_for(world, seed)
@@ -74,22 +79,22 @@ def full_case(ctx, rank, world, out, cfg):
     g = synth.device_gns_gradients(world, N, b, seed=seed, dtype=dt, ranks=[rank])[0]
     bucket = ta.bucket_tensor(ctx, N, tdt)
     bucket.copy_(g)
-    idx = torch.from_numpy(np.random.default_rng(0).choice(N, 200_000, replace=False)).cuda()
     ins = [torch.empty_like(g) for _ in range(world)]
     dist.all_gather(ins, g)  # plumbing: every rank's input of record, for the oracle on rank 0
+    del g
     ta.weighted_allreduce(ctx, bucket, b[rank] / B)
     loc, glob = ctx.gns_stats()
-    res = {"idx": idx.cpu().numpy(), "out": from_dev(bucket[idx], dt),
-           "ins": np.stack([from_dev(x[idx], dt) for x in ins]), "loc": np.array(loc),
-           "glob": glob, "b": np.array(b)}
+    outs = [torch.empty_like(bucket) for _ in range(world)]
+    dist.all_gather(outs, bucket)
+    res = {"loc": np.array(loc), "glob": glob, "b": np.array(b)}
     if rank == 0:
-        chunk = 10_000_000
-        for a in range(0, N, chunk):
-            np.save(os.path.join(out, f"full_in_{a:012d}.npy"),
-                    np.stack([from_dev(x[a:a + chunk], dt) for x in ins]))
+        from oracle import aggregate as agg
+        err, lsum, gsum = parity.compare_full(outs, ins, agg.ratios(b), dt,
+                                              1e-2 if dt == "bf16" else 1e-5, chunk=20_000_000)
+        res.update(max_err=err, oracle_loc=lsum, oracle_glob=gsum)
     np.savez(os.path.join(out, f"rank{rank}_full.npz"), **res)
     ta.free_bucket_tensor(ctx, bucket)
-    del ins, g
+    del ins, outs
 
 
 def main():
@@ -135,14 +140,12 @@ def main():
         return
     if args.variants:
         # the same inputs through every K3 variant: the result bits must not depend on it
-        VARS = {"static": ("0", "0", "0", "0", "0", "0"), "dyn": ("1", "0", "0", "0", "0", "0"),
-                "push": ("0", "1", "0", "0", "0", "0"), "pushdyn": ("0", "2", "0", "0", "0", "0"),
-                "oneshot": ("0", "0", "1", "0", "0", "0"), "ll": ("0", "0", "0", "1", "0", "0"),
-                "ll128": ("0", "0", "0", "0", "1", "0"), "ll128os": ("0", "0", "0", "0", "0", "1")}
-        for name, (dyn, push, one, ll, ll128, ll128os) in VARS.items():
-            os.environ.update(CANNIKIN_AR_DYN=dyn, CANNIKIN_AR_PUSH=push, CANNIKIN_AR_ONESHOT=one,
-                              CANNIKIN_AR_LL=ll, CANNIKIN_AR_LL128=ll128,
-                              CANNIKIN_AR_LL128OS=ll128os, CANNIKIN_PD_CHUNK_KB="16")
+        VARS = {"static": ("0", "0", "0", "0"), "dyn": ("1", "0", "0", "0"),
+                "push": ("0", "1", "0", "0"), "ll": ("0", "0", "1", "0"),
+                "ll128": ("0", "0", "0", "1")}
+        for name, (dyn, push, ll, ll128) in VARS.items():
+            os.environ.update(CANNIKIN_AR_DYN=dyn, CANNIKIN_AR_PUSH=push, CANNIKIN_AR_LL=ll,
+                              CANNIKIN_AR_LL128=ll128)
             ctx = ta.init_distributed_context(heap_bytes=(1 << 22), grid=args.grid)
             for N, dtype in ((100_003, "f32"), (200_011, "bf16")):
                 b = b_for(world, 21)

@@ -18,6 +18,8 @@ from paper_2402_05302_b200 import torch_api as ta  # noqa: E402
 from oracle import aggregate as agg  # noqa: E402
 from oracle import gns as ogns  # noqa: E402
 
+import parity  # noqa: E402
+
 TOL = {"f32": 1e-5, "bf16": 1e-2}
 TDT = {"f32": torch.float32, "bf16": torch.bfloat16}
 
@@ -205,9 +207,10 @@ def test_errors(ctx):
 
 @pytest.mark.parametrize("variant", ["ldg", "tma"])
 @pytest.mark.parametrize("nr", [8])
-def test_full_size_c4_sampled(ctx, nr, variant):
+def test_full_size_c4(ctx, nr, variant):
     """configs[3] at full size in the bench launch configuration: 110M bf16, 8 emulated ranks.
-    Sampled elements vs the oracle one by one; the norms vs the oracle over the whole vectors."""
+    EVERY element against the oracle (chunked, tests/parity.py); the norms against the oracle
+    over the whole vectors."""
     N = 110_000_000
     b = [37, 29, 21, 12, 9, 8, 3, 1]
     gs = synth.device_gns_gradients(nr, N, b, seed=0, dtype="bf16")
@@ -217,23 +220,44 @@ def test_full_size_c4_sampled(ctx, nr, variant):
     glob = torch.zeros(1, dtype=torch.float64, device="cuda")
     ta.weighted_sum_local(ctx, gs, r, out, local, glob, variant=variant)
     torch.cuda.synchronize()
-    idx = torch.from_numpy(np.random.default_rng(0).choice(N, 200_000, replace=False)).cuda()
-    samp = [from_dev(g[idx], "bf16") for g in gs]
-    ref = agg.weighted_sum([agg.to_f64(s, "bf16") for s in samp], r)
-    got = agg.to_f64(from_dev(out[idx], "bf16"), "bf16")
-    scale = np.maximum(agg.elementwise_scale([agg.to_f64(s, "bf16") for s in samp], r), 1e-30)
-    assert np.max(np.abs(got - ref) / scale) <= 1e-2
-    ls = local.cpu().numpy()
-    chunk = 10_000_000
-    gsum = 0.0
-    lsum = np.zeros(nr)
-    for a in range(0, N, chunk):
-        parts = [agg.to_f64(from_dev(g[a:a + chunk], "bf16"), "bf16") for g in gs]
-        for j in range(nr):
-            lsum[j] += agg.sq_norm(parts[j])
-        gsum += agg.sq_norm(agg.weighted_sum(parts, r))
-    assert np.allclose(ls, lsum, rtol=1e-4)
+    _, lsum, gsum = parity.compare_full([out], gs, r, "bf16", TOL["bf16"], chunk=10_000_000)
+    assert np.allclose(local.cpu().numpy(), lsum, rtol=1e-4)
     assert abs(float(glob.cpu()[0]) - gsum) <= 1e-4 * gsum
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("nr,N", [(1, (8 << 20) + 3), (2, (8 << 20) + 3), (3, (4 << 20) + 5),
+                                  (4, (4 << 20) + 5), (2, 33_554_435)])
+def test_unrolled_main_loops_every_element(ctx, dtype, nr, N):
+    """The unrolled grid-stride loops of K2 (U = 4 vectors per thread per rank for n <= 2, U = 2 for
+    n <= 4; wsum_local.cu) only run once the bucket exceeds (U-1) grid strides (~151k vectors per
+    stride at 4 CTAs/SM), i.e. beyond the 2^20-element cases above: 4-33M elements, every element
+    against the oracle, both dtypes, ragged tails."""
+    b = [int(x) for x in np.random.default_rng(nr + N).integers(1, 100, size=nr)]
+    gs = synth.device_gns_gradients(nr, N, b, seed=nr * 3 + 1, dtype=dtype)
+    r = agg.ratios(b)
+    out = torch.empty(N, dtype=TDT[dtype], device="cuda")
+    local = torch.zeros(nr, dtype=torch.float64, device="cuda")
+    glob = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ta.weighted_sum_local(ctx, gs, r, out, local, glob, variant="ldg")
+    torch.cuda.synchronize()
+    _, lsum, gsum = parity.compare_full([out], gs, r, dtype, TOL[dtype])
+    assert np.allclose(local.cpu().numpy(), lsum, rtol=1e-4)
+    assert abs(float(glob.cpu()[0]) - gsum) <= 1e-4 * gsum
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_world1_allreduce_large_every_element(ctx, dtype):
+    """world-1 cannikin_weighted_allreduce over a > 8M-element bucket (K2 with n = 1, U = 4 loop):
+    g = r_0 g_0 in place, every element against the oracle; statistics through gns_stats."""
+    N = (9 << 20) + 7
+    g = synth.device_gns_gradients(1, N, [8], seed=21, dtype=dtype)[0]
+    t = g.clone()
+    ta.weighted_allreduce(ctx, t, 0.625)
+    loc, glob = ctx.gns_stats()
+    _, lsum, gsum = parity.compare_full([t], [g], [0.625], dtype, TOL[dtype])
+    assert abs(loc[0] - lsum[0]) <= 1e-4 * lsum[0]
+    assert abs(glob - gsum) <= 1e-4 * gsum
 
 
 @pytest.mark.parametrize("variant", ["ldg", "tma"])
@@ -260,9 +284,9 @@ def test_no_out_of_bounds_writes(ctx, dtype, N, variant):
     del esz
 
 
-def test_full_size_c5_sampled(ctx):
-    """configs[4]'s 355M fp32 gradient at full size on one GPU (3 emulated ranks): sampled
-    elements against the oracle one by one, norms against the oracle over the whole vectors."""
+def test_full_size_c5(ctx):
+    """configs[4]'s 355M fp32 gradient at full size on one GPU (3 emulated ranks): EVERY element
+    against the oracle (chunked), norms against the oracle over the whole vectors."""
     N, nr = 354_823_168, 3
     b = [5, 17, 40]
     gs = synth.device_gns_gradients(nr, N, b, seed=2, dtype="f32")
@@ -272,18 +296,6 @@ def test_full_size_c5_sampled(ctx):
     glob = torch.zeros(1, dtype=torch.float64, device="cuda")
     ta.weighted_sum_local(ctx, gs, r, out, local, glob)
     torch.cuda.synchronize()
-    idx = torch.from_numpy(np.random.default_rng(1).choice(N, 200_000, replace=False)).cuda()
-    samp = [agg.to_f64(g[idx].cpu().numpy(), "f32") for g in gs]
-    ref = agg.weighted_sum(samp, r)
-    got = out[idx].cpu().numpy().astype(np.float64)
-    scale = np.maximum(agg.elementwise_scale(samp, r), 1e-30)
-    assert np.max(np.abs(got - ref) / scale) <= 1e-5
-    lsum, gsum = np.zeros(nr), 0.0
-    chunk = 20_000_000
-    for a in range(0, N, chunk):
-        parts = [agg.to_f64(g[a:a + chunk].cpu().numpy(), "f32") for g in gs]
-        for j in range(nr):
-            lsum[j] += agg.sq_norm(parts[j])
-        gsum += agg.sq_norm(agg.weighted_sum(parts, r))
+    _, lsum, gsum = parity.compare_full([out], gs, r, "f32", TOL["f32"], chunk=20_000_000)
     assert np.allclose(local.cpu().numpy(), lsum, rtol=1e-4)
     assert abs(float(glob.cpu()[0]) - gsum) <= 1e-4 * gsum

@@ -34,8 +34,7 @@ def _port():
     return p
 
 
-@pytest.fixture(scope="module", params=["static", "dyn", "push", "pushdyn", "oneshot", "ll", "ll128", "ll128os",
-                                               "nccl"])
+@pytest.fixture(scope="module", params=["static", "dyn", "push", "ll", "ll128", "nccl"])
 def results(request):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -46,18 +45,13 @@ def results(request):
            os.path.join(os.path.dirname(__file__), "mp_allreduce_worker.py"), "--out", d]
     env = dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000",
                CANNIKIN_AR_DYN="1" if request.param == "dyn" else "0",
-               CANNIKIN_AR_PUSH={"push": "1", "pushdyn": "2"}.get(request.param, "0"),
-               CANNIKIN_PD_CHUNK_KB="16",  # many chunks (grown where the row table needs it)
-               # "oneshot": every bucket that fits the one-shot kernel uses it (larger ones, and
-               # the larger pieces of case (4), fall back to two-shot: mixed sequences)
-               CANNIKIN_AR_ONESHOT="1" if request.param == "oneshot" else "0",
+               CANNIKIN_AR_PUSH="1" if request.param == "push" else "0",
                # "ll": buckets <= 1 MiB / (W-1) through the low-latency kernel (no heap bucket needed)
                CANNIKIN_AR_LL="1" if request.param == "ll" else "0",
                # "ll128": every bucket up to 64 MiB (all but the 355M full-size case) through the
                # flag-in-line two-shot kernel
                CANNIKIN_AR_LL128="1" if request.param == "ll128" else "0",
-               # "ll128os": its one-shot form for every bucket its slots hold (all but C5 full)
-               CANNIKIN_AR_LL128OS="1" if request.param == "ll128os" else "0",
+               CANNIKIN_LL128_MAX_MB="64",
                # "nccl": the cases through cannikin_weighted_allreduce_nccl (K4: NCCL
                # reduce-scatter / all-gather with fused pre/post kernels)
                CANNIKIN_TEST_PATH="nccl" if request.param == "nccl" else "p2p")
@@ -138,7 +132,7 @@ def test_result_bits_independent_of_variant():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     for dtype in ("f32", "bf16"):
         ref = np.load(os.path.join(d, f"rank0_var_static_{dtype}.npy"))
-        for name in ("static", "dyn", "push", "pushdyn", "oneshot", "ll", "ll128", "ll128os"):
+        for name in ("static", "dyn", "push", "ll", "ll128"):
             for k in range(world):
                 got = np.load(os.path.join(d, f"rank{k}_var_{name}_{dtype}.npy"))
                 assert np.array_equal(got, ref), (name, dtype, k)

@@ -100,3 +100,33 @@ def test_bf16_round_to_nearest_even():
     x = np.array([1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8], dtype=np.float32)
     back = agg.to_f64(synth.f32_to_bf16_bits(x), "bf16")
     assert back[0] == 1.0 and back[1] == 1.0 + 2 ** -6
+
+
+def test_elementwise_scale_hand_values():
+    """Pin of the error-metric denominator (reading Q1): sum_i |r_i g_i[e]| per element, by hand.
+    r = (0.25, 0.75), g_0 = (2, 4, 0), g_1 = (-1, 4, -8):
+      e=0: |0.25*2| + |0.75*(-1)| = 0.5 + 0.75 = 1.25   (a plain |sum| would give 0.25)
+      e=1: 1 + 3 = 4                                    (no cancellation: equals |sum|)
+      e=2: 0 + 6 = 6                                    (one rank zero)
+    Catches: a dropped r (|g_0|+|g_1| = 3), a max over ranks (0.75), |sum| (0.25), or the sum
+    without abs (-0.25)."""
+    g0 = np.array([2.0, 4.0, 0.0])
+    g1 = np.array([-1.0, 4.0, -8.0])
+    s = agg.elementwise_scale([g0, g1], [0.25, 0.75])
+    assert s.tolist() == [1.25, 4.0, 6.0]
+
+
+def test_elementwise_scale_bounds_the_aggregate():
+    """Triangle inequality: |sum_i r_i g_i[e]| <= scale[e], with equality where all terms share a
+    sign; scale is linear in |r| (doubling r doubles it) and independent of the sign of r_i."""
+    gs = synth.gns_gradients(4, 4099, [3, 5, 7, 9], seed=8)
+    gs64 = [agg.to_f64(g, "f32") for g in gs]
+    r = agg.ratios([3, 5, 7, 9])
+    s = agg.elementwise_scale(gs64, r)
+    g = agg.weighted_sum(gs64, r)
+    assert np.all(np.abs(g) <= s * (1 + 1e-15))
+    same = np.all(np.stack(gs64) > 0, axis=0) | np.all(np.stack(gs64) < 0, axis=0)
+    assert same.any()
+    assert np.allclose(np.abs(g[same]), s[same], rtol=1e-14)
+    assert np.allclose(agg.elementwise_scale(gs64, 2 * r), 2 * s, rtol=1e-15)
+    assert np.array_equal(agg.elementwise_scale(gs64, -r), s)

@@ -49,7 +49,7 @@ def main():
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--grids", default="0")
     ap.add_argument("--variants", default="0",
-                    help="CANNIKIN_AR_DYN values (two-shot), 'push', 'oneshot' (2 vectors per thread), 'oneshot1', 'pushdyn[:chunk_kb]', 'll', 'll128', 'k4' (NCCL path) or 'auto'")
+                    help="CANNIKIN_AR_DYN values (two-shot), 'push', 'll', 'll128', 'k4' (NCCL path) or 'auto'")
     ap.add_argument("--sizes-mb", default="1,4,16,64,256,1024")
     ap.add_argument("--total", type=int, default=TOTAL)
     ap.add_argument("--nvls", action="store_true", help="also time the NVLS kernel (fp32)")
@@ -65,24 +65,20 @@ def main():
     r = b[rank] / sum(b)
     combos = [(int(g), v) for g in args.grids.split(",") for v in args.variants.split(",")]
     for grid, var in combos:
-        os.environ["CANNIKIN_AR_LL"] = "1" if var == "ll" else "0"
-        os.environ["CANNIKIN_AR_LL128"] = "1" if var == "ll128" else "0"
-        os.environ["CANNIKIN_AR_LL128OS"] = "1" if var == "ll128os" else "0"
+        knobs = ("CANNIKIN_AR_PUSH", "CANNIKIN_AR_DYN", "CANNIKIN_AR_LL", "CANNIKIN_AR_LL128")
         if var == "auto":
-            for k in ("CANNIKIN_AR_PUSH", "CANNIKIN_AR_DYN", "CANNIKIN_AR_ONESHOT", "CANNIKIN_AR_LL",
-                      "CANNIKIN_AR_LL128", "CANNIKIN_AR_LL128OS"):
+            for k in knobs:
                 os.environ.pop(k, None)
-        elif var in ("ll", "ll128", "ll128os", "k4"):
-            os.environ.update(CANNIKIN_AR_PUSH="0", CANNIKIN_AR_DYN="0", CANNIKIN_AR_ONESHOT="0")
-        elif var.startswith("pushdyn"):
-            os.environ["CANNIKIN_AR_PUSH"] = "2"
-            os.environ["CANNIKIN_AR_ONESHOT"] = "0"
-            os.environ["CANNIKIN_PD_CHUNK_KB"] = var.split(":")[1] if ":" in var else "256"
         else:
-            os.environ["CANNIKIN_AR_PUSH"] = "1" if var == "push" else "0"
-            os.environ["CANNIKIN_AR_ONESHOT"] = "1" if var.startswith("oneshot") else "0"
-            os.environ["CANNIKIN_OS_VPT"] = "1" if var == "oneshot1" else "2"
-            os.environ["CANNIKIN_AR_DYN"] = "0" if var == "push" or var.startswith("oneshot") else var
+            os.environ.update(dict.fromkeys(knobs, "0"))
+            if var == "ll":
+                os.environ["CANNIKIN_AR_LL"] = "1"
+            elif var == "ll128":
+                os.environ["CANNIKIN_AR_LL128"] = "1"
+            elif var == "push":
+                os.environ["CANNIKIN_AR_PUSH"] = "1"
+            elif var != "k4":
+                os.environ["CANNIKIN_AR_DYN"] = var
         ctx = ta.init_distributed_context(heap_bytes=N * s, grid=grid)
         bucket = ta.bucket_tensor(ctx, N, tdt)
         mcb = ta.McBucket(N, tdt) if args.nvls else None
