@@ -202,6 +202,23 @@ cannikin_status cannikin_weighted_allreduce_nvls(cannikin_ctx* ctx, void* bucket
 cannikin_status cannikin_gns_stats(cannikin_ctx* ctx, void* stream, double* out_local_sq,
                                    double* out_global_sq);
 
+/* Out-of-place statistics of ONE bucket (the north-star form gns_stats(bucket, b_i, ...) with a
+ * non-NULL bucket): the Eq. 10 inputs of this bucket alone,
+ *   out_local_sq[j] = |g_j|^2 for every rank j,  *out_global_sq = |g|^2,  g = sum_j (b_j/B) g_j,
+ * without modifying `bucket` and without touching the statistics the in-place reductions have
+ * accumulated (they stay pending for the next cannikin_gns_stats).
+ *   bucket : device pointer, n elements of dt, 16-byte aligned: this rank's mean gradient g_i
+ *   b_i    : this rank's local batch (>= 0); B = sum_j b_j is exchanged between the ranks and
+ *            r_j = b_j / B formed in double from the integers
+ * COLLECTIVE for world > 1 (NCCL all-gather of the b_j, then the same reduction kernels as
+ * cannikin_weighted_allreduce on a copy of the bucket).  Synchronises `stream`; a work buffer of
+ * ~n * sizeof(dt) is allocated on first use / growth (synchronises the device).  Identical bits on
+ * every rank.  Errors: INVALID, DOMAIN (b_i < 0 or B == 0), UNSUPPORTED (dtype; in-process group:
+ * no communicator), CUDA, NCCL. */
+cannikin_status cannikin_gns_stats_bucket(cannikin_ctx* ctx, const void* bucket, size_t n,
+                                          cannikin_dtype dt, int64_t b_i, void* stream,
+                                          double* out_local_sq, double* out_global_sq);
+
 /* Stream-ordered variant: one finalize kernel writes the (world+1) accumulated doubles
  * [local_sq..., global_sq] to d_out (device memory, or pinned host memory) and resets the
  * accumulator, without host synchronisation. */
@@ -385,8 +402,9 @@ cannikin_status cannikin_analyzer_plan(cannikin_analyzer* an, int64_t B, const i
 
 /* Exponential moving average of the aggregated G and S (separately: the ratio estimator is
  * biased).  Set decay in [0,1) and count = 0 before the first update.  A snapshot with
- * G2 <= 0 is skipped (reading Q26).  B_noise = trS / G2 of the average. */
-typedef struct { double G2, trS, decay; int count; } cannikin_gns_ema;
+ * G2 <= 0 is skipped (reading Q26).  Every update call sets B_noise = trS / G2 of the averages
+ * (P:364), or NaN while no snapshot has been accepted (count == 0). */
+typedef struct { double G2, trS, decay; int count; double B_noise; } cannikin_gns_ema;
 cannikin_status cannikin_gns_ema_update(cannikin_gns_ema* ema, double G2, double trS);
 
 /* Statistical efficiency of total batch B relative to the initial batch B0 for noise scale

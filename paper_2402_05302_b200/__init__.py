@@ -73,7 +73,7 @@ class _CommModel(ctypes.Structure):
 
 class _GnsEma(ctypes.Structure):
     _fields_ = [("G2", ctypes.c_double), ("trS", ctypes.c_double), ("decay", ctypes.c_double),
-                ("count", ctypes.c_int)]
+                ("count", ctypes.c_int), ("B_noise", ctypes.c_double)]
 
 
 _LIB = None
@@ -99,6 +99,7 @@ SIGNATURES = {
     "cannikin_weighted_allreduce_nccl": (_I, [_P, _P, _Z, _I, _D, _P]),
     "cannikin_gns_stats": (_I, [_P, _P, _DP, _DP]),
     "cannikin_gns_stats_async": (_I, [_P, _P, _P]),
+    "cannikin_gns_stats_bucket": (_I, [_P, _P, _Z, _I, _L, _P, _DP, _DP]),
     "cannikin_device_status": (_I, [_P]),
     "cannikin_weighted_sum_local": (_I, [_P, ctypes.POINTER(_P), _I, _DP, _P, _Z, _I, _P, _P, _U, _P]),
     "cannikin_ddp_allreduce_mean": (_I, [_P, _P, _Z, _I, _P]),
@@ -237,6 +238,15 @@ class Context:
         out = (ctypes.c_double * self.world)()
         g = ctypes.c_double()
         _check(lib().cannikin_gns_stats(self._h, _stream(stream), out, ctypes.byref(g)))
+        return list(out), g.value
+
+    def gns_stats_bucket(self, ptr: int, n: int, dtype: int, b_i: int, stream=None):
+        """Out-of-place statistics of one bucket (cannikin_gns_stats_bucket): (|g_j|^2 for every
+        rank j, |g|^2) with g = sum_j (b_j / B) g_j; the bucket is not modified.  Collective."""
+        out = (ctypes.c_double * self.world)()
+        g = ctypes.c_double()
+        _check(lib().cannikin_gns_stats_bucket(self._h, ptr, n, dtype, int(b_i), _stream(stream),
+                                               out, ctypes.byref(g)))
         return list(out), g.value
 
     def gns_stats_async(self, d_out: int, stream=None):
@@ -404,7 +414,7 @@ class GnsEma:
     """EMA of the aggregated G and S (separately), B_noise = S / G of the averages."""
 
     def __init__(self, decay: float = 0.9):
-        self._s = _GnsEma(0.0, 0.0, float(decay), 0)
+        self._s = _GnsEma(0.0, 0.0, float(decay), 0, float("nan"))
 
     def update(self, G2: float, trS: float):
         _check(lib().cannikin_gns_ema_update(ctypes.byref(self._s), float(G2), float(trS)))
@@ -415,7 +425,8 @@ class GnsEma:
 
     @property
     def B_noise(self) -> float:
-        return self._s.trS / self._s.G2 if self._s.count else float("nan")
+        """S / G of the averages, as cannikin_gns_ema_update last set it (NaN before any)."""
+        return self._s.B_noise
 
 
 def efficiency(B: int, B0: int, B_noise: float) -> float:
@@ -442,7 +453,7 @@ class ControlStep:
         self.n = len(b)
         self._b = _i64(b)
         self._nodes, self._cm = _models(nodes, comm)
-        self._ema = _GnsEma(0.0, 0.0, float(decay), 0)
+        self._ema = _GnsEma(0.0, 0.0, float(decay), 0, float("nan"))
         self._res = _GnsResult()
         self._bn = (ctypes.c_int64 * self.n)()
         self._t = ctypes.c_double()
@@ -463,4 +474,4 @@ class ControlStep:
         r = self._res
         return {"G2": r.G2, "trS": r.trS, "B_noise": r.B_noise, "wG": list(r.wG[:n]),
                 "wS": list(r.wS[:n]), "b_next": list(self._bn), "T_next": self._t.value,
-                "ema_B_noise": self._ema.trS / self._ema.G2 if self._ema.count else float("nan")}
+                "ema_B_noise": self._ema.B_noise}

@@ -10,6 +10,7 @@
 // Host-only, pure C++, -ffp-contract=off.
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <vector>
 
 #include "common.h"
@@ -306,15 +307,18 @@ extern "C" cannikin_status cannikin_gns_ema_update(cannikin_gns_ema* ema, double
   if (!ema || !(ema->decay >= 0.0) || !(ema->decay < 1.0))
     return fail(CANNIKIN_ERR_INVALID, "gns_ema_update: decay must be in [0, 1)");
   if (!std::isfinite(G2) || !std::isfinite(trS)) return fail(CANNIKIN_ERR_DOMAIN, "gns_ema_update: non-finite");
-  if (!(G2 > 0.0)) return CANNIKIN_OK;  // a non-positive G snapshot is left out (reading Q26)
-  if (ema->count == 0) {
-    ema->G2 = G2;
-    ema->trS = trS;
-  } else {
-    ema->G2 = ema->decay * ema->G2 + (1.0 - ema->decay) * G2;
-    ema->trS = ema->decay * ema->trS + (1.0 - ema->decay) * trS;
+  if (G2 > 0.0) {  // a non-positive G snapshot is left out (reading Q26)
+    if (ema->count == 0) {
+      ema->G2 = G2;
+      ema->trS = trS;
+    } else {
+      ema->G2 = ema->decay * ema->G2 + (1.0 - ema->decay) * G2;
+      ema->trS = ema->decay * ema->trS + (1.0 - ema->decay) * trS;
+    }
+    ema->count++;
   }
-  ema->count++;
+  // B_noise = S / G of the averages
+  ema->B_noise = ema->count ? ema->trS / ema->G2 : std::numeric_limits<double>::quiet_NaN();
   return CANNIKIN_OK;
 }
 

@@ -52,6 +52,7 @@ static cannikin_status destroy_partial(cannikin_ctx* ctx) {
   if (ctx->nccl_comm) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl_comm));
   if (ctx->base) cudaFree(ctx->base);
   if (ctx->k4_buf) cudaFree(ctx->k4_buf);
+  if (ctx->work_buf) cudaFree(ctx->work_buf);
   if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
   delete ctx;
   return CANNIKIN_OK;
@@ -431,6 +432,64 @@ extern "C" cannikin_status cannikin_gns_stats(cannikin_ctx* ctx, void* stream,
   for (int j = 0; j < W; ++j) out_local_sq[j] = ctx->h_stats[j];
   *out_global_sq = ctx->h_stats[W];
   return check_device_code(ctx, "gns_stats");
+}
+
+extern "C" cannikin_status cannikin_gns_stats_bucket(cannikin_ctx* ctx, const void* bucket, size_t n,
+                                                     cannikin_dtype dt, int64_t b_i, void* stream,
+                                                     double* out_local_sq, double* out_global_sq) {
+  if (!ctx || !out_local_sq || !out_global_sq)
+    return fail(CANNIKIN_ERR_INVALID, "gns_stats_bucket: NULL argument");
+  if (dt != CANNIKIN_F32 && dt != CANNIKIN_BF16)
+    return fail(CANNIKIN_ERR_UNSUPPORTED, "gns_stats_bucket: dtype %d", (int)dt);
+  if (n > 0 && !bucket) return fail(CANNIKIN_ERR_INVALID, "gns_stats_bucket: bucket == NULL");
+  if (reinterpret_cast<uintptr_t>(bucket) % 16)
+    return fail(CANNIKIN_ERR_INVALID, "gns_stats_bucket: bucket not 16-byte aligned");
+  if (b_i < 0) return fail(CANNIKIN_ERR_DOMAIN, "gns_stats_bucket: b_i = %lld < 0", (long long)b_i);
+  const int W = ctx->world;
+  if (W > 1 && !ctx->nccl_comm)
+    return fail(CANNIKIN_ERR_UNSUPPORTED, "gns_stats_bucket: no NCCL communicator (in-process group)");
+  CK_CUDA(cudaSetDevice(ctx->device));
+  const size_t bytes = n * elem_size(dt);
+  // work buffer: [bucket copy | W+1 held statistics | W int64 batch sizes]
+  const size_t copy_bytes = align_up(bytes, 256);
+  const size_t need = copy_bytes + 2 * 8 * (cannikin::kMaxWorld + 1);
+  if (need > ctx->work_bytes) {  // grow (synchronises the device: first use or a larger bucket)
+    CK_CUDA(cudaDeviceSynchronize());
+    if (ctx->work_buf) CK_CUDA(cudaFree(ctx->work_buf));
+    ctx->work_buf = nullptr;
+    ctx->work_bytes = 0;
+    CK_CUDA(cudaMalloc(&ctx->work_buf, need));
+    ctx->work_bytes = need;
+  }
+  double* hold = reinterpret_cast<double*>(ctx->work_buf + copy_bytes);
+  int64_t* d_b = reinterpret_cast<int64_t*>(hold + cannikin::kMaxWorld + 1);
+  // B = sum_j b_j over the ranks, in rank order (every rank forms the same r_j = b_j / B)
+  int64_t all_b[cannikin::kMaxWorld] = {b_i};
+  if (W > 1) {
+    CK_CUDA(cudaMemcpyAsync(d_b + ctx->rank, &b_i, sizeof b_i, cudaMemcpyHostToDevice, S(stream)));
+    CK_NCCL(ncclAllGather(d_b + ctx->rank, d_b, 1, ncclInt64, static_cast<ncclComm_t>(ctx->nccl_comm),
+                          S(stream)));
+    CK_CUDA(cudaMemcpyAsync(all_b, d_b, sizeof(int64_t) * W, cudaMemcpyDeviceToHost, S(stream)));
+    CK_CUDA(cudaStreamSynchronize(S(stream)));
+  }
+  int64_t B = 0;
+  for (int j = 0; j < W; ++j) B += all_b[j];
+  if (B <= 0) return fail(CANNIKIN_ERR_DOMAIN, "gns_stats_bucket: total batch B = %lld", (long long)B);
+  const double r_i = (double)b_i / (double)B;
+  // set the pending fused statistics aside, reduce a copy of the bucket (its statistics are then
+  // the only ones accumulated), read them, and put the fused ones back
+  CK_CUDA(cannikin::launch_stats_finalize(ctx, hold, S(stream)));
+  if (bytes) CK_CUDA(cudaMemcpyAsync(ctx->work_buf, bucket, bytes, cudaMemcpyDeviceToDevice, S(stream)));
+  {
+    const cannikin_status st = cannikin_weighted_allreduce(ctx, ctx->work_buf, n, dt, r_i, stream);
+    if (st != CANNIKIN_OK) return st;
+  }
+  CK_CUDA(cannikin::launch_stats_finalize(ctx, ctx->h_stats, S(stream)));
+  CK_CUDA(cannikin::launch_stats_add(ctx, hold, S(stream)));
+  CK_CUDA(cudaStreamSynchronize(S(stream)));
+  for (int j = 0; j < W; ++j) out_local_sq[j] = ctx->h_stats[j];
+  *out_global_sq = ctx->h_stats[W];
+  return check_device_code(ctx, "gns_stats_bucket");
 }
 
 extern "C" cannikin_status cannikin_gns_stats_async(cannikin_ctx* ctx, double* d_out, void* stream) {

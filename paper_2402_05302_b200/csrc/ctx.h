@@ -72,6 +72,8 @@ struct cannikin_ctx {
   void* nccl_comm = nullptr;  // ncclComm_t
   void* k4_buf = nullptr;     // NCCL-path (K4) work buffer, grown on demand
   size_t k4_bytes = 0;
+  char* work_buf = nullptr;   // cannikin_gns_stats_bucket: out-of-place copy + held statistics
+  size_t work_bytes = 0;
   bool in_process = false;    // cannikin_init_group_local: peers are this process's allocations
   std::map<size_t, size_t> free_blocks;  // offset -> size within the user heap
   std::map<size_t, size_t> used_blocks;

@@ -832,23 +832,42 @@ cudaError_t launch_twoshot_group(cannikin_ctx* const* ctxs, int W, size_t off, s
 }
 
 // Finalize the statistics of all calls since the last finalize: out[j] = stats[j] (dynamic / push
-// two-shot, NVLS, world 1) + sum over b of cta_acc[b][j] (static two-shot, LL, LL128) in ascending
-// b, then zero both.  One warp; `out` may be device or pinned host memory.
-__global__ void stats_finalize_kernel(Ctrl* c, int W, double* out) {
-  const int j = threadIdx.x;
-  if (j > W) return;
-  double t = c->stats[j];
-  c->stats[j] = 0.0;
-  double s = 0.0;
-  for (int b = 0; b < kMaxArBlocks; ++b) {
-    s += c->cta_acc[b][j];
-    c->cta_acc[b][j] = 0.0;
+// two-shot, NVLS, world 1) + the sum over b of cta_acc[b][j] (static two-shot, LL, LL128), then
+// zero both.  One thread per row b; the rows are summed by the fixed-order block reduction
+// (butterfly within warps, warps in order), so every rank forms the same bits.  `out` may be
+// device or pinned host memory.
+__global__ void __launch_bounds__(kMaxArBlocks) stats_finalize_kernel(Ctrl* c, int W, double* out) {
+  __shared__ double red[32 * (kMaxWorld + 1)];
+  const int b = threadIdx.x;
+  double v[kMaxWorld + 1];
+#pragma unroll
+  for (int j = 0; j <= kMaxWorld; ++j) {
+    v[j] = (j <= W) ? __ldcg(&c->cta_acc[b][j]) : 0.0;
+    if (j <= W) c->cta_acc[b][j] = 0.0;
   }
-  out[j] = t + s;
+  dev::block_sum(v, red);
+  if (b == 0) {
+    for (int j = 0; j <= W; ++j) {
+      out[j] = c->stats[j] + v[j];
+      c->stats[j] = 0.0;
+    }
+  }
 }
 
 cudaError_t launch_stats_finalize(cannikin_ctx* ctx, double* out, cudaStream_t st) {
-  stats_finalize_kernel<<<1, 32, 0, st>>>(ctx->ctrl, ctx->world, out);
+  stats_finalize_kernel<<<1, kMaxArBlocks, 0, st>>>(ctx->ctrl, ctx->world, out);
+  return cudaGetLastError();
+}
+
+// Add W+1 held statistics back into the accumulator (cannikin_gns_stats_bucket keeps the fused
+// statistics pending across its own out-of-place reduction).
+__global__ void stats_add_kernel(Ctrl* c, int W, const double* in) {
+  const int j = threadIdx.x;
+  if (j <= W) c->stats[j] += in[j];
+}
+
+cudaError_t launch_stats_add(cannikin_ctx* ctx, const double* in, cudaStream_t st) {
+  stats_add_kernel<<<1, 32, 0, st>>>(ctx->ctrl, ctx->world, in);
   return cudaGetLastError();
 }
 

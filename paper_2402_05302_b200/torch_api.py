@@ -52,6 +52,13 @@ def weighted_allreduce(ctx: Context, bucket: torch.Tensor, r_i: float, stream=No
                            _cur(stream))
 
 
+def gns_stats_bucket(ctx: Context, bucket: torch.Tensor, b_i: int, stream=None):
+    """Out-of-place Eq. 10 inputs of one bucket (bucket unchanged): ([|g_j|^2], |g|^2)."""
+    assert bucket.is_cuda and bucket.is_contiguous()
+    return ctx.gns_stats_bucket(bucket.data_ptr(), bucket.numel(), dtype_code(bucket.dtype), b_i,
+                                _cur(stream))
+
+
 def weighted_allreduce_group(ctxs, buckets, r, stream=None):
     """Every rank of an in-process group (Context.group_local) in ONE kernel launch: buckets[k]
     <- sum_j r[j] buckets[j] (Eq. 9), norms accumulated in every rank's ctx."""

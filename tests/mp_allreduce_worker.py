@@ -181,6 +181,13 @@ def main():
         bucket = ta.bucket_tensor(ctx, N, tdt[dtype])
         bucket.copy_(to_dev(gs[rank], dtype))
         AR(ctx, bucket, b[rank] / B)
+        # (5) out-of-place statistics of the unreduced gradient (cannikin_gns_stats_bucket), while
+        # (1)'s fused statistics are pending: the bucket is not modified and (1)'s are kept
+        src = to_dev(gs[rank], dtype)
+        loc5, glob5 = ta.gns_stats_bucket(ctx, src, b[rank])
+        same5 = bool(torch.equal(src.view(torch.int16) if dtype == "bf16" else src,
+                                 to_dev(gs[rank], dtype).view(torch.int16) if dtype == "bf16"
+                                 else to_dev(gs[rank], dtype)))
         loc, glob = ctx.gns_stats()
         out1 = from_dev(bucket, dtype)
         # (2) again (determinism, flag epochs advance)
@@ -204,7 +211,7 @@ def main():
         np.savez(os.path.join(args.out, f"rank{rank}_{name}.npz"), out1=out1, out2=out2,
                  out3=out3, out4=out4, loc=np.array(loc), glob=glob, loc2=np.array(loc2),
                  glob2=glob2, loc3=np.array(loc3), glob3=glob3, loc4=np.array(loc4), glob4=glob4,
-                 b=np.array(b))
+                 loc5=np.array(loc5), glob5=glob5, same5=same5, b=np.array(b))
     # guard bands: buckets A | B | C adjacent in the heap; reducing B (ragged) must not touch A, C
     for N in (1, 7, 4099, (1 << 20) + 3):
         for dtype in ("f32", "bf16"):

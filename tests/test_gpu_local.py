@@ -188,6 +188,30 @@ def test_world1_allreduce_and_stats(ctx):
     assert ctx.gns_stats() == ([0.0], 0.0)   # reset after read
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_gns_stats_bucket_out_of_place(ctx, dtype):
+    """cannikin_gns_stats_bucket (world 1): |g_0|^2 and |g|^2 = |r_0 g_0|^2 with r_0 = b_0/B = 1 of
+    an unreduced bucket against the oracle, the bucket unchanged, and the statistics of an earlier
+    in-place reduction still pending for gns_stats."""
+    N = (3 << 20) + 5
+    g = synth.device_gns_gradients(1, N, [12], seed=41, dtype=dtype)[0]
+    h = synth.device_gns_gradients(1, N, [12], seed=42, dtype=dtype)[0]
+    ref_g = parity.host_bits(g, dtype)
+    t = h.clone()
+    ta.weighted_allreduce(ctx, t, 1.0)             # fused statistics of h, pending
+    loc, glob = ta.gns_stats_bucket(ctx, g, 12)    # out of place, of g
+    assert np.array_equal(parity.host_bits(g, dtype), ref_g)
+    x = agg.to_f64(ref_g, dtype)
+    want = agg.sq_norm(x)
+    assert abs(loc[0] - want) <= 1e-4 * want and abs(glob - want) <= 1e-4 * want
+    loc_h, glob_h = ctx.gns_stats()
+    want_h = agg.sq_norm(agg.to_f64(parity.host_bits(h, dtype), dtype))
+    assert abs(loc_h[0] - want_h) <= 1e-4 * want_h and abs(glob_h - want_h) <= 1e-4 * want_h
+    with pytest.raises(ck.CannikinError) as e:
+        ta.gns_stats_bucket(ctx, g, -1)
+    assert e.value.name == "DOMAIN"
+
+
 def test_errors(ctx):
     x = torch.zeros(1024, device="cuda")
     loc = torch.zeros(17, dtype=torch.float64, device="cuda")

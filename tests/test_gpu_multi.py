@@ -78,7 +78,7 @@ def test_parity_and_identity(results, case):
             assert np.array_equal(ranks[q][k], ranks[0][k]), (k, q)
     # the two zero-copy runs are bitwise identical (determinism)
     assert np.array_equal(ranks[0]["out1"], ranks[0]["out2"])
-    for sfx in ("", "2", "3", "4"):
+    for sfx in ("", "2", "3", "4", "5"):  # 5: out-of-place cannikin_gns_stats_bucket
         loc, glob = ranks[0]["loc" + sfx], float(ranks[0]["glob" + sfx])
         assert np.allclose(loc, ls_ref, rtol=1e-4, atol=0), (sfx, loc, ls_ref)
         assert abs(glob - gsq_ref) <= 1e-4 * max(gsq_ref, 1e-300), (sfx, glob, gsq_ref)
@@ -87,6 +87,7 @@ def test_parity_and_identity(results, case):
             assert float(ranks[q]["glob" + sfx]) == glob
     assert np.array_equal(ranks[0]["loc"], ranks[0]["loc2"])
     assert float(ranks[0]["glob"]) == float(ranks[0]["glob2"])
+    assert all(bool(ranks[q]["same5"]) for q in range(world))  # out-of-place: bucket unchanged
 
 
 def test_ddp_baseline_mean(results):

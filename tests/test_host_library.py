@@ -10,6 +10,7 @@ import pytest
 
 import cannikin_synth as synth
 import paper_2402_05302_b200 as ck
+from oracle import goodput as ogp
 from oracle import gns as ogns
 from oracle import optsplit as osp
 
@@ -289,5 +290,9 @@ def test_control_step_matches_parts():
         e = ck.gns_estimate(lsq, gsq, b)
         assert r["G2"] == e["G2"] and r["trS"] == e["trS"] and r["wS"] == e["wS"]
         assert r["b_next"] == ck.opt_split(nodes, comm, Bn)["b"]
+        oe = ogp.Ema(0.9)  # the oracle's EMA (reading Q26) of the same snapshot
+        oe.update(e["G2"], e["trS"])
         if e["G2"] > 0:
-            assert math.isclose(r["ema_B_noise"], e["trS"] / e["G2"], rel_tol=1e-15)
+            assert r["ema_B_noise"] == oe.B_noise
+        else:
+            assert math.isnan(r["ema_B_noise"]) and oe.count == 0

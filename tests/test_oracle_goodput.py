@@ -45,10 +45,28 @@ def test_ema_separately_not_ratio():
     assert e.B_noise == 100.0 / 2.0                 # not mean(100, 33.3)
     e.update(-1.0, 5.0)                             # non-positive G skipped (reading Q26)
     assert e.count == 2
-    le = ck.GnsEma(0.5)
-    for G, S in [(1.0, 100.0), (3.0, 100.0), (-1.0, 5.0)]:
+    # the worked example above by hand: G = 0.5*1 + 0.5*3 = 2, S = 100 -> 50
+    assert e.G2 == 2.0 and e.trS == 100.0
+
+
+@pytest.mark.parametrize("decay", [0.0, 0.5, 0.9, 0.99])
+def test_library_ema_matches_oracle(decay):
+    """cannikin_gns_ema_update (library, which also sets B_noise) against the oracle's Ema over a
+    seeded sequence of snapshots with non-positive G's mixed in: the same averages, count and
+    B_noise = S / G of the averages (reading Q26); NaN before the first accepted one."""
+    rng = np.random.default_rng(int(decay * 100))
+    le, oe = ck.GnsEma(decay), ogp.Ema(decay)
+    assert math.isnan(le.B_noise) and le.count == 0
+    le.update(-1.0, 3.0)
+    assert math.isnan(le.B_noise) and le.count == 0  # skipped snapshot: still none
+    for _ in range(200):
+        G = float(rng.normal(1.0, 0.7))
+        S = float(rng.uniform(10.0, 500.0))
         le.update(G, S)
-    assert le.count == 2 and le.B_noise == e.B_noise
+        oe.update(G, S)
+        assert le.count == oe.count
+        if oe.count:
+            assert le.B_noise == oe.B_noise
 
 
 @pytest.mark.parametrize("seed", range(5))
