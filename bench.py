@@ -5,10 +5,12 @@ A *step* is one pass of the whole hot path over one batch of synthetic gradients
   weighted aggregation g = sum_i r_i g_i with the fused norms |g_i|^2, |g|^2   (Eq. 9-10)
   -> read the norm statistics -> heterogeneous GNS estimate (Theorem 1)
   -> OptPerf split for the next step (opt_split).
-N = 1 : the ranks are emulated on one GPU (K2, `cannikin_weighted_sum_local`); metric bytes are
-        the kernel's HBM algorithmic bytes (n+1) N s.
-N > 1 : one process per GPU (torchrun); `cannikin_weighted_allreduce` (K3, NVLink two-shot);
-        metric bytes are the NVLink bus bytes of the whole job, n * 2(n-1)/n * N s.
+N = 1 : the ranks are emulated on one GPU (K2, `cannikin_weighted_sum_local`); with --bucket-mb
+        the gradient is cut into buckets whose K2 launches are PDL-chained.
+N > 1 : one process per GPU (torchrun); `cannikin_weighted_allreduce` (K3 variants over NVLink).
+value : gradient bytes aggregated per second, n x N x s per step (n ranks, emulated at N = 1) --
+        the same quantity at every N.  The roofline object uses each bound's own bytes: K2's HBM
+        bytes (n+1) N s at N = 1, the bus bytes 2(n-1)/n N s per rank at N > 1.
 
     python bench.py [--gpus N --steps K --warmup W --config c4 --impl {cannikin,reference}]
 """
@@ -58,9 +60,10 @@ def node_models(n):
 
 
 def hetero_models(n):
-    """Per-node (q, s, k, m) in seconds for the step-time comparison: an A100-class node spends
-    0.04 ms/sample forward and 0.08 ms/sample backward (+0.3 / 0.2 ms fixed); slower nodes scale
-    the per-sample terms by Table 1's TFLOPS ratio."""
+    """Per-node (q, s, k, m) in seconds for the emulated-compute tools (tools/optperf_loop.py,
+    tools/adaptive_batch.py): an A100-class node spends 0.04 ms/sample forward and 0.08 ms/sample
+    backward (+0.3 / 0.2 ms fixed); slower nodes scale the per-sample terms by Table 1's TFLOPS
+    ratio (P:97-99)."""
     out = []
     for i in range(n):
         f = TFLOPS["A100"] / TFLOPS[MIX[i % len(MIX)]]
@@ -68,99 +71,127 @@ def hetero_models(n):
     return out
 
 
-def hetero_step_compare(ctx, bucket, N, s, rank, world, B, steps, dist, ta, ck, torch):
-    """Step time of Cannikin (opt_split b_i + the fused weighted all-reduce, K3) against
-    equal-split DDP (b_i = B/n + NCCL average) on ranks made heterogeneous by emulated compute
-    (K7, the Eq. 3 model of each rank).  Backprop is split into NB chunks; bucket j is reduced on a
-    comm stream as soon as chunk j is done (the bucketed overlap of §3.2.3), so
-    gamma = 1/NB.  T_o and T_u are measured from the comm kernels themselves."""
-    NB = 9
-    be = (N // NB) - (N // NB) % 8
-    cuts = [i * be for i in range(NB)] + [N]
-    cs = torch.cuda.current_stream()
+# Compute-rate caps for the step-time comparison (north_star: "per-rank compute-rate caps (...
+# SM-partitioned contexts)"): rank i runs its compute on a CUDA green context holding this many of
+# the 148 SMs -- 148 x Table 1's FP16 TFLOPS ratio A100 : V100 : P100, rounded.
+SM_CAPS = {"A100": 148, "V100": 60, "P100": 40}
+
+
+def hetero_sm_compare(N, s, tdt, rank, world, local_rank, B, iters, dist, ta, ck, torch):
+    """Step time of Cannikin against equal-split DDP on ranks made heterogeneous by REAL compute
+    under SM caps (green contexts, SM_CAPS by the cyclic A100/V100/P100 mix), not by injected
+    delays.  The compute is a synthetic layer stack of bf16 GEMMs (each sample = T tokens of width
+    H; forward NB GEMMs, backward NB chunks of two GEMMs), so its time is linear in b_i at a rate
+    the SM cap sets.  Bucket j of the C4 gradient (NB buckets) is reduced on a comm stream as soon
+    as backward chunk j is done (§3.2.3 overlap).  Cannikin: the measured-model loop --
+    epoch 0 even split, epoch 1 Eq. 8, epoch 2 OptPerf from the models the analyzer LEARNED from
+    per-rank CUDA-event timings (a_i, P_i, gamma_i, T_o, T_u) -- with the fused weighted
+    all-reduce.  DDP: b_i = B/n with the NCCL average.  The prediction error compares the
+    analyzer's Eq. 7 prediction with the measured step.  Max over ranks throughout."""
+    from torch.cuda.green_contexts import GreenContext
+
+    NB, T, H = 9, 512, 2048
+    gpu = MIX[rank % len(MIX)]
+    gctx = GreenContext.create(SM_CAPS[gpu], local_rank)
+    cs = gctx.Stream()
     ms = torch.cuda.Stream()
-    models = hetero_models(world)
-
-    def time_comm(op, reps=10):
-        for _ in range(2):
-            for j in range(NB):
-                op(j)
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(ms):
-            e0.record(ms)
-            for _ in range(reps):
-                for j in range(NB):
-                    op(j)
-            e1.record(ms)
-        torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / reps / NB * 1e-3], device="cuda",
-                         dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
+    # reductions overlap a peer's compute: a small grid leaves the SMs to the backward pass
+    ctx = ta.init_distributed_context(heap_bytes=N * s, grid=24)
+    bucket = ta.bucket_tensor(ctx, N, tdt)
+    bucket.normal_()
+    cuts = [j * (N // NB - (N // NB) % 8) for j in range(NB)] + [N]
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    Wt = [torch.randn(H, H, device="cuda", dtype=torch.bfloat16, generator=gen) * 0.02
+          for _ in range(NB)]
+    acts = [torch.randn(B * T, H, device="cuda", dtype=torch.bfloat16, generator=gen) * 0.1
+            for _ in range(NB + 1)]
+    dx = torch.empty(B * T, H, device="cuda", dtype=torch.bfloat16)
+    dw = [torch.empty(H, H, device="cuda", dtype=torch.bfloat16) for _ in range(NB)]
     stats = torch.zeros(world + 1, dtype=torch.float64, device="cuda")
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    ev = [(E(), E(), E()) for _ in range(NB)]  # (chunk done, comm start, comm end)
 
-    def ours_op(j, r):
-        ta.weighted_allreduce(ctx, bucket[cuts[j]:cuts[j + 1]], r, stream=ms)
-
-    def ddp_op(j):
-        ta.ddp_allreduce_mean(ctx, bucket[cuts[j]:cuts[j + 1]], stream=ms)
-
-    t_ours = time_comm(lambda j: ours_op(j, 1.0 / world))
-    ctx.gns_stats(ms)
-    t_nccl = time_comm(ddp_op)
-    comm_ours = (1.0 / NB, (NB - 1) * t_ours, t_ours)
-    comm_nccl = (1.0 / NB, (NB - 1) * t_nccl, t_nccl)
-    sp = ck.opt_split(models, comm_ours, B)
-    b_c = sp["b"]
-    b_d = [B // world + (1 if i < B % world else 0) for i in range(world)]
-    pred_ddp = max(ck.node_time(models[i], comm_nccl, b_d[i]) for i in range(world))
-    evs = [torch.cuda.Event() for _ in range(NB)]
-
-    def step(b_i, op):
-        q, s0, k, m = models[rank]
-        ck.emulate_compute(q * b_i + s0, cs)
-        for j in range(NB):
-            ck.emulate_compute((k * b_i + m) / NB, cs)
-            evs[j].record(cs)
-            ms.wait_event(evs[j])
-            op(j)
-        cs.wait_stream(ms)
-
-    def run(b_vec, op, with_stats):
-        for _ in range(3):
-            step(b_vec[rank], op)
-            if with_stats:
+    def step(b_i, r_i, ours):
+        M = b_i * T
+        e0, e1, e2, e3 = E(), E(), E(), E()
+        with torch.cuda.stream(cs):
+            e0.record(cs)
+            for l in range(NB):
+                torch.matmul(acts[l][:M], Wt[l], out=acts[l + 1][:M])
+            e1.record(cs)
+            for j in range(NB):
+                l = NB - 1 - j
+                torch.matmul(acts[l + 1][:M], Wt[l].t(), out=dx[:M])
+                torch.matmul(acts[l][:M].t(), acts[l + 1][:M], out=dw[l])
+                ev[j][0].record(cs)
+                ms.wait_event(ev[j][0])
+                with torch.cuda.stream(ms):
+                    ev[j][1].record(ms)
+                    if ours:
+                        ta.weighted_allreduce(ctx, bucket[cuts[j]:cuts[j + 1]], r_i, stream=ms)
+                    else:
+                        ta.ddp_allreduce_mean(ctx, bucket[cuts[j]:cuts[j + 1]], stream=ms)
+                    ev[j][2].record(ms)
+            e2.record(cs)
+            cs.wait_stream(ms)
+            if ours:
                 ctx.gns_stats_async(stats.data_ptr(), cs)
+            e3.record(cs)
         torch.cuda.synchronize()
-        dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(cs)
-        for _ in range(steps):
-            step(b_vec[rank], op)
-            if with_stats:
-                ctx.gns_stats_async(stats.data_ptr(), cs)
-        e1.record(cs)
-        torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / steps], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        a_t = e0.elapsed_time(e1) * 1e-3
+        P_t = e1.elapsed_time(e2) * 1e-3
+        gam = e1.elapsed_time(ev[0][0]) * 1e-3 / P_t
+        t_o = sum(ev[j][1].elapsed_time(ev[j][2]) for j in range(NB - 1)) * 1e-3
+        t_u = ev[NB - 1][1].elapsed_time(ev[NB - 1][2]) * 1e-3
+        return [a_t, P_t, min(max(gam, 0.0), 0.99), t_o, t_u, e0.elapsed_time(e3)]
 
-    Bsum = sum(b_c)
-    ms_c = run(b_c, lambda j: ours_op(j, b_c[rank] / Bsum), True)
-    ms_d = run(b_d, ddp_op, False)
-    return {"cannikin_ms": round(ms_c, 4), "ddp_ms": round(ms_d, 4),
-            "saving": round(1.0 - ms_c / ms_d, 4),
-            "predicted_cannikin_ms": round(sp["T_int"] * 1e3, 4),
-            "predicted_ddp_ms": round(pred_ddp * 1e3, 4),
-            "prediction_error": round(abs(sp["T_int"] * 1e3 - ms_c) / ms_c, 4),
-            "b_cannikin": b_c, "b_ddp": b_d, "buckets": NB,
-            "bucket_comm_ms": {"cannikin_k3": round(t_ours * 1e3, 4), "nccl": round(t_nccl * 1e3, 4)},
-            "mix": [MIX[i % len(MIX)] for i in range(world)],
-            "note": "compute emulated per rank from the Eq. 3 model (K7); comm kernels real; "
-                    "gamma = 1/buckets; max over ranks"}
+    def run(b_vec, ours, count, an=None, gid0=0):
+        steps = []
+        for it in range(count + 2):
+            dist.barrier()
+            mine = step(b_vec[rank], b_vec[rank] / sum(b_vec), ours)
+            allv = [None] * world
+            dist.all_gather_object(allv, mine)  # plumbing: every rank's timings, off the clock
+            if it < 2:
+                continue
+            if an is not None:
+                for node in range(world):
+                    an.observe(node, gid0 + it, b_vec[node], *allv[node][:5])
+            steps.append(max(v[5] for v in allv))
+        return statistics.median(steps)
+
+    b_eq = [B // world + (1 if i < B % world else 0) for i in range(world)]
+    ddp_ms = run(b_eq, False, iters)
+    an = ck.Analyzer(world)
+    epochs = []
+    for ep in range(3):
+        plan = an.plan(B)
+        meas = run(plan["b"], True, iters, an, 100 * ep)
+        epochs.append({"epoch": ep, "phase": plan["phase"], "b": plan["b"],
+                       "measured_ms": round(meas, 4),
+                       "predicted_ms": None if plan["T_pred"] != plan["T_pred"]
+                       else round(plan["T_pred"] * 1e3, 4)})
+    nodes, comm = an.models()
+    last = epochs[-1]
+    out = {"cannikin_ms": last["measured_ms"], "ddp_ms": round(ddp_ms, 4),
+           "saving": round(1.0 - last["measured_ms"] / ddp_ms, 4),
+           "predicted_cannikin_ms": last["predicted_ms"],
+           "prediction_error": (None if last["predicted_ms"] is None else
+                                round(abs(last["predicted_ms"] - last["measured_ms"])
+                                      / last["measured_ms"], 4)),
+           "b_cannikin": last["b"], "b_ddp": b_eq, "epochs": epochs, "buckets": NB,
+           "mix": [MIX[i % len(MIX)] for i in range(world)],
+           "sm_caps": [SM_CAPS[MIX[i % len(MIX)]] for i in range(world)],
+           "learned_ms_per_sample": [round((q + k) * 1e3, 4) for q, _, k, _ in nodes],
+           "learned_comm": {"gamma": round(comm[0], 4), "t_o_ms": round(comm[1] * 1e3, 4),
+                            "t_u_ms": round(comm[2] * 1e3, 4)},
+           "compute": f"bf16 GEMM stack, {T} tokens x {H} wide per sample, {NB} layers",
+           "note": "heterogeneity = real compute on SM-capped green contexts; split from models "
+                   "learned from measured timings (not from the generator); comm kernels real; "
+                   "median step of the last epoch, max over ranks"}
+    ta.free_bucket_tensor(ctx, bucket)
+    ctx.close()
+    return out
 
 
 def nvls_sidecar(ctx, N, rank, world, r_i, steps, dist, ta, torch):
@@ -339,7 +370,7 @@ def cpu_baseline(cfg, n, seconds=10.0, sample_elems=1 << 22):
         el = time.perf_counter() - t0
         if el >= seconds:
             break
-    nbytes = (n + 1) * sample_elems * esize(cfg["dtype"])
+    nbytes = n * sample_elems * esize(cfg["dtype"])  # the metric: gradient bytes aggregated
     out = {"value": round(nbytes * calls / el / 1e9, 4), "unit": "GB/s", "cores": 1,
            "kind": "oracle",
            "sample": f"{calls} oracle passes over {n} ranks x {sample_elems} {cfg['dtype']} "
@@ -380,7 +411,7 @@ def cpu_baseline_all_cores(cfg, n, gs, r, seconds=5.0, chunk=1 << 18):
     except Exception as e:  # noqa: BLE001
         return {"error": str(e)[:200]}
     es = esize(cfg["dtype"])
-    gbps = sum((n + 1) * len(j[0][0]) * es * c / el for j, (c, el) in zip(jobs, res)) / 1e9
+    gbps = sum(n * len(j[0][0]) * es * c / el for j, (c, el) in zip(jobs, res)) / 1e9
     return {"value": round(gbps, 3), "unit": "GB/s", "cores": cores, "kind": "oracle",
             "sample": f"{cores} processes, each the oracle's Eq. 9 + norms over a fixed "
                       f"{chunk}-element chunk of the same {n}-rank sample for {seconds:.0f} s"}
@@ -400,7 +431,7 @@ def run_reference(args, cfg, rank, world):
     for _ in range(args.steps):
         oracle_step(gs, r, cfg["dtype"], b, models, cfg["B"])
     el = time.perf_counter() - t0
-    nbytes = (n + 1) * sample * esize(cfg["dtype"])
+    nbytes = n * sample * esize(cfg["dtype"])  # the metric: gradient bytes aggregated
     val = nbytes * args.steps / el / 1e9
     line = {"impl": "reference", "metric": "weighted-allreduce+GNS GB/s (% HBM/NVLink roofline)", "value": round(val, 4),
             "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -444,6 +475,8 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    # a bench must end: a peer wait longer than 2 min reports a protocol error instead of hanging
+    os.environ.setdefault("CANNIKIN_SPIN_TIMEOUT_MS", "120000")
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
 
@@ -490,14 +523,16 @@ def main():
         ctx = ck.Context(world=1, device=local_rank)
         gs = synth.device_gns_gradients(n, N, b, seed=0, dtype=cfg["dtype"])
         out = torch.empty(N, dtype=tdt, device="cuda")
-        step_bytes = (n + 1) * N * s
+        alg_bytes = (n + 1) * N * s  # K2's HBM algorithmic bytes (roofline)
 
         def launch(bi, k):
             a, c = cuts[bi], cuts[bi + 1]
             # the last CTA writes the n+1 statistics straight into pinned host memory (mapped,
             # device-accessible): no separate readback copy in the step
+            # buckets after the first are PDL-chained (CANNIKIN_LOCAL_CHAIN): their loads start
+            # while the previous bucket's last CTAs finish
             ta.weighted_sum_local(ctx, [g[a:c] for g in gs], r, out[a:c], stats_h[k][:n],
-                                  stats_h[k][n:], accumulate=bi > 0)
+                                  stats_h[k][n:], accumulate=bi > 0, chain=bi > 0)
 
         def read_stats(k):
             pass
@@ -507,7 +542,7 @@ def main():
         g0 = synth.device_gns_gradients(n, N, b, seed=0, dtype=cfg["dtype"], ranks=[rank])[0]
         bucket.copy_(g0)
         del g0
-        step_bytes = n * 2 * (n - 1) * N * s // n  # whole-job NVLink bus bytes
+        alg_bytes = 2 * (n - 1) * N * s  # whole-job NVLink bus bytes, n x 2(n-1)/n N s
 
         def launch(bi, k):
             a, c = cuts[bi], cuts[bi + 1]
@@ -521,11 +556,21 @@ def main():
              torch.cuda.Event(enable_timing=True, external=True)) for _ in range(nb)]
            for _ in range(NBUF)]
 
+    # N = 1 with several buckets: consecutive K2 launches overlap (PDL), so they are timed as one
+    # chain (first start to last end) and a launch's duration is the chain's / nb
+    chain_timing = world == 1 and nb > 1
+
     def device_part(k):
-        for bi in range(nb):
-            evs[k][bi][0].record()
-            launch(bi, k)
-            evs[k][bi][1].record()
+        if chain_timing:
+            evs[k][0][0].record()
+            for bi in range(nb):
+                launch(bi, k)
+            evs[k][0][1].record()
+        else:
+            for bi in range(nb):
+                evs[k][bi][0].record()
+                launch(bi, k)
+                evs[k][bi][1].record()
         read_stats(k)
 
     kernel_ms = []
@@ -537,7 +582,11 @@ def main():
         ready[k].synchronize()
         control(stats_h[k].data_ptr())
         if record:
-            kernel_ms.extend(a.elapsed_time(c) for a, c in evs[k])
+            if chain_timing:
+                a, c = evs[k][0]
+                kernel_ms.extend([a.elapsed_time(c) / nb] * nb)
+            else:
+                kernel_ms.extend(a.elapsed_time(c) for a, c in evs[k])
 
     graphs = None
     for k in range(NBUF):
@@ -598,23 +647,31 @@ def main():
     kdist = {"p10": round(kq[0], 4), "p50": round(statistics.median(kernel_ms), 4),
              "p90": round(kq[8], 4), "launches": len(kernel_ms), "rank": rank}
     ms_step = ms / args.steps
-    value = step_bytes / (ms_step * 1e-3) / 1e9
+    # value: gradient bytes aggregated per second, n x N x s per step (n = emulated ranks at N = 1,
+    # GPUs at N > 1) -- the same quantity at every N; the roofline below uses each bound's bytes
+    grad_bytes = n * N * s
+    value = grad_bytes / (ms_step * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel (per launch)
-    launch_bytes = step_bytes / launches_per_step()
+    launch_bytes = alg_bytes / launches_per_step()
     if world == 1:
         achieved = launch_bytes / (kmean * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
-                "peak_kind": peak_kind, "kernel": "wsum_local_kernel (K2)",
+                "peak_kind": peak_kind,
+                "kernel": ("wsum_local_kernel (K2)" if nb == 1 else
+                           f"wsum_local_kernel (K2), {nb} PDL-chained bucket launches per step, "
+                           "timed as one chain: kernel_ms = chain / launches"),
                 "kernel_ms": round(kmean, 4), "kernel_ms_dist": kdist,
                 "traffic": ncu_traffic(f"{args.config}_n{n}_{cfg['dtype']}_b{launches_per_step()}")}
     else:
         busbw = (N * s / len(cuts[:-1])) / (kmean * 1e-3) * 2 * (n - 1) / n / 1e9
         roof = {"bound": "nvlink", "achieved": round(busbw, 1), "peak": 770.0, "unit": "GB/s",
                 "frac": round(busbw / 770.0, 4),
-                "peak_kind": "measured peer copy per GPU per direction (B200_PROFILING.md); 900 nominal",
-                "kernel": "K3 two-shot (pull / dynamic / push variant by size)",
+                "peak_kind": "measured peer copy per GPU per direction (B200_PROFILING.md)",
+                "nominal": {"peak": 900.0, "frac": round(busbw / 900.0, 4),
+                            "kind": "NVLink 5 nominal per GPU per direction (north_star)"},
+                "kernel": f"K3 {ctx.last_variant()} (variant chosen by size)",
                 "kernel_ms": round(kmean, 4), "kernel_ms_dist": kdist,
                 "traffic": ncu_traffic(f"{args.config}_w{n}_{cfg['dtype']}"),
                 # an all-reduce loads BOTH directions at once; the same SM-driven copy with both
@@ -658,8 +715,11 @@ def main():
 
     hetero = None
     if world > 1 and not args.no_hetero:
-        hetero = hetero_step_compare(ctx, bucket, N, s, rank, world, max(B, world), args.steps,
-                                     dist, ta, ck, torch)
+        try:
+            hetero = hetero_sm_compare(N, s, tdt, rank, world, local_rank, max(B, world), 6, dist,
+                                       ta, ck, torch)
+        except Exception as e:  # green contexts unavailable: report, do not sink the bench line
+            hetero = {"unavailable": str(e)[:300]}
 
     # ---- end to end through the public API with host buffers
     e2e = None
@@ -703,7 +763,7 @@ def main():
         if dist is not None:
             dist.all_reduce(em, op=dist.ReduceOp.MAX)
         em = float(em.item())
-        e2e = {"value": round(step_bytes / (em * 1e-3) / 1e9, 3), "unit": "GB/s",
+        e2e = {"value": round(grad_bytes / (em * 1e-3) / 1e9, 3), "unit": "GB/s",
                "ms_per_step": round(em, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "steps": ek}
 
@@ -720,10 +780,14 @@ def main():
             "config": {"workload": cfg["workload"], "elements": N, "ranks": n,
                        "emulated": world == 1, "b": b, "B": B,
                        "buckets_per_step": launches_per_step(),
-                       "bytes_per_step": step_bytes,
-                       "bytes_model": "(n+1)*N*s HBM" if world == 1 else "n*2(n-1)/n*N*s NVLink",
-                       "l2": (f"inputs larger than L2 ({step_bytes / 126e6:.1f}x 126 MB), no flush"
-                              if step_bytes > 2 * 126e6 else
+                       "value_model": "gradient bytes aggregated per second: n*N*s per step "
+                                      "(n ranks, emulated at N=1), the same quantity at every N",
+                       "grad_bytes_per_step": grad_bytes,
+                       "roofline_bytes_per_step": alg_bytes,
+                       "roofline_bytes_model": ("(n+1)*N*s HBM (K2)" if world == 1 else
+                                                "n*2(n-1)/n*N*s NVLink bus bytes (K3)"),
+                       "l2": (f"inputs larger than L2 ({alg_bytes / 126e6:.1f}x 126 MB), no flush"
+                              if alg_bytes > 2 * 126e6 else
                               "working set fits in L2 (not flushed): latency-bound case, "
                               "not a roofline claim"),
                        "cuda_graph": graphs is not None,

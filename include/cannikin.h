@@ -86,6 +86,12 @@ cannikin_status cannikin_get_unique_id(void* out_id);
  *   and must lie within 2^-23 of 1.  A violation does not stop the reduction; it is reported as
  *   DOMAIN by the next cannikin_gns_stats or cannikin_device_status.  Free (one comparison in one
  *   thread); not applied by the NVLS variant, which exchanges no shares.
+ * Peer waits: the reduction kernels wait for their peers on the device.  CANNIKIN_SPIN_TIMEOUT_MS
+ *   (environment, read here): unset or 0 = wait as long as it takes (as NCCL does: a peer may be
+ *   late for a checkpoint or a data load); > 0 = after that long a waiting kernel stops waiting,
+ *   records a protocol error (that call's results are invalid) and finishes -- the next
+ *   cannikin_gns_stats / cannikin_device_status reports it as CUDA.  Never a trap.  (Exception:
+ *   ranks reducing different buckets -- a usage error whose shard ranges would disagree -- trap.)
  * Errors: INVALID (rank/world/device out of range, out == NULL, unknown flag), CUDA, NCCL. */
 #define CANNIKIN_INIT_CHECK_RATIOS 1u
 
@@ -101,7 +107,8 @@ cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world, const voi
  *     by construction -- also under a profiler that serialises kernels;
  *   - cannikin_weighted_allreduce per ctx, each rank on its own stream, issued concurrently (as
  *     W processes would); relies on the W kernels running at the same time (a serialising
- *     profiler breaks that: the first kernel waits for its peers until CANNIKIN_SPIN_TIMEOUT_MS).
+ *     profiler breaks that: the first kernel waits for its peers until CANNIKIN_SPIN_TIMEOUT_MS,
+ *     default 20000 for these contexts, and then reports a protocol error).
  * cannikin_ddp_allreduce_mean is UNSUPPORTED on such contexts; each is destroyed separately.
  * Errors: INVALID (world outside 2..CANNIKIN_MAX_WORLD, grid <= 0, unknown flag), CUDA. */
 cannikin_status cannikin_init_group_local(cannikin_ctx** out, int world, int device,
@@ -241,10 +248,18 @@ cannikin_status cannikin_device_status(cannikin_ctx* ctx);
  *   flags & CANNIKIN_LOCAL_LDG / CANNIKIN_LOCAL_TMA: force the 128-bit-load or the TMA-bulk-staged
  *         kernel variant (identical output bits; norms equal up to fp64 summation grouping);
  *         default: the faster one
- * 1 <= n_ranks <= CANNIKIN_MAX_EMULATED.  Errors: INVALID, UNSUPPORTED, CUDA. */
+ *   flags & CANNIKIN_LOCAL_CHAIN: the caller asserts that no input of this call is written by the
+ *         kernel enqueued immediately before it on `stream` (e.g. the next bucket of the same
+ *         gradient after the previous bucket's call).  The (LDG) kernel is always launched with
+ *         programmatic dependent launch; with this flag it streams its inputs while the preceding
+ *         kernel's last CTAs still run and waits for that kernel only before touching the shared
+ *         partial table and the statistics -- consecutive bucket launches overlap their ramps.
+ *         Without it the kernel waits for its predecessor before reading anything.
+ * 1 <= n_ranks <= CANNIKIN_MAX_EMULATED.  Errors: INVALID (also: unknown flag), UNSUPPORTED, CUDA. */
 #define CANNIKIN_ACCUMULATE 1u
 #define CANNIKIN_LOCAL_LDG 2u
 #define CANNIKIN_LOCAL_TMA 4u
+#define CANNIKIN_LOCAL_CHAIN 8u
 cannikin_status cannikin_weighted_sum_local(cannikin_ctx* ctx, const void* const* in, int n_ranks,
                                             const double* r, void* out, size_t n, cannikin_dtype dt,
                                             double* d_local_sq, double* d_global_sq, unsigned flags,
@@ -272,6 +287,11 @@ cannikin_status cannikin_trace(cannikin_ctx* ctx, uint64_t* out, int max_ctas, i
  * for launch accounting: 1 for a zero-copy or LL/LL128 reduction, 3 for a staged one (copy in,
  * kernel, copy out); for cannikin_weighted_allreduce_group it is recorded on ctxs[0]. */
 int cannikin_last_launch_count(cannikin_ctx* ctx);
+
+/* Name of the kernel variant the last hot-path call on this ctx ran: "k2", "k2_tma", "ll",
+ * "ll128", "twoshot", "twoshot_dyn", "push", "k4_nccl", "nvls" ("" before any; a static string,
+ * never NULL).  For cannikin_weighted_allreduce_group it is recorded on ctxs[0]. */
+const char* cannikin_last_variant(cannikin_ctx* ctx);
 
 /* ------------------------------------------------------------------------------------------
  * Host solvers (pure, thread-safe, no CUDA)

@@ -32,6 +32,7 @@ F32, BF16 = 0, 1
 ACCUMULATE = 1
 LOCAL_LDG = 2
 LOCAL_TMA = 4
+LOCAL_CHAIN = 8
 ROUND_PAPER = 1
 GNS_G_NONPOSITIVE = 1
 MAX_WORLD = 8
@@ -104,6 +105,7 @@ SIGNATURES = {
     "cannikin_weighted_sum_local": (_I, [_P, ctypes.POINTER(_P), _I, _DP, _P, _Z, _I, _P, _P, _U, _P]),
     "cannikin_ddp_allreduce_mean": (_I, [_P, _P, _Z, _I, _P]),
     "cannikin_last_launch_count": (_I, [_P]),
+    "cannikin_last_variant": (ctypes.c_char_p, [_P]),
     "cannikin_emulate_compute": (_I, [_D, _P]),
     "cannikin_trace": (_I, [_P, ctypes.POINTER(ctypes.c_uint64), _I, _IP]),
     "cannikin_gns_estimate": (_I, [_DP, _D, _LP, _I, ctypes.POINTER(_GnsResult)]),
@@ -259,12 +261,14 @@ class Context:
 
     def weighted_sum_local(self, in_ptrs, r, out_ptr: int, n: int, dtype: int, d_local_sq: int,
                            d_global_sq: int, accumulate: bool = False, stream=None,
-                           variant: str | None = None):
+                           variant: str | None = None, chain: bool = False):
         """variant: None (library default), "ldg" or "tma": same per-element arithmetic (identical
-        output bits); the fp64 norm partials differ only in summation grouping."""
+        output bits); the fp64 norm partials differ only in summation grouping.  chain: the inputs
+        are not written by the kernel enqueued just before (CANNIKIN_LOCAL_CHAIN)."""
         arr = (ctypes.c_void_p * len(in_ptrs))(*in_ptrs)
         flags = (ACCUMULATE if accumulate else 0) | {None: 0, "ldg": LOCAL_LDG,
                                                      "tma": LOCAL_TMA}[variant]
+        flags |= LOCAL_CHAIN if chain else 0
         _check(lib().cannikin_weighted_sum_local(self._h, arr, len(in_ptrs), _dbl(r), out_ptr, n,
                                                  dtype, d_local_sq, d_global_sq, flags,
                                                  _stream(stream)))
@@ -282,6 +286,9 @@ class Context:
 
     def last_launch_count(self) -> int:
         return int(lib().cannikin_last_launch_count(self._h))
+
+    def last_variant(self) -> str:
+        return lib().cannikin_last_variant(self._h).decode()
 
 
 def weighted_allreduce_group(ctxs, ptrs, n: int, dtype: int, r, stream=None):

@@ -230,6 +230,9 @@ extern "C" cannikin_status cannikin_init_group_local(cannikin_ctx** out, int wor
       return st;
     }
     out[k]->in_process = true;
+    // the ranks of an in-process group must run concurrently; a wait that lasts 20 s means they
+    // do not (e.g. per-rank calls under a serialising profiler): report instead of hanging
+    if (!std::getenv("CANNIKIN_SPIN_TIMEOUT_MS")) out[k]->spin_timeout_ns = 20ull * 1000000000ull;
   }
   for (int k = 0; k < world; ++k)
     for (int j = 0; j < world; ++j) out[k]->peer_base[j] = out[j]->base;
@@ -297,18 +300,21 @@ extern "C" cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* 
     CK_CUDA(cannikin::launch_wsum_local(ctx, in, 1, r, bucket, n, dt, &ctx->ctrl->stats[0],
                                         &ctx->ctrl->stats[1], true, 0, S(stream)));
     ctx->last_launches = 1;
+    ctx->last_variant = "k2";
     return CANNIKIN_OK;
   }
   if (cannikin::ll128_eligible(ctx, bytes)) {
     // mid-size bucket: flag-in-line two-shot, no barrier; touches only this rank's bucket
     CK_CUDA(cannikin::launch_ll128(ctx, bucket, n, dt, r_i, S(stream)));
     ctx->last_launches = 1;
+    ctx->last_variant = "ll128";
     return CANNIKIN_OK;
   }
   if (cannikin::ll_eligible(ctx, bytes)) {
     // small bucket: the LL kernel reads and writes only this rank's bucket (any device memory)
     CK_CUDA(cannikin::launch_ll(ctx, bucket, n, dt, r_i, S(stream)));
     ctx->last_launches = 1;
+    ctx->last_variant = "ll";
     return CANNIKIN_OK;
   }
   if (bytes > ctx->heap_bytes)
@@ -363,11 +369,13 @@ extern "C" cannikin_status cannikin_weighted_allreduce_group(cannikin_ctx* const
   if (cannikin::ll128_eligible(c0, bytes)) {
     CK_CUDA(cannikin::launch_ll128_group(ctxs, world, buckets, n, dt, r, S(stream)));
     ctxs[0]->last_launches = 1;
+    ctxs[0]->last_variant = "ll128";
     return CANNIKIN_OK;
   }
   if (cannikin::ll_eligible(c0, bytes)) {
     CK_CUDA(cannikin::launch_ll_group(ctxs, world, buckets, n, dt, r, S(stream)));
     ctxs[0]->last_launches = 1;
+    ctxs[0]->last_variant = "ll";
     return CANNIKIN_OK;
   }
   if (bytes > c0->heap_bytes)
@@ -410,7 +418,8 @@ static cannikin_status check_device_code(cannikin_ctx* ctx, const char* who) {
     CK_CUDA(cudaMemcpy(&ctx->ctrl->error_code, &zero, sizeof zero, cudaMemcpyHostToDevice));
     return fail(CANNIKIN_ERR_DOMAIN, "%s: the ranks' shares r_j sum to %.17g, not 1", who, s);
   }
-  if (code) return fail(CANNIKIN_ERR_CUDA, "%s: device protocol error %d", who, code);
+  if (code == 2) return fail(CANNIKIN_ERR_CUDA, "%s: the ranks reduced different buckets (device protocol error 2)", who);
+  if (code) return fail(CANNIKIN_ERR_CUDA, "%s: device protocol error %d (a peer wait timed out after CANNIKIN_SPIN_TIMEOUT_MS; results of the affected call are invalid)", who, code);
   return CANNIKIN_OK;
 }
 
@@ -524,16 +533,20 @@ extern "C" cannikin_status cannikin_weighted_sum_local(cannikin_ctx* ctx, const 
     return fail(CANNIKIN_ERR_INVALID, "weighted_sum_local: out not 16-byte aligned");
   CK_CUDA(cudaSetDevice(ctx->device));
   const bool acc = (flags & CANNIKIN_ACCUMULATE) != 0;
+  const bool chain = (flags & CANNIKIN_LOCAL_CHAIN) != 0;
   bool use_tma = ctx->local_tma;
   if (flags & CANNIKIN_LOCAL_LDG) use_tma = false;
   if (flags & CANNIKIN_LOCAL_TMA) use_tma = true;
+  if (flags & ~(CANNIKIN_ACCUMULATE | CANNIKIN_LOCAL_LDG | CANNIKIN_LOCAL_TMA | CANNIKIN_LOCAL_CHAIN))
+    return fail(CANNIKIN_ERR_INVALID, "weighted_sum_local: unknown flags %#x", flags);
   if (use_tma)
     CK_CUDA(cannikin::launch_wsum_local_tma(ctx, in, n_ranks, r, out, n, dt, d_local_sq,
                                             d_global_sq, acc, S(stream)));
   else
     CK_CUDA(cannikin::launch_wsum_local(ctx, in, n_ranks, r, out, n, dt, d_local_sq, d_global_sq,
-                                        acc, ctx->grid_local, S(stream)));
+                                        acc, ctx->grid_local, S(stream), chain));
   ctx->last_launches = 1;
+  ctx->last_variant = use_tma ? "k2_tma" : "k2";
   return CANNIKIN_OK;
 }
 
@@ -578,10 +591,13 @@ extern "C" cannikin_status cannikin_weighted_allreduce_nccl(cannikin_ctx* ctx, v
     CK_CUDA(cudaMalloc(&ctx->k4_buf, need));
     ctx->k4_bytes = need;
   }
+  ctx->last_variant = "k4_nccl";
   return cannikin::launch_k4(ctx, bucket, n, dt, r_i, S(stream));
 }
 
 extern "C" int cannikin_last_launch_count(cannikin_ctx* ctx) { return ctx ? ctx->last_launches : 0; }
+
+extern "C" const char* cannikin_last_variant(cannikin_ctx* ctx) { return ctx ? ctx->last_variant : ""; }
 
 extern "C" cannikin_status cannikin_emulate_compute(double seconds, void* stream) {
   if (!(seconds >= 0.0) || seconds > 60.0)
@@ -624,5 +640,6 @@ extern "C" cannikin_status cannikin_weighted_allreduce_nvls(cannikin_ctx* ctx, v
   CK_CUDA(cudaSetDevice(ctx->device));
   CK_CUDA(cannikin::launch_nvls(ctx, bucket, mc_bucket, n, dt, r_i, S(stream)));
   ctx->last_launches = 1;
+  ctx->last_variant = "nvls";
   return CANNIKIN_OK;
 }

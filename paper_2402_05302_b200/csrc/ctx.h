@@ -79,5 +79,8 @@ struct cannikin_ctx {
   std::map<size_t, size_t> used_blocks;
   double* h_stats = nullptr;  // pinned host staging for gns_stats
   int last_launches = 0;
-  uint64_t spin_timeout_ns = 20ull * 1000 * 1000 * 1000;
+  const char* last_variant = "";  // kernel variant of the last hot-path call (diagnostics)
+  // peer-wait timeout (dev::SpinClock): 0 = wait forever (multi-process default, as NCCL);
+  // in-process groups default to 20 s; CANNIKIN_SPIN_TIMEOUT_MS overrides either
+  uint64_t spin_timeout_ns = 0;
 };

@@ -200,6 +200,37 @@ __device__ __forceinline__ void st_relaxed_sys_f64(double* p, double v) {
 __device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Bookkeeping of a peer wait: expired() is true once timeout_ns (> 0) of device time has passed
+// since the first check (every `mask`+1 polls); it then records `code` in *err (the first code
+// wins) and the caller stops waiting -- the kernel finishes with a recorded protocol error, which
+// cannikin_gns_stats / cannikin_device_status report, instead of trapping (a trap would kill the
+// process's CUDA context) or hanging.  timeout_ns == 0 waits forever, as NCCL does: the default
+// for multi-process contexts, where a peer may legitimately be late (checkpoint, data loading).
+struct SpinClock {
+  uint64_t t0 = 0;
+  unsigned it = 0;
+  __device__ __forceinline__ bool expired(uint64_t timeout_ns, unsigned mask, int* err, int code) {
+    if ((++it & mask) != 0u || timeout_ns == 0) return false;
+    uint64_t now;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+    if (t0 == 0) {
+      t0 = now;
+      return false;
+    }
+    if (now - t0 <= timeout_ns) return false;
+    atomicCAS(err, 0, code);
+    return true;
+  }
+};
+
+// Programmatic dependent launch (sm_90+): let the next kernel on the stream be scheduled now (its
+// CTAs take SM slots as ours exit), and wait until the preceding kernel has completed and its
+// memory is visible (a no-op for a kernel launched without the programmatic attribute).
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -30,12 +30,13 @@ struct LocalArgs {
   uint64_t* trace;   // [grid][5] per-CTA timeline (LDG variant)
   int* trace_grid;
   int accumulate;
+  int chain;         // CANNIKIN_LOCAL_CHAIN: inputs may be read before the preceding kernel ends
 };
 
 cudaError_t launch_wsum_local(cannikin_ctx* ctx, const void* const* in, int nr, const double* r,
                               void* out, size_t n, cannikin_dtype dt, double* d_local_sq,
                               double* d_global_sq, bool accumulate, int grid_override,
-                              cudaStream_t st);
+                              cudaStream_t st, bool chain = false);
 cudaError_t launch_wsum_local_tma(cannikin_ctx* ctx, const void* const* in, int nr,
                                   const double* r, void* out, size_t n, cannikin_dtype dt,
                                   double* d_local_sq, double* d_global_sq, bool accumulate,

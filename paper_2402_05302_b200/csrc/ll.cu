@@ -59,19 +59,9 @@ __device__ __forceinline__ uint64_t wait_ll(const void* p, uint32_t e32, Ctrl* c
                                             uint64_t timeout_ns) {
   uint64_t w = ld_ll(p);
   if ((uint32_t)(w >> 32) == e32) return w;
-  uint64_t t0 = 0;
-  unsigned it = 0;
-  while ((uint32_t)((w = ld_ll(p)) >> 32) != e32) {
-    if ((++it & 1023u) == 0u) {
-      const uint64_t now = dev::globaltimer_ns();
-      if (t0 == 0) {
-        t0 = now;
-      } else if (now - t0 > timeout_ns) {
-        atomicExch(&ctrl->error_code, 8);
-        __trap();  // a peer never sent its words: fail loudly instead of hanging the GPU
-      }
-    }
-  }
+  dev::SpinClock clk;
+  while ((uint32_t)((w = ld_ll(p)) >> 32) != e32)
+    if (clk.expired(timeout_ns, 1023u, &ctrl->error_code, 8)) break;  // a peer never sent
   return w;
 }
 

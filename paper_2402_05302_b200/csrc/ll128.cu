@@ -82,22 +82,14 @@ __device__ __forceinline__ uint64_t ld_word(const void* p) {
   return v;
 }
 
-__device__ __noinline__ void l8_fail(Ctrl* ctrl) {
-  atomicExch(&ctrl->error_code, 9);
-  __trap();  // a peer never sent: fail loudly instead of hanging the GPU
-}
-
-// Spin until the epoch half of the 8-byte header word at p equals e32.
+// Spin until the epoch half of the 8-byte header word at p equals e32 (timeout: error code 9,
+// see dev::SpinClock).
 __device__ __forceinline__ uint64_t wait_word(const void* p, uint32_t e32, Ctrl* ctrl,
                                               uint64_t timeout_ns) {
-  uint64_t w = ld_word(p), t0 = 0;
-  unsigned it = 0;
+  uint64_t w = ld_word(p);
+  dev::SpinClock clk;
   while ((uint32_t)(w >> 32) != e32) {
-    if ((++it & 1023u) == 0u) {
-      const uint64_t now = dev::globaltimer_ns();
-      if (t0 == 0) t0 = now;
-      else if (now - t0 > timeout_ns) l8_fail(ctrl);
-    }
+    if (clk.expired(timeout_ns, 1023u, &ctrl->error_code, 9)) break;
     w = ld_word(p);
   }
   return w;
@@ -111,14 +103,10 @@ __device__ __forceinline__ bool flag_ok(const uint4& v, bool flag_lane, uint64_t
 // Wait until all four lines of the group at p carry epoch e (warp-uniform call).
 __device__ __forceinline__ uint4 wait_group(const char* p, uint4 v, bool flag_lane, uint64_t e,
                                             Ctrl* ctrl, uint64_t timeout_ns) {
-  uint64_t t0 = 0;
-  unsigned it = 0;
+  dev::SpinClock clk;
   while (!__all_sync(0xffffffffu, flag_ok(v, flag_lane, e))) {
-    if ((++it & 255u) == 0u) {
-      const uint64_t now = dev::globaltimer_ns();
-      if (t0 == 0) t0 = now;
-      else if (now - t0 > timeout_ns) l8_fail(ctrl);
-    }
+    // warp-uniform exit (the loop condition is a warp vote)
+    if (__any_sync(0xffffffffu, clk.expired(timeout_ns, 255u, &ctrl->error_code, 9))) break;
     v = ld_vol16(p);
   }
   return v;

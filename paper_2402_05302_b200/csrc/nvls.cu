@@ -69,19 +69,9 @@ __device__ __forceinline__ void st(void* p, const uint4& v, __nv_bfloat16) {
 
 __device__ __forceinline__ void wait_at_least(const uint64_t* flag, uint64_t ep, Ctrl* ctrl,
                                               uint64_t timeout_ns, int code) {
-  uint64_t t0 = 0;
-  unsigned it = 0;
-  while (dev::ld_acquire_sys(flag) < ep) {
-    if ((++it & 1023u) == 0u) {
-      const uint64_t now = dev::globaltimer_ns();
-      if (t0 == 0) {
-        t0 = now;
-      } else if (now - t0 > timeout_ns) {
-        atomicExch(&ctrl->error_code, code);
-        __trap();
-      }
-    }
-  }
+  dev::SpinClock clk;
+  while (dev::ld_acquire_sys(flag) < ep)
+    if (clk.expired(timeout_ns, 1023u, &ctrl->error_code, code)) return;
 }
 
 }  // namespace mc

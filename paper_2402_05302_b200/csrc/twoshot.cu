@@ -62,19 +62,9 @@ __device__ __forceinline__ void check_ratios(const float* r, Ctrl* c) {
 
 __device__ __forceinline__ void spin_until(const uint64_t* flag, uint64_t ep, Ctrl* ctrl,
                                            uint64_t timeout_ns, int code) {
-  uint64_t t0 = 0;
-  unsigned it = 0;
-  while (dev::ld_acquire_sys(flag) < ep) {
-    if ((++it & 1023u) == 0u) {
-      const uint64_t now = dev::globaltimer_ns();
-      if (t0 == 0) {
-        t0 = now;
-      } else if (now - t0 > timeout_ns) {
-        atomicExch(&ctrl->error_code, code);
-        __trap();  // a peer never arrived: fail loudly instead of hanging the GPU
-      }
-    }
-  }
+  dev::SpinClock clk;
+  while (dev::ld_acquire_sys(flag) < ep)
+    if (clk.expired(timeout_ns, 1023u, &ctrl->error_code, code)) return;  // peer never arrived
 }
 
 __device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
@@ -86,20 +76,10 @@ __device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
 // Spin until the low 32 bits of *word (an epoch tag) reach e32 (wrap-safe); returns the word.
 __device__ __forceinline__ uint64_t spin_word(const uint64_t* word, uint32_t e32, Ctrl* ctrl,
                                               uint64_t timeout_ns, int code) {
-  uint64_t t0 = 0;
-  unsigned it = 0;
+  dev::SpinClock clk;
   uint64_t w;
-  while ((int32_t)((uint32_t)(w = ld_relaxed_sys(word)) - e32) < 0) {
-    if ((++it & 1023u) == 0u) {
-      const uint64_t now = dev::globaltimer_ns();
-      if (t0 == 0) {
-        t0 = now;
-      } else if (now - t0 > timeout_ns) {
-        atomicExch(&ctrl->error_code, code);
-        __trap();
-      }
-    }
-  }
+  while ((int32_t)((uint32_t)(w = ld_relaxed_sys(word)) - e32) < 0)
+    if (clk.expired(timeout_ns, 1023u, &ctrl->error_code, code)) break;
   return w;
 }
 
@@ -122,7 +102,9 @@ __device__ __forceinline__ void entry_barrier_thread(const ArArgs& a, int b, uin
   const uint64_t wm = spin_word(&a.ctrl->meta_word[b][tid], e32, a.ctrl, a.timeout_ns, 1);
   s_r[tid] = __uint_as_float((uint32_t)(wr >> 32));
   if ((uint32_t)(wm >> 32) != m32) {
-    atomicExch(&a.ctrl->error_code, 2);  // ranks disagree on bucket offset/size/dtype/grid
+    // ranks disagree on bucket offset/size/dtype/grid: a usage error whose shard ranges would
+    // differ between ranks (out-of-range peer accesses) -- stop the context, do not continue
+    atomicExch(&a.ctrl->error_code, 2);
     __trap();
   }
 }
@@ -529,15 +511,9 @@ __device__ __forceinline__ void twoshot_push_body(const PushArgs& a, const int b
                         ((uint64_t)__float_as_uint(a.r_me) << 32) | e32);
     uint64_t w;
     {
-      uint64_t t0 = 0;
-      unsigned it = 0;
-      while ((int32_t)((uint32_t)(w = dev::ld_acquire_sys(&a.ctrl->pmid[b][tid])) - e32) < 0) {
-        if ((++it & 1023u) == 0u) {
-          const uint64_t now = dev::globaltimer_ns();
-          if (t0 == 0) t0 = now;
-          else if (now - t0 > a.timeout_ns) { atomicExch(&a.ctrl->error_code, 6); __trap(); }
-        }
-      }
+      dev::SpinClock clk;
+      while ((int32_t)((uint32_t)(w = dev::ld_acquire_sys(&a.ctrl->pmid[b][tid])) - e32) < 0)
+        if (clk.expired(a.timeout_ns, 1023u, &a.ctrl->error_code, 6)) break;
     }
     s_r[tid] = __uint_as_float((uint32_t)(w >> 32));
     const uint64_t wm = spin_word(&a.ctrl->meta_word[b][tid], e32, a.ctrl, a.timeout_ns, 2);
@@ -817,6 +793,8 @@ cudaError_t launch_twoshot(cannikin_ctx* ctx, size_t off, size_t n, cannikin_dty
                            cudaStream_t st) {
   ArPlan p;
   plan_twoshot(ctx, off, n, dt, r_i, &p);
+  static const char* const kNames[3] = {"twoshot", "twoshot_dyn", "push"};
+  ctx->last_variant = kNames[p.kind];
   if (dt == CANNIKIN_F32) return dispatch_plan<float>(ctx->world, &p, false, st);
   return dispatch_plan<__nv_bfloat16>(ctx->world, &p, false, st);
 }
@@ -827,6 +805,8 @@ cudaError_t launch_twoshot_group(cannikin_ctx* const* ctxs, int W, size_t off, s
                                  cannikin_dtype dt, const double* r, cudaStream_t st) {
   ArPlan p[kMaxWorld];
   for (int k = 0; k < W; ++k) plan_twoshot(ctxs[k], off, n, dt, r[k], &p[k]);
+  static const char* const kNames[3] = {"twoshot", "twoshot_dyn", "push"};
+  ctxs[0]->last_variant = kNames[p[0].kind];
   if (dt == CANNIKIN_F32) return dispatch_plan<float>(W, p, true, st);
   return dispatch_plan<__nv_bfloat16>(W, p, true, st);
 }

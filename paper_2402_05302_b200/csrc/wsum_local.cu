@@ -35,6 +35,12 @@ __global__ void __launch_bounds__(NT, NT == 256 && NR <= 8 ? CANNIKIN_K2_MINB : 
   __shared__ double red[32 * (NR + 1)];
   __shared__ bool s_last;
 
+  // Programmatic dependent launch: the next kernel may be scheduled at once -- a chained next
+  // bucket (CANNIKIN_LOCAL_CHAIN) then streams its inputs while this grid's last CTAs finish.
+  // Without the chain flag this launch waits for its predecessor before reading anything (it may
+  // have produced our inputs); with it, only before the shared partial table and the statistics.
+  dev::pdl_launch_dependents();
+  if (!a.chain) dev::pdl_wait();
   if (threadIdx.x == 0) {
     a.trace[blockIdx.x * 5] = dev::globaltimer_ns();
     unsigned smid;
@@ -92,6 +98,9 @@ __global__ void __launch_bounds__(NT, NT == 256 && NR <= 8 ? CANNIKIN_K2_MINB : 
   for (int j = 0; j < NR; ++j) vals[j] = lsq[j];
   vals[NR] = gsq;
   dev::block_sum(vals, red);
+  // the partial table, the ticket and the (accumulated) statistics are shared with the preceding
+  // chained launch: from here on it must have completed
+  if (a.chain) dev::pdl_wait();
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int j = 0; j <= NR; ++j) a.partials[(size_t)blockIdx.x * (NR + 1) + j] = vals[j];
@@ -149,8 +158,18 @@ static cudaError_t launch_nt(const LocalArgs& a, int num_sms, int grid_override,
   const size_t need = (a.nvec + NT - 1) / NT;
   if ((size_t)grid > need) grid = need < 1 ? 1 : (int)need;
   if (grid > kMaxLocalBlocks) grid = kMaxLocalBlocks;
-  wsum_local_kernel<T, NR, U, NT><<<grid, NT, 0, st>>>(a);
-  return cudaGetLastError();
+  // launched with programmatic stream serialization (PDL): see the kernel's prologue
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, wsum_local_kernel<T, NR, U, NT>, a);
 }
 
 template <typename T, int NR>
@@ -183,7 +202,7 @@ static cudaError_t dispatch(int nr, const LocalArgs& a, int num_sms, int grid_ov
 cudaError_t launch_wsum_local(cannikin_ctx* ctx, const void* const* in, int nr, const double* r,
                               void* out, size_t n, cannikin_dtype dt, double* d_local_sq,
                               double* d_global_sq, bool accumulate, int grid_override,
-                              cudaStream_t st) {
+                              cudaStream_t st, bool chain) {
   LocalArgs a{};
   for (int j = 0; j < nr; ++j) {
     a.in[j] = static_cast<const char*>(in[j]);
@@ -200,6 +219,7 @@ cudaError_t launch_wsum_local(cannikin_ctx* ctx, const void* const* in, int nr, 
   a.local_sq = d_local_sq;
   a.global_sq = d_global_sq;
   a.accumulate = accumulate ? 1 : 0;
+  a.chain = chain ? 1 : 0;
   // partial rows are (nr+1) doubles wide: reinterpret local_part as a flat array
   if (dt == CANNIKIN_F32)
     return dispatch<float>(nr, a, ctx->num_sms, grid_override, ctx->local_nt, st);

@@ -5,13 +5,19 @@ and collects the GNS norm statistics of every bucket in the same pass (Eq. 10 in
 DDP already does the bucketing and overlaps each bucket's sync with the rest of backprop (the
 mechanism §3.2.3 models); the hook only swaps the reduction.  Each rank's local loss
 must be the MEAN over its b_i samples (Eq. 1) and r_i = b_i / B.  After backward,
-`state.ctx.gns_stats()` returns |g_j|^2 for every rank and |g|^2 of the whole gradient.
+`state.gns_stats()` returns |g_j|^2 for every rank and |g|^2 of the whole gradient (ordered after
+the hook's reductions, whatever stream the training loop runs on).
 
+    ctx = torch_api.init_distributed_context(heap_bytes, grid=24)   # small grid: see below
     state = CannikinHookState(ctx, r_i)
     ddp_model.register_comm_hook(state, cannikin_hook)
 
-Argument marshalling only: the reduction runs in libcannikin.so (two-shot NVLink kernel; DDP's
-bucket buffers are not in the peer-mapped heap, so each bucket is staged through it).
+The reductions run on the hook's own stream, overlapped with backprop.  A reduction kernel whose
+peer is still computing waits on the device, holding its CTAs' SMs; give the ctx a small grid
+(NCCL likewise uses a few channels) so the fast rank's backward keeps its SMs.  DDP's buckets
+(25 MB by default) fall in the LL128 kernel's range, which reads and writes only the local bucket
+(no staging); larger buckets outside the ctx heap are staged through it.
+Argument marshalling only: the reduction runs in libcannikin.so.
 """
 import torch
 
@@ -34,6 +40,12 @@ class CannikinHookState:
     def set_ratio(self, r_i: float):
         """Update r_i = b_i / B when the split changes (a new epoch's plan)."""
         self.r_i = float(r_i)
+
+    def gns_stats(self):
+        """Read and reset the statistics of every bucket reduced since the last call: ordered on
+        the hook's stream after the calling stream's work (hence after DDP's last bucket)."""
+        self.stream.wait_stream(torch.cuda.current_stream())
+        return self.ctx.gns_stats(stream=self.stream)
 
 
 def cannikin_hook(state: CannikinHookState, bucket) -> torch.futures.Future[torch.Tensor]:

@@ -78,9 +78,10 @@ def weighted_allreduce_nccl(ctx: Context, bucket: torch.Tensor, r_i: float, stre
 
 def weighted_sum_local(ctx: Context, grads, r, out: torch.Tensor, local_sq: torch.Tensor,
                        global_sq: torch.Tensor, accumulate: bool = False, stream=None,
-                       variant=None):
+                       variant=None, chain: bool = False):
     """Emulated ranks on one GPU: out <- sum_j r_j grads[j]; local_sq[j] <- |grads[j]|^2;
-    global_sq <- |out|^2 (float64 device tensors)."""
+    global_sq <- |out|^2 (float64 device tensors).  chain=True: consecutive bucket of the same
+    gradient (its inputs are not produced by the kernel just before; CANNIKIN_LOCAL_CHAIN)."""
     dt = dtype_code(out.dtype)
     # local_sq / global_sq: float64 device tensors or pinned (device-mapped) host tensors
     for g in grads:
@@ -88,7 +89,7 @@ def weighted_sum_local(ctx: Context, grads, r, out: torch.Tensor, local_sq: torc
     assert local_sq.dtype == torch.float64 and global_sq.dtype == torch.float64
     ctx.weighted_sum_local([g.data_ptr() for g in grads], list(r), out.data_ptr(), out.numel(), dt,
                            local_sq.data_ptr(), global_sq.data_ptr(), accumulate, _cur(stream),
-                           variant)
+                           variant, chain)
 
 
 def ddp_allreduce_mean(ctx: Context, bucket: torch.Tensor, stream=None):

@@ -31,6 +31,7 @@ CANDS = [9, 16, 32, 64, 96, 128, 192, 256, 384, 512, 768, 1024]
 
 
 def main():
+    os.environ.setdefault("CANNIKIN_SPIN_TIMEOUT_MS", "120000")  # report, do not hang
     ap = argparse.ArgumentParser()
     ap.add_argument("--epochs", type=int, default=8)
     ap.add_argument("--steps", type=int, default=10)

@@ -88,6 +88,7 @@ class SlowResNet(nn.Module):
 
 
 def main():
+    os.environ.setdefault("CANNIKIN_SPIN_TIMEOUT_MS", "120000")  # report, do not hang
     ap = argparse.ArgumentParser()
     ap.add_argument("--B", type=int, default=512)
     ap.add_argument("--epochs", type=int, default=4)

@@ -45,6 +45,7 @@ def timed(fn, reps):
 
 
 def main():
+    os.environ.setdefault("CANNIKIN_SPIN_TIMEOUT_MS", "120000")  # report, do not hang
     ap = argparse.ArgumentParser()
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--grids", default="0")

@@ -30,6 +30,7 @@ from paper_2402_05302_b200 import torch_api as ta  # noqa: E402
 
 
 def main():
+    os.environ.setdefault("CANNIKIN_SPIN_TIMEOUT_MS", "120000")  # report, do not hang
     ap = argparse.ArgumentParser()
     ap.add_argument("--epochs", type=int, default=5)
     ap.add_argument("--iters", type=int, default=6)
