@@ -194,6 +194,57 @@ def hetero_sm_compare(N, s, tdt, rank, world, local_rank, B, iters, dist, ta, ck
     return out
 
 
+def bucketed_sidecar(launch, N, s, n, world, bucket_mb, steps, peak, alg_bytes, dist, torch):
+    """The paper's bucketed regime (DDP-style buckets) on the bench gradient: the step's
+    reduction cut into buckets of `bucket_mb` per rank, one library call per bucket, captured in
+    one CUDA graph and timed as a chain (first start to last end, CUDA events, max over ranks).
+    launch(a, c, first) enqueues the call for elements [a, c).  At N = 1 consecutive K2 launches are
+    PDL-chained (CANNIKIN_LOCAL_CHAIN), so a launch's duration is the chain's / launches."""
+    be = int(bucket_mb * 2**20) // s
+    be -= be % 8
+    cuts = list(range(0, N, be)) + [N]
+    nb = len(cuts) - 1
+
+    def seq():
+        for i in range(nb):
+            launch(cuts[i], cuts[i + 1], i == 0)
+
+    seq()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        seq()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / steps], device="cuda", dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    chain_ms = float(t.item())
+    out = {"bucket_mb": bucket_mb, "launches_per_step": nb, "chain_ms": round(chain_ms, 4),
+           "kernel_ms": round(chain_ms / nb, 4),
+           "value": round(n * N * s / (chain_ms * 1e-3) / 1e9, 2), "unit": "GB/s"}
+    if world == 1:
+        ach = alg_bytes / (chain_ms * 1e-3) / 1e9
+        out["roofline"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+                           "frac": round(ach / peak, 4),
+                           "kernel": "wsum_local_kernel (K2), PDL-chained bucket launches"}
+    else:
+        busbw = N * s / (chain_ms * 1e-3) * 2 * (n - 1) / n / 1e9
+        out["roofline"] = {"bound": "nvlink", "achieved": round(busbw, 1), "peak": 770.0,
+                           "frac": round(busbw / 770.0, 4),
+                           "nominal_frac": round(busbw / 900.0, 4)}
+    return out
+
+
 def nvls_sidecar(ctx, N, rank, world, r_i, steps, dist, ta, torch):
     """fp32 weighted all-reduce of N elements through NVSwitch multicast (K6) next to the two-shot
     kernel (K3) on the same bytes: kernel time (CUDA events, max over ranks) and busbw."""
@@ -705,6 +756,27 @@ def main():
         except Exception as e:  # a sidecar must not sink the bench line
             ddp["k4_nccl_path"] = {"unavailable": str(e)[:200]}
 
+    # ---- the bucketed regime (DDP-style 25 MB buckets per rank) next to the whole-gradient line
+    bucketed = None
+    if nb == 1:
+        if world == 1:
+            sc = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+
+            def blaunch(a, c, first):
+                ta.weighted_sum_local(ctx, [g[a:c] for g in gs], r, out[a:c], sc[:n], sc[n:],
+                                      accumulate=not first, chain=not first)
+        else:
+            def blaunch(a, c, first):
+                ta.weighted_allreduce(ctx, bucket[a:c], r[rank])
+        try:
+            bucketed = bucketed_sidecar(blaunch, N, s, n, world, 25.0, args.steps,
+                                        peaks["hbm_gbs"], alg_bytes, dist, torch)
+            if world > 1:
+                bucketed["kernel"] = f"K3 {ctx.last_variant()}"
+                ctx.gns_stats()
+        except Exception as e:  # a sidecar must not sink the bench line
+            bucketed = {"unavailable": str(e)[:200]}
+
     # ---- NVSwitch-multicast (NVLS) variant, fp32 sidecar on the same element count (K6)
     nvls = None
     if world > 1 and not args.no_nvls:
@@ -792,7 +864,8 @@ def main():
                               "not a roofline claim"),
                        "cuda_graph": graphs is not None,
                        "host_overlap": "host half of step t overlaps device half of step t+1"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "ddp_baseline": ddp,
+            "roofline": roof, "bucketed_25mb": bucketed, "cpu_baseline": cpu, "e2e": e2e,
+            "ddp_baseline": ddp,
             "step_vs_ddp": hetero, "nvls_f32": nvls,
             # K2 / K3 per bucket, plus (N > 1) the statistics-finalize kernel per step
             "gpu_launches": (launches_per_step() + (1 if world > 1 else 0)) * args.steps,
