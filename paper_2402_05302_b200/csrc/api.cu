@@ -627,7 +627,9 @@ extern "C" cannikin_status cannikin_weighted_allreduce_nvls(cannikin_ctx* ctx, v
   ctx->last_launches = 0;
   // bf16: the switch's bf16 ld_reduce (SASS HPADD.BF16x8) does not keep the sum within the 1e-2
   // bf16 tolerance (measured 1.06e-2 at W = 2, tests/test_gpu_nvls.py), so NVLS is fp32-only
-  if (dt != CANNIKIN_F32)
+  // CANNIKIN_NVLS_BF16=1 (characterisation only, tools/nvls_bf16_probe.py) lets bf16 through
+  static const bool bf16_probe = std::getenv("CANNIKIN_NVLS_BF16") && std::atoi(std::getenv("CANNIKIN_NVLS_BF16"));
+  if (dt != CANNIKIN_F32 && !(dt == CANNIKIN_BF16 && bf16_probe))
     return fail(CANNIKIN_ERR_UNSUPPORTED, "weighted_allreduce_nvls: fp32 buckets only (dtype %d)", (int)dt);
   if (ctx->world < 2) return fail(CANNIKIN_ERR_UNSUPPORTED, "weighted_allreduce_nvls: world < 2");
   if (n == 0) return CANNIKIN_OK;

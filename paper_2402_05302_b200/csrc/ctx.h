@@ -25,6 +25,7 @@ struct Ctrl {
   uint64_t mid[kMaxArBlocks][kMaxWorld];                     // [peer] NVLS: "my piece is scaled"
   uint64_t nv_exit[kMaxArBlocks][kMaxWorld];                 // [peer] NVLS: "my stores landed"
   uint64_t nv_epoch;                                         // [local] NVLS call counter
+  uint64_t nv_meta[kMaxArBlocks][kMaxWorld];                 // [peer] NVLS: (bucket hash32, epoch32)
   uint64_t rv_word[kMaxArBlocks][kMaxWorld];                 // [peer] entry: (float r_src, epoch32)
   uint64_t meta_word[kMaxArBlocks][kMaxWorld];               // [peer] entry: (bucket hash32, epoch32)
   uint64_t pmid[kMaxArBlocks][kMaxWorld];                    // [peer] push variant: (r_src, epoch32)

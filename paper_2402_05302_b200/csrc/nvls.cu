@@ -137,9 +137,18 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const McArgs a, int W) {
   // piece b of every rank: the piece of my shard that CTA b reduces below is scaled everywhere
   __syncthreads();
   if (tid < W) {
+    // the bucket identity (size, dtype, grid) travels with the barrier: ranks that disagree would
+    // pair different shard ranges, so a mismatch stops the context (code 2, as K3's entry check)
+    const uint32_t m32 = (uint32_t)(a.meta ^ (a.meta >> 32));
+    dev::st_relaxed_sys_u64(&a.pctrl[tid]->nv_meta[b][a.rank], ((uint64_t)m32 << 32) | (uint32_t)ep);
     __threadfence_system();
     dev::st_release_sys(&a.pctrl[tid]->mid[b][a.rank], ep);
     mc::wait_at_least(&a.ctrl->mid[b][tid], ep, a.ctrl, a.timeout_ns, 4);
+    const uint64_t wm = dev::ld_acquire_sys(&a.ctrl->nv_meta[b][tid]);
+    if ((uint32_t)wm == (uint32_t)ep && (uint32_t)(wm >> 32) != m32) {
+      atomicExch(&a.ctrl->error_code, 2);
+      __trap();
+    }
   }
   __syncthreads();
   if (tid == 0) a.ctrl->trace[b][1] = dev::globaltimer_ns();

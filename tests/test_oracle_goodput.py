@@ -100,3 +100,13 @@ def test_analyzer_choose_batch_cache_equals_brute_force_with_fixed_models():
         assert r["B"] == ogp.choose_batch(learned, lcomm, CANDS, 16, bn)
         assert sum(r["b"]) == r["B"]
     assert fulls[0] is True and fulls[-1] is False
+
+
+def test_goodput_hand_value():
+    """goodput(B) = B / T(B) x efficiency (reading Q27), T = Eq. 7 at the integer split.
+    One node with f(b) = 0.01 b (q = 0.01, other terms 0, gamma = 0): B = 100 -> T = 1.0 s,
+    throughput 100/s; B0 = 20, B_noise = 80 -> efficiency (80+20)/(80+100) = 5/9 -> 55.5...; also
+    T is returned as the second value."""
+    g, T = ogp.goodput([(0.01, 0.0, 0.0, 0.0)], (0.0, 0.0, 0.0), 100, 20, 80.0)
+    assert abs(T - 1.0) <= 1e-15
+    assert abs(g - 100.0 * 5.0 / 9.0) <= 1e-12

@@ -145,3 +145,11 @@ def test_library_fit_and_ivw_match_oracle():
         ck.fit_linear([1.0, 1.0], [1.0, 2.0])
     with pytest.raises(ck.CannikinError):
         ck.ivw([1.0], [-1.0])
+
+
+def test_sample_variance_hand_values():
+    """Eq. 12's sample variance (reading Q22: ddof = 1): [1, 2, 3, 4] -> 5/3; [2, 2] -> 0;
+    [0, 10] -> 50 (the population variance would give 25)."""
+    assert abs(learn.sample_variance([1.0, 2.0, 3.0, 4.0]) - 5.0 / 3.0) <= 1e-15
+    assert learn.sample_variance([2.0, 2.0]) == 0.0
+    assert learn.sample_variance([0.0, 10.0]) == 50.0

@@ -245,3 +245,30 @@ def test_algorithm1_agrees_with_exact_split_whenever_it_answers():
         assert math.isclose(r["T"], T, rel_tol=1e-9)
         assert np.allclose(r["b"], b, rtol=1e-7, atol=1e-7)
     assert answered > 10 * max(failed, 1)
+
+
+def test_node_inverse_hand_values_and_both_branches():
+    """node_inverse = the largest b with f(b) <= T, f = max(compute line, comm line).  Hand example:
+    q, s, k, m = 1, 2, 3, 4; gamma = 0.5, T_o = 10, T_u = 1:
+      compute line (q+k) b + (s+m+T_u)               = 4 b + 7
+      comm line    (q+gamma k) b + (s+gamma m+T_o+T_u) = 2.5 b + 15
+    The lines cross at b = 8/1.5 = 16/3 (f = 85/3): below it the comm line binds, above the compute.
+    T = 40: compute 33/4 = 8.25, comm 10  -> 8.25 (compute-bound side);
+    T = 20: compute 13/4 = 3.25, comm 2   -> 2    (comm-bound side)."""
+    node, comm = (1.0, 2.0, 3.0, 4.0), (0.5, 10.0, 1.0)
+    assert osp.node_inverse(node, comm, 40.0) == 8.25
+    assert osp.node_inverse(node, comm, 20.0) == 2.0
+    for T in (20.0, 85.0 / 3.0, 40.0, 123.0):  # f(f^-1(T)) = T on both branches and at the kink
+        assert abs(osp.node_time(node, comm, osp.node_inverse(node, comm, T)) - T) <= 1e-12 * T
+
+
+def test_breakpoint_time_hand_value():
+    """T* = f(b_bp) with b_bp = (T_o/(1-gamma) - m)/k where (1-gamma) P = T_o.  Same node:
+    b_bp = (10/0.5 - 4)/3 = 16/3, the crossing of the two lines above, f = 4*16/3 + 7 = 85/3; a
+    node with k = 0 is compute-bound forever iff (1-gamma) m >= T_o."""
+    node, comm = (1.0, 2.0, 3.0, 4.0), (0.5, 10.0, 1.0)
+    assert abs(osp.breakpoint_time(node, comm) - 85.0 / 3.0) <= 1e-13
+    assert osp.is_compute_bound(node, comm, 16.0 / 3.0 + 1e-9)
+    assert not osp.is_compute_bound(node, comm, 16.0 / 3.0 - 1e-9)
+    assert osp.breakpoint_time((1.0, 0.0, 0.0, 30.0), comm) == -math.inf   # (1-g) m = 15 >= 10
+    assert osp.breakpoint_time((1.0, 0.0, 0.0, 10.0), comm) == math.inf    # 5 < 10
