@@ -77,7 +77,8 @@ def hetero_models(n):
 SM_CAPS = {"A100": 148, "V100": 60, "P100": 40}
 
 
-def hetero_sm_compare(N, s, tdt, rank, world, local_rank, B, iters, dist, ta, ck, torch):
+def hetero_sm_compare(N, s, tdt, rank, world, local_rank, B, iters, dist, ta, ck, torch,
+                      grid=0, gated=True):
     """Step time of Cannikin against equal-split DDP on ranks made heterogeneous by REAL compute
     under SM caps (green contexts, SM_CAPS by the cyclic A100/V100/P100 mix), not by injected
     delays.  The compute is a synthetic layer stack of bf16 GEMMs (each sample = T tokens of width
@@ -87,7 +88,10 @@ def hetero_sm_compare(N, s, tdt, rank, world, local_rank, B, iters, dist, ta, ck
     epoch 0 even split, epoch 1 Eq. 8, epoch 2 OptPerf from the models the analyzer LEARNED from
     per-rank CUDA-event timings (a_i, P_i, gamma_i, T_o, T_u) -- with the fused weighted
     all-reduce.  DDP: b_i = B/n with the NCCL average.  The prediction error compares the
-    analyzer's Eq. 7 prediction with the measured step.  Max over ranks throughout."""
+    analyzer's Eq. 7 prediction with the measured step.  Max over ranks throughout.
+    `gated` (CANNIKIN_INIT_GATED_ENTRY): a fast rank waits for its slow peers in a one-warp gate
+    kernel instead of in the reduction grid, which would otherwise hold SMs its own backward pass
+    needs; `grid` is the reduction kernels' CTA count (0 = one per SM)."""
     from torch.cuda.green_contexts import GreenContext
 
     NB, T, H = 9, 512, 2048
@@ -95,8 +99,7 @@ def hetero_sm_compare(N, s, tdt, rank, world, local_rank, B, iters, dist, ta, ck
     gctx = GreenContext.create(SM_CAPS[gpu], local_rank)
     cs = gctx.Stream()
     ms = torch.cuda.Stream()
-    # reductions overlap a peer's compute: a small grid leaves the SMs to the backward pass
-    ctx = ta.init_distributed_context(heap_bytes=N * s, grid=24)
+    ctx = ta.init_distributed_context(heap_bytes=N * s, grid=grid, gated=gated)
     bucket = ta.bucket_tensor(ctx, N, tdt)
     bucket.normal_()
     cuts = [j * (N // NB - (N // NB) % 8) for j in range(NB)] + [N]
@@ -186,6 +189,7 @@ def hetero_sm_compare(N, s, tdt, rank, world, local_rank, B, iters, dist, ta, ck
            "learned_comm": {"gamma": round(comm[0], 4), "t_o_ms": round(comm[1] * 1e3, 4),
                             "t_u_ms": round(comm[2] * 1e3, 4)},
            "compute": f"bf16 GEMM stack, {T} tokens x {H} wide per sample, {NB} layers",
+           "reduction": {"gated_entry": gated, "grid": grid or "one CTA per SM"},
            "note": "heterogeneity = real compute on SM-capped green contexts; split from models "
                    "learned from measured timings (not from the generator); comm kernels real; "
                    "median step of the last epoch, max over ranks"}
@@ -514,6 +518,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of a CUDA graph")
     ap.add_argument("--no-hetero", action="store_true", help="skip the step-time-vs-DDP comparison")
+    ap.add_argument("--hetero-grid", type=int, default=0,
+                    help="step-vs-DDP: CTAs of the reduction kernels (0 = one per SM)")
+    ap.add_argument("--hetero-ungated", action="store_true",
+                    help="step-vs-DDP: wait for late peers inside the reduction grid (no gate)")
     ap.add_argument("--no-nvls", action="store_true", help="skip the NVLS fp32 sidecar")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -789,7 +797,8 @@ def main():
     if world > 1 and not args.no_hetero:
         try:
             hetero = hetero_sm_compare(N, s, tdt, rank, world, local_rank, max(B, world), 6, dist,
-                                       ta, ck, torch)
+                                       ta, ck, torch, grid=args.hetero_grid,
+                                       gated=not args.hetero_ungated)
         except Exception as e:  # green contexts unavailable: report, do not sink the bench line
             hetero = {"unavailable": str(e)[:300]}
 

@@ -86,6 +86,13 @@ cannikin_status cannikin_get_unique_id(void* out_id);
  *   and must lie within 2^-23 of 1.  A violation does not stop the reduction; it is reported as
  *   DOMAIN by the next cannikin_gns_stats or cannikin_device_status.  Free (one comparison in one
  *   thread); not applied by the NVLS variant, which exchanges no shares.
+ * `flags` may also include CANNIKIN_INIT_GATED_ENTRY (world > 1; ignored for world == 1): every
+ *   cannikin_weighted_allreduce first enqueues a one-warp gate kernel that waits until every peer
+ *   has reached the same call, and only then the reduction kernel.  For reductions that overlap
+ *   the rank's own compute under heterogeneous ranks: a fast rank's wait for a slow
+ *   peer then holds one SM slot of 32 threads instead of the reduction grid.  Costs one extra
+ *   launch and a round trip per call (cannikin_last_launch_count counts it).  Every rank of a
+ *   communicator must use the same setting.
  * Peer waits: the reduction kernels wait for their peers on the device.  CANNIKIN_SPIN_TIMEOUT_MS
  *   (environment, read here): unset or 0 = wait as long as it takes (as NCCL does: a peer may be
  *   late for a checkpoint or a data load); > 0 = after that long a waiting kernel stops waiting,
@@ -94,6 +101,7 @@ cannikin_status cannikin_get_unique_id(void* out_id);
  *   ranks reducing different buckets -- a usage error whose shard ranges would disagree -- trap.)
  * Errors: INVALID (rank/world/device out of range, out == NULL, unknown flag), CUDA, NCCL. */
 #define CANNIKIN_INIT_CHECK_RATIOS 1u
+#define CANNIKIN_INIT_GATED_ENTRY 2u
 
 cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world, const void* unique_id,
                               int device, size_t heap_bytes, int grid, unsigned flags);

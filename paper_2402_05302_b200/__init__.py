@@ -46,7 +46,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def lib_path() -> str:
-    return os.path.join(_HERE, "libcannikin.so")
+    # CANNIKIN_LIB: an alternative build of the same library (tools' build-time A/B runs only)
+    return os.environ.get("CANNIKIN_LIB") or os.path.join(_HERE, "libcannikin.so")
 
 
 class CannikinError(RuntimeError):
@@ -171,6 +172,7 @@ def _stream(s) -> int | None:
 
 # ----------------------------------------------------------------------------- device context
 INIT_CHECK_RATIOS = 1  # cannikin.h CANNIKIN_INIT_CHECK_RATIOS
+INIT_GATED_ENTRY = 2   # cannikin.h CANNIKIN_INIT_GATED_ENTRY
 
 
 class Context:
@@ -178,14 +180,14 @@ class Context:
 
     def __init__(self, rank: int = 0, world: int = 1, unique_id: bytes | None = None,
                  device: int = 0, heap_bytes: int = 0, grid: int = 0,
-                 check_ratios: bool = False):
+                 check_ratios: bool = False, gated: bool = False):
         L = lib()
         h = ctypes.c_void_p()
         uid = None
         if unique_id is not None:
             assert len(unique_id) == 128
             uid = ctypes.create_string_buffer(bytes(unique_id), 128)
-        flags = INIT_CHECK_RATIOS if check_ratios else 0
+        flags = (INIT_CHECK_RATIOS if check_ratios else 0) | (INIT_GATED_ENTRY if gated else 0)
         _check(L.cannikin_init(ctypes.byref(h), rank, world, uid, device, heap_bytes, grid, flags))
         self._h = h
         self.rank, self.world, self.device = rank, world, device

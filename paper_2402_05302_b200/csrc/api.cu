@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -29,6 +31,23 @@ using cannikin::fail;
       return fail(CANNIKIN_ERR_NCCL, "%s: %s (%s:%d)", #expr, ncclGetErrorString(r_),     \
                   __FILE__, __LINE__);                                                    \
   } while (0)
+
+// NVTX range around one hot-path call (host side: the enqueue; a profiler attached through NVTX
+// correlates it with the kernels it launched), payload = the call's bucket bytes -- SURVEY §5's
+// per-bucket ranges.  Header-only NVTX v3: free when no tool is attached.
+struct NvtxRange {
+  NvtxRange(const char* name, uint64_t bytes) {
+    nvtxEventAttributes_t a = {};
+    a.version = NVTX_VERSION;
+    a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    a.message.ascii = name;
+    a.payloadType = NVTX_PAYLOAD_TYPE_UNSIGNED_INT64;
+    a.payload.ullValue = bytes;
+    nvtxRangePushEx(&a);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 static inline size_t elem_size(cannikin_dtype dt) { return dt == CANNIKIN_F32 ? 4 : 2; }
@@ -71,6 +90,7 @@ static cannikin_status create_local(cannikin_ctx** out, int rank, int world, int
   ctx->rank = rank;
   ctx->world = world;
   ctx->check_ratios = (flags & CANNIKIN_INIT_CHECK_RATIOS) ? 1 : 0;
+  ctx->gated = world > 1 && (flags & CANNIKIN_INIT_GATED_ENTRY);
   ctx->device = device;
   cudaError_t ce = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (ce != cudaSuccess) { destroy_partial(ctx); CK_CUDA(ce); }
@@ -138,7 +158,8 @@ extern "C" cannikin_status cannikin_init(cannikin_ctx** out, int rank, int world
                                          int grid, unsigned flags) {
   if (!out) return fail(CANNIKIN_ERR_INVALID, "init: out == NULL");
   *out = nullptr;
-  if (flags & ~CANNIKIN_INIT_CHECK_RATIOS) return fail(CANNIKIN_ERR_INVALID, "init: unknown flags %#x", flags);
+  if (flags & ~(CANNIKIN_INIT_CHECK_RATIOS | CANNIKIN_INIT_GATED_ENTRY))
+    return fail(CANNIKIN_ERR_INVALID, "init: unknown flags %#x", flags);
   if (world < 1 || world > CANNIKIN_MAX_WORLD || rank < 0 || rank >= world)
     return fail(CANNIKIN_ERR_INVALID, "init: rank=%d world=%d (world must be 1..%d)", rank, world,
                 CANNIKIN_MAX_WORLD);
@@ -282,6 +303,7 @@ extern "C" cannikin_status cannikin_free_bucket(cannikin_ctx* ctx, void* dptr) {
 extern "C" cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* bucket, size_t n,
                                                        cannikin_dtype dt, double r_i,
                                                        void* stream) {
+  NvtxRange nvtx_("cannikin_weighted_allreduce", n * (dt == CANNIKIN_F32 ? 4 : 2));
   if (!ctx) return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce: ctx == NULL");
   ctx->last_launches = 0;
   if (dt != CANNIKIN_F32 && dt != CANNIKIN_BF16)
@@ -303,28 +325,35 @@ extern "C" cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* 
     ctx->last_variant = "k2";
     return CANNIKIN_OK;
   }
+  if (bytes > ctx->heap_bytes && !cannikin::ll128_eligible(ctx, bytes) &&
+      !cannikin::ll_eligible(ctx, bytes))
+    return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce: %zu bytes > heap %zu", bytes,
+                ctx->heap_bytes);
+  int gate = 0;
+  if (ctx->gated) {
+    // the long wait for late peers in one warp, not in the data kernel's grid (gate.cu)
+    CK_CUDA(cannikin::launch_gate(ctx, S(stream)));
+    gate = 1;
+  }
   if (cannikin::ll128_eligible(ctx, bytes)) {
     // mid-size bucket: flag-in-line two-shot, no barrier; touches only this rank's bucket
     CK_CUDA(cannikin::launch_ll128(ctx, bucket, n, dt, r_i, S(stream)));
-    ctx->last_launches = 1;
+    ctx->last_launches = 1 + gate;
     ctx->last_variant = "ll128";
     return CANNIKIN_OK;
   }
   if (cannikin::ll_eligible(ctx, bytes)) {
     // small bucket: the LL kernel reads and writes only this rank's bucket (any device memory)
     CK_CUDA(cannikin::launch_ll(ctx, bucket, n, dt, r_i, S(stream)));
-    ctx->last_launches = 1;
+    ctx->last_launches = 1 + gate;
     ctx->last_variant = "ll";
     return CANNIKIN_OK;
   }
-  if (bytes > ctx->heap_bytes)
-    return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce: %zu bytes > heap %zu", bytes,
-                ctx->heap_bytes);
   char* p = static_cast<char*>(bucket);
   char* heap_lo = ctx->base + ctx->user_off;
   if (p >= heap_lo && p + bytes <= heap_lo + ctx->heap_bytes) {
     CK_CUDA(cannikin::launch_twoshot(ctx, p - ctx->base, n, dt, r_i, S(stream)));
-    ctx->last_launches = 1;
+    ctx->last_launches = 1 + gate;
     return CANNIKIN_OK;
   }
   // not peer-mapped: stage through the scratch half of the heap (same offset on every rank)
@@ -332,7 +361,7 @@ extern "C" cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* 
   CK_CUDA(cudaMemcpyAsync(scratch, bucket, bytes, cudaMemcpyDeviceToDevice, S(stream)));
   CK_CUDA(cannikin::launch_twoshot(ctx, ctx->scratch_off, n, dt, r_i, S(stream)));
   CK_CUDA(cudaMemcpyAsync(bucket, scratch, bytes, cudaMemcpyDeviceToDevice, S(stream)));
-  ctx->last_launches = 3;  // copy in, kernel, copy out
+  ctx->last_launches = 3 + gate;  // copy in, kernel, copy out
   return CANNIKIN_OK;
 }
 
@@ -340,6 +369,7 @@ extern "C" cannikin_status cannikin_weighted_allreduce_group(cannikin_ctx* const
                                                              void* const* buckets, size_t n,
                                                              cannikin_dtype dt, const double* r,
                                                              void* stream) {
+  NvtxRange nvtx_("cannikin_weighted_allreduce_group", n * (dt == CANNIKIN_F32 ? 4 : 2));
   if (!ctxs || !buckets || !r) return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_group: NULL argument");
   if (world < 2 || world > CANNIKIN_MAX_WORLD)
     return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_group: world=%d", world);
@@ -432,6 +462,7 @@ extern "C" cannikin_status cannikin_device_status(cannikin_ctx* ctx) {
 
 extern "C" cannikin_status cannikin_gns_stats(cannikin_ctx* ctx, void* stream,
                                               double* out_local_sq, double* out_global_sq) {
+  NvtxRange nvtx_("cannikin_gns_stats", 0);
   if (!ctx || !out_local_sq || !out_global_sq)
     return fail(CANNIKIN_ERR_INVALID, "gns_stats: NULL argument");
   CK_CUDA(cudaSetDevice(ctx->device));
@@ -513,6 +544,7 @@ extern "C" cannikin_status cannikin_weighted_sum_local(cannikin_ctx* ctx, const 
                                                        size_t n, cannikin_dtype dt,
                                                        double* d_local_sq, double* d_global_sq,
                                                        unsigned flags, void* stream) {
+  NvtxRange nvtx_("cannikin_weighted_sum_local", n * (dt == CANNIKIN_F32 ? 4 : 2));
   if (!ctx) return fail(CANNIKIN_ERR_INVALID, "weighted_sum_local: ctx == NULL");
   ctx->last_launches = 0;
   if (dt != CANNIKIN_F32 && dt != CANNIKIN_BF16)
@@ -569,6 +601,7 @@ extern "C" cannikin_status cannikin_ddp_allreduce_mean(cannikin_ctx* ctx, void* 
 extern "C" cannikin_status cannikin_weighted_allreduce_nccl(cannikin_ctx* ctx, void* bucket,
                                                             size_t n, cannikin_dtype dt,
                                                             double r_i, void* stream) {
+  NvtxRange nvtx_("cannikin_weighted_allreduce_nccl", n * (dt == CANNIKIN_F32 ? 4 : 2));
   if (!ctx) return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_nccl: ctx == NULL");
   ctx->last_launches = 0;
   if (dt != CANNIKIN_F32 && dt != CANNIKIN_BF16)
@@ -623,6 +656,7 @@ extern "C" cannikin_status cannikin_weighted_allreduce_nvls(cannikin_ctx* ctx, v
                                                             void* mc_bucket, size_t n,
                                                             cannikin_dtype dt, double r_i,
                                                             void* stream) {
+  NvtxRange nvtx_("cannikin_weighted_allreduce_nvls", n * (dt == CANNIKIN_F32 ? 4 : 2));
   if (!ctx) return fail(CANNIKIN_ERR_INVALID, "weighted_allreduce_nvls: ctx == NULL");
   ctx->last_launches = 0;
   // bf16: the switch's bf16 ld_reduce (SASS HPADD.BF16x8) does not keep the sum within the 1e-2

@@ -29,6 +29,8 @@ struct Ctrl {
   uint64_t rv_word[kMaxArBlocks][kMaxWorld];                 // [peer] entry: (float r_src, epoch32)
   uint64_t meta_word[kMaxArBlocks][kMaxWorld];               // [peer] entry: (bucket hash32, epoch32)
   uint64_t pmid[kMaxArBlocks][kMaxWorld];                    // [peer] push variant: (r_src, epoch32)
+  uint64_t gate[kMaxWorld];                                  // [peer] gated entry: epoch of rank j
+  uint64_t gate_epoch;                                       // [local] gated calls so far
   uint64_t ll_epoch;                                         // [local] LL-kernel call counter
   unsigned ticket_ll;                                        // [local] LL last-CTA ticket
   uint64_t ll128_epoch;                                      // [local] LL128-kernel call counter
@@ -55,6 +57,7 @@ struct cannikin_ctx {
   int ar_dyn = -1;          // CANNIKIN_AR_DYN=0|1 forces static/dynamic chunks; -1 = by size
   int ar_push = -1;         // CANNIKIN_AR_PUSH=0|1 forces pull / push; -1 = by size
   int check_ratios = 0;     // CANNIKIN_INIT_CHECK_RATIOS
+  bool gated = false;       // CANNIKIN_INIT_GATED_ENTRY: one-warp peer wait before each reduction
   int ar_chunk_max = 512 * 16;  // CANNIKIN_AR_CHUNK: dynamic two-shot max chunk (16-B vectors)
   int ar_ll = -1;           // CANNIKIN_AR_LL=0|1 forbids/prefers the LL kernel; -1 = by size
   size_t ll_max_bytes = 0;  // largest LL bucket = its slot payload: 1 MiB / (W - 1), 64 KiB steps

@@ -97,7 +97,7 @@ def ddp_allreduce_mean(ctx: Context, bucket: torch.Tensor, stream=None):
 
 
 def init_distributed_context(heap_bytes: int, grid: int = 0, group=None,
-                             check_ratios: bool = False) -> Context:
+                             check_ratios: bool = False, gated: bool = False) -> Context:
     """Create the ctx of this rank of an initialised torch.distributed group: rank 0 draws the NCCL
     unique id, which is broadcast over the torch process group (plumbing only)."""
     import torch.distributed as dist
@@ -107,7 +107,7 @@ def init_distributed_context(heap_bytes: int, grid: int = 0, group=None,
     dist.broadcast_object_list(obj, src=0, group=group)
     dev = torch.cuda.current_device()
     return Context(rank=rank, world=world, unique_id=obj[0], device=dev, heap_bytes=heap_bytes,
-                   grid=grid, check_ratios=check_ratios)
+                   grid=grid, check_ratios=check_ratios, gated=gated)
 
 
 class McBucket:

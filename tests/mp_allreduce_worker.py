@@ -104,6 +104,9 @@ def main():
     ap.add_argument("--full", default="", choices=["", "c4", "c5"])
     ap.add_argument("--variants", action="store_true")
     ap.add_argument("--mixed", action="store_true")
+    ap.add_argument("--gated", action="store_true",
+                    help="with --mixed: CANNIKIN_INIT_GATED_ENTRY, and one rank arrives late "
+                         "(a 2 ms device busy-wait before its call) at every call")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr = int(os.environ.get("LOCAL_RANK", rank))
@@ -114,7 +117,7 @@ def main():
         # a seeded random sequence of sizes, dtypes and buffer kinds under the automatic variant
         # choice: LL, two-shot pull/dynamic/push and staged calls interleave on one ctx, so the
         # epochs, parities and statistics rows of the different kernels must compose
-        ctx = ta.init_distributed_context(heap_bytes=(24 << 20), grid=args.grid)
+        ctx = ta.init_distributed_context(heap_bytes=(24 << 20), grid=args.grid, gated=args.gated)
         rng = np.random.default_rng(77)
         tdt = {"f32": torch.float32, "bf16": torch.bfloat16}
         for t in range(MIXED_CALLS):
@@ -128,10 +131,15 @@ def main():
             else:
                 x = ta.bucket_tensor(ctx, N, tdt[dtype])
                 x.copy_(to_dev(gs[rank], dtype))
+            torch.cuda.synchronize()
+            if args.gated and rank == t % world:
+                ck.emulate_compute(2e-3, torch.cuda.current_stream().cuda_stream)  # late rank
             ta.weighted_allreduce(ctx, x, b[rank] / sum(b))
+            launches = ctx.last_launch_count()
             loc, glob = ctx.gns_stats()
             np.savez(os.path.join(args.out, f"rank{rank}_mixed_{t}.npz"), out=from_dev(x, dtype),
-                     loc=np.array(loc), glob=glob, N=N, dtype=dtype, b=np.array(b))
+                     loc=np.array(loc), glob=glob, N=N, dtype=dtype, b=np.array(b),
+                     launches=launches, staged=staged)
             if not staged:
                 ta.free_bucket_tensor(ctx, x)
         dist.barrier()

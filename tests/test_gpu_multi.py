@@ -139,10 +139,13 @@ def test_result_bits_independent_of_variant():
                 assert np.array_equal(got, ref), (name, dtype, k)
 
 
-def test_mixed_sequence_of_sizes_dtypes_and_variants():
+@pytest.mark.parametrize("gated", [False, True], ids=["plain", "gated"])
+def test_mixed_sequence_of_sizes_dtypes_and_variants(gated):
     """40 calls of seeded random size (1 .. 5M elements), dtype and buffer kind (heap bucket or
     staged tensor) on ONE ctx under the automatic variant choice: every result matches the oracle,
-    is bitwise identical on every rank, and every call's statistics match the oracle."""
+    is bitwise identical on every rank, and every call's statistics match the oracle.  `gated`:
+    the same with CANNIKIN_INIT_GATED_ENTRY while a different rank arrives 2 ms late at every call
+    (the one-warp gate holds the wait); one extra launch per call is counted."""
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
     world = min(torch.cuda.device_count(), 8)
@@ -150,6 +153,8 @@ def test_mixed_sequence_of_sizes_dtypes_and_variants():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
            os.path.join(os.path.dirname(__file__), "mp_allreduce_worker.py"), "--out", d, "--mixed"]
+    if gated:
+        cmd.append("--gated")
     r = run_torchrun(cmd, capture_output=True, text=True, timeout=900,
                        env=dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000"))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
@@ -168,3 +173,5 @@ def test_mixed_sequence_of_sizes_dtypes_and_variants():
         for k in range(1, world):
             assert np.array_equal(ranks[k]["out"], ranks[0]["out"]), (t, k)
             assert np.array_equal(ranks[k]["loc"], ranks[0]["loc"]), (t, k)
+        # launches of the call: the reduction (+ 2 staging copies) (+ the gate kernel)
+        assert int(ranks[0]["launches"]) in ((2, 4) if gated else (1, 3)), (t, ranks[0]["launches"])

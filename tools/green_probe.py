@@ -32,6 +32,15 @@ def main():
     def mm():
         return a @ a
 
+    # the bench's step_vs_ddp compute: 48 samples x 512 tokens, width 2048
+    h = torch.randn(48 * 512, 2048, device="cuda", dtype=torch.bfloat16)
+    w = torch.randn(2048, 2048, device="cuda", dtype=torch.bfloat16)
+    o = torch.empty_like(h)
+
+    def stack():
+        for _ in range(9):
+            torch.matmul(h, w, out=o)
+
     def rn():
         m(x).sum().backward()
 
@@ -43,6 +52,7 @@ def main():
             print(json.dumps({"num_sms": nsm, "error": str(e)[:200]}), flush=True)
             continue
         print(json.dumps({"num_sms": nsm, "matmul_ms": round(timed(mm, s), 3),
+                          "bench_stack_ms": round(timed(stack, s), 3),
                           "resnet18_b128_fwdbwd_ms": round(timed(rn, s), 3)}), flush=True)
     print(json.dumps({"default_stream": True, "matmul_ms": round(timed(mm, torch.cuda.current_stream()), 3),
                       "resnet18_b128_fwdbwd_ms": round(timed(rn, torch.cuda.current_stream()), 3)}))
