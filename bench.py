@@ -584,17 +584,22 @@ def main():
         out = torch.empty(N, dtype=tdt, device="cuda")
         alg_bytes = (n + 1) * N * s  # K2's HBM algorithmic bytes (roofline)
 
+        # one bucket: its last CTA writes the n+1 statistics straight into pinned host memory
+        # (mapped, device-accessible), no readback copy.  Several buckets: they accumulate in
+        # device memory (a host-memory read-modify-write per bucket would sit on the chain's
+        # critical path) and one 72-byte copy reads them back.
+        st_acc = stats_h if nb == 1 else stats_d
+
         def launch(bi, k):
             a, c = cuts[bi], cuts[bi + 1]
-            # the last CTA writes the n+1 statistics straight into pinned host memory (mapped,
-            # device-accessible): no separate readback copy in the step
             # buckets after the first are PDL-chained (CANNIKIN_LOCAL_CHAIN): their loads start
             # while the previous bucket's last CTAs finish
-            ta.weighted_sum_local(ctx, [g[a:c] for g in gs], r, out[a:c], stats_h[k][:n],
-                                  stats_h[k][n:], accumulate=bi > 0, chain=bi > 0)
+            ta.weighted_sum_local(ctx, [g[a:c] for g in gs], r, out[a:c], st_acc[k][:n],
+                                  st_acc[k][n:], accumulate=bi > 0, chain=bi > 0)
 
         def read_stats(k):
-            pass
+            if nb > 1:
+                stats_h[k].copy_(stats_d[k], non_blocking=True)
     else:
         ctx = ta.init_distributed_context(heap_bytes=N * s, grid=args.grid)
         bucket = ta.bucket_tensor(ctx, N, tdt)

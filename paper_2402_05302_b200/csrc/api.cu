@@ -573,7 +573,7 @@ extern "C" cannikin_status cannikin_weighted_sum_local(cannikin_ctx* ctx, const 
     return fail(CANNIKIN_ERR_INVALID, "weighted_sum_local: unknown flags %#x", flags);
   if (use_tma)
     CK_CUDA(cannikin::launch_wsum_local_tma(ctx, in, n_ranks, r, out, n, dt, d_local_sq,
-                                            d_global_sq, acc, S(stream)));
+                                            d_global_sq, acc, S(stream), chain));
   else
     CK_CUDA(cannikin::launch_wsum_local(ctx, in, n_ranks, r, out, n, dt, d_local_sq, d_global_sq,
                                         acc, ctx->grid_local, S(stream), chain));

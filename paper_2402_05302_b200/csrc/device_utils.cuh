@@ -98,12 +98,13 @@ __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
   return d;
 }
 
-// The emulated-rank pass over one 16-byte vector index (K2, both variants): out = sum_j r_j x_j in
-// rank order from 0 (fp32 fma: the same bits as a scalar fmaf chain), |x_j|^2 and |out|^2 of the
-// vector in fp32 (even and odd elements in two chains, then added), accumulated in fp64.
-template <typename T, int NR, typename A = double>
-__device__ __forceinline__ void wsum16(const uint4 (&x)[NR], const float (&r)[NR], char* dst,
-                                       A (&lsq)[NR], A& gsq) {
+// The emulated-rank pass over one 16-byte vector index (K2, both variants): returns the packed
+// out = sum_j r_j x_j in rank order from 0 (fp32 fma: the same bits as a scalar fmaf chain) and
+// adds |x_j|^2 and |out|^2 of the vector, formed in fp32 (even and odd elements in two chains, then
+// added), to fp64 accumulators.
+template <typename T, int NR>
+__device__ __forceinline__ uint4 wsum16v(const uint4 (&x)[NR], const float (&r)[NR],
+                                         double (&lsq)[NR], double& gsq) {
   using V = Vec<T>;
   constexpr int E = V::E;
   constexpr int P = E / 2;
@@ -122,7 +123,7 @@ __device__ __forceinline__ void wsum16(const uint4 (&x)[NR], const float (&r)[NR
       acc[p] = ffma2(rr, gp, acc[p]);
       sq = ffma2(gp, gp, sq);
     }
-    lsq[j] += (A)(f2lo(sq) + f2hi(sq));
+    lsq[j] += (double)(f2lo(sq) + f2hi(sq));
   }
   uint64_t gs = 0ull;
   float out[E];
@@ -132,8 +133,15 @@ __device__ __forceinline__ void wsum16(const uint4 (&x)[NR], const float (&r)[NR
     out[2 * p] = f2lo(acc[p]);
     out[2 * p + 1] = f2hi(acc[p]);
   }
-  gsq += (A)(f2lo(gs) + f2hi(gs));
-  st16(dst, V::pack(out));
+  gsq += (double)(f2lo(gs) + f2hi(gs));
+  return V::pack(out);
+}
+
+// ... and stores it (streaming 16-byte store).
+template <typename T, int NR>
+__device__ __forceinline__ void wsum16(const uint4 (&x)[NR], const float (&r)[NR], char* dst,
+                                       double (&lsq)[NR], double& gsq) {
+  st16(dst, wsum16v<T, NR>(x, r, lsq, gsq));
 }
 
 // ------------------------------------------------------------------ deterministic reductions

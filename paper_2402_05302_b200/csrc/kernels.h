@@ -40,7 +40,7 @@ cudaError_t launch_wsum_local(cannikin_ctx* ctx, const void* const* in, int nr, 
 cudaError_t launch_wsum_local_tma(cannikin_ctx* ctx, const void* const* in, int nr,
                                   const double* r, void* out, size_t n, cannikin_dtype dt,
                                   double* d_local_sq, double* d_global_sq, bool accumulate,
-                                  cudaStream_t st);
+                                  cudaStream_t st, bool chain = false);
 cudaError_t launch_emulate(double seconds, cudaStream_t st);
 cudaError_t launch_nvls(cannikin_ctx* ctx, void* local, void* mc, size_t n, cannikin_dtype dt,
                         double r_i, cudaStream_t st);

@@ -27,13 +27,6 @@ namespace cannikin {
 #ifndef CANNIKIN_K2_MINB
 #define CANNIKIN_K2_MINB 4
 #endif
-// Build-time experiment: per-thread norm accumulators in fp32 (8 fewer registers for n = 8) --
-// CANNIKIN_K2_LSQ32=1; the default is fp64 beyond one vector.
-#if defined(CANNIKIN_K2_LSQ32) && CANNIKIN_K2_LSQ32
-typedef float LsqT;
-#else
-typedef double LsqT;
-#endif
 template <typename T, int NR, int U, int NT>
 __global__ void __launch_bounds__(NT, NT == 256 && NR <= 8 ? CANNIKIN_K2_MINB : 1)
     wsum_local_kernel(const LocalArgs a) {
@@ -61,10 +54,10 @@ __global__ void __launch_bounds__(NT, NT == 256 && NR <= 8 ? CANNIKIN_K2_MINB : 
     r[j] = a.r[j];
     in[j] = a.in[j];
   }
-  LsqT lsq[NR];
+  double lsq[NR];
 #pragma unroll
-  for (int j = 0; j < NR; ++j) lsq[j] = 0;
-  LsqT gsq = 0;
+  for (int j = 0; j < NR; ++j) lsq[j] = 0.0;
+  double gsq = 0.0;
 
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -92,9 +85,9 @@ __global__ void __launch_bounds__(NT, NT == 256 && NR <= 8 ? CANNIKIN_K2_MINB : 
       for (int j = 0; j < NR; ++j) {
         const float g = V::load1(in[j] + e * sizeof(T));
         acc = fmaf(r[j], g, acc);
-        lsq[j] += (LsqT)(g * g);
+        lsq[j] += (double)(g * g);
       }
-      gsq += (LsqT)(acc * acc);
+      gsq += (double)(acc * acc);
       V::store1(a.out + e * sizeof(T), acc);
     }
   }
@@ -102,8 +95,8 @@ __global__ void __launch_bounds__(NT, NT == 256 && NR <= 8 ? CANNIKIN_K2_MINB : 
   if (threadIdx.x == 0) a.trace[blockIdx.x * 5 + 2] = dev::globaltimer_ns();
   double vals[NR + 1];
 #pragma unroll
-  for (int j = 0; j < NR; ++j) vals[j] = (double)lsq[j];
-  vals[NR] = (double)gsq;
+  for (int j = 0; j < NR; ++j) vals[j] = lsq[j];
+  vals[NR] = gsq;
   dev::block_sum(vals, red);
   // the partial table, the ticket and the (accumulated) statistics are shared with the preceding
   // chained launch: from here on it must have completed

@@ -222,7 +222,10 @@ static cudaError_t dispatch_tma(int nr, const LocalArgs& a, int num_sms, cudaStr
 cudaError_t launch_wsum_local_tma(cannikin_ctx* ctx, const void* const* in, int nr,
                                   const double* r, void* out, size_t n, cannikin_dtype dt,
                                   double* d_local_sq, double* d_global_sq, bool accumulate,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, bool chain) {
+  // a plain launch: stream-ordered after its predecessor, so CANNIKIN_LOCAL_CHAIN is satisfied
+  // trivially (no overlap with the previous bucket, unlike the LDG variant)
+  (void)chain;
   LocalArgs a{};
   for (int j = 0; j < nr; ++j) {
     a.in[j] = static_cast<const char*>(in[j]);

@@ -54,7 +54,7 @@ def main():
     # this rank's local gradient g_i (for |g_i|^2)
     ce(loc_model(Xl), yl).backward()
     gi = flat_grad(loc_model)
-    ctx = ta.init_distributed_context(heap_bytes=64 << 20)
+    ctx = ta.init_distributed_context(heap_bytes=64 << 20, gated=True)  # as ddp_hook.py documents
     ddp = nn.parallel.DistributedDataParallel(model, device_ids=[lr], bucket_cap_mb=4)
     state = CannikinHookState(ctx, b[rank] / B)
     ddp.register_comm_hook(state, cannikin_hook)

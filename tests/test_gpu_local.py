@@ -176,6 +176,34 @@ def test_in_place_and_accumulate(ctx, variant):
     check(gs, r, "f32", ins[0], local, glob)
 
 
+@pytest.mark.parametrize("variant", ["ldg", "tma"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_pdl_chained_buckets(ctx, dtype, variant):
+    """CANNIKIN_LOCAL_CHAIN (the bucketed bench): buckets after the first are launched as
+    programmatic dependents and start reading while the previous bucket finishes; results and the
+    accumulated statistics match the oracle, and the bits equal an unchained run."""
+    N = 5 * 300_007 + 3
+    b = [4, 9, 1, 30]
+    gs = synth.gns_gradients(4, N, b, seed=17, dtype=dtype)
+    r = agg.ratios(b)
+    ins = [to_dev(g, dtype) for g in gs]
+    outs = []
+    for chain in (True, False):
+        out = torch.empty_like(ins[0])
+        local = torch.zeros(4, dtype=torch.float64, device="cuda")
+        glob = torch.zeros(1, dtype=torch.float64, device="cuda")
+        cuts = [0, 300_000, 2 * 300_000 + 8, 3 * 300_000 + 16, 4 * 300_000, N]
+        for i, (a, c) in enumerate(zip(cuts[:-1], cuts[1:])):
+            ta.weighted_sum_local(ctx, [x[a:c] for x in ins], r, out[a:c], local, glob,
+                                  accumulate=i > 0, variant=variant, chain=chain and i > 0)
+        torch.cuda.synchronize()
+        check(gs, r, dtype, out, local, glob)
+        outs.append((out, local.clone(), glob.clone()))
+    v = (lambda t: t.view(torch.int16)) if dtype == "bf16" else (lambda t: t)
+    assert torch.equal(v(outs[0][0]), v(outs[1][0]))
+    assert torch.equal(outs[0][1], outs[1][1]) and torch.equal(outs[0][2], outs[1][2])
+
+
 def test_world1_allreduce_and_stats(ctx):
     N = 123457
     g = synth.gns_gradients(1, N, [8], seed=6)[0]

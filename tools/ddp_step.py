@@ -93,7 +93,9 @@ def main():
     ap.add_argument("--B", type=int, default=512)
     ap.add_argument("--epochs", type=int, default=4)
     ap.add_argument("--iters", type=int, default=10)
-    ap.add_argument("--grid", type=int, default=24)
+    ap.add_argument("--grid", type=int, default=0, help="reduction CTAs (0 = one per SM)")
+    ap.add_argument("--ungated", action="store_true",
+                    help="wait for late peers inside the reduction grid (no gate kernel)")
     ap.add_argument("--model", default="resnet18", choices=["resnet18", "resnet50"])
     ap.add_argument("--img", type=int, default=32)
     ap.add_argument("--hetero", default="delay", choices=["delay", "sm"])
@@ -203,10 +205,11 @@ def main():
     del ddp, opt, model
 
     # ---------------- Cannikin: comm hook + measured-model loop
-    # a reduction that waits for a slower peer spins on its SMs: overlapping it with backprop needs
-    # a small grid (NCCL uses a few channels for the same reason)
+    # gated entry: the wait for a slower peer is done by a one-warp gate kernel, not by the
+    # reduction grid (which would take the SMs of this rank's backward pass)
     # DDP's first iteration reduces the whole gradient as one bucket: heap = gradient bytes
-    ctx = ta.init_distributed_context(heap_bytes=out["params"] * 4 + (1 << 20), grid=args.grid)
+    ctx = ta.init_distributed_context(heap_bytes=out["params"] * 4 + (1 << 20), grid=args.grid,
+                                      gated=not args.ungated)
     state = CannikinHookState(ctx, 1.0 / world, timing=True)
     model, ddp, opt = build(state)
     an = ck.Analyzer(world)
@@ -252,6 +255,7 @@ def main():
         out["prediction_error"] = round(abs(out["predicted_ms"] - out["cannikin_ms"]) / out["cannikin_ms"], 4)
     out["buckets_per_step"] = len(state.events)
     out["k3_grid"] = args.grid
+    out["gated_entry"] = not args.ungated
     if rank == 0:
         print(json.dumps({"summary": out}), flush=True)
     dist.barrier()
