@@ -68,9 +68,15 @@ def main():
     torch.cuda.synchronize()
     got = flat_grad(model)
     loc, glob = ctx.gns_stats()
+    # a third iteration read through the hook state's own ordering (no host synchronisation
+    # between backward and the read: state.gns_stats() orders itself after DDP's last bucket)
+    model.zero_grad(set_to_none=False)
+    ce(ddp(Xl), yl).backward()
+    hloc, hglob = state.gns_stats()
     np.savez(os.path.join(args.out, f"rank{rank}.npz"), got=got.cpu().numpy(), ref=ref.cpu().numpy(),
-             gi_sq=float((gi.double() ** 2).sum()), loc=np.array(loc), glob=glob,
-             buckets=state.buckets, b=np.array(b))
+             gi=gi.cpu().numpy(), gi_sq=float((gi.double() ** 2).sum()), loc=np.array(loc),
+             glob=glob, buckets=state.buckets, hook_loc=np.array(hloc), hook_glob=hglob,
+             b=np.array(b))
     dist.barrier()
     ctx.close()
     dist.destroy_process_group()

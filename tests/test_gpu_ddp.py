@@ -15,6 +15,8 @@ torch = pytest.importorskip("torch")
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from launch import run_torchrun  # noqa: E402
 
+from oracle import aggregate as agg  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 
 
@@ -26,10 +28,7 @@ def _port():
     return p
 
 
-def test_ddp_hook_equals_full_batch_gradient():
-    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
-        pytest.skip("needs >= 2 GPUs")
-    world = min(torch.cuda.device_count(), 8)
+def _run(world):
     d = tempfile.mkdtemp()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
@@ -37,7 +36,43 @@ def test_ddp_hook_equals_full_batch_gradient():
     r = run_torchrun(cmd, capture_output=True, text=True, timeout=900,
                        env=dict(os.environ, CANNIKIN_SPIN_TIMEOUT_MS="20000"))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    ranks = [dict(np.load(os.path.join(d, f"rank{k}.npz"))) for k in range(world)]
+    return [dict(np.load(os.path.join(d, f"rank{k}.npz"))) for k in range(world)]
+
+
+def _check_oracle(ranks):
+    """Every rank's hook result against the oracle's Eq. 9 of the ranks' local gradients (Q1
+    metric, fp32 1e-5) and the hook statistics against the oracle's norms (1e-4)."""
+    b = [int(x) for x in ranks[0]["b"]]
+    gs = [rk["gi"] for rk in ranks]
+    r = agg.ratios(b)
+    g_ref, ls_ref, gsq_ref = agg.aggregate(gs, r, "f32")
+    scale = np.maximum(agg.elementwise_scale([agg.to_f64(g, "f32") for g in gs], r), 1e-30)
+    for rk in ranks:
+        err = np.max(np.abs(rk["got"].astype(np.float64) - g_ref) / scale)
+        assert err <= 1e-5, err
+        for key_l, key_g in (("loc", "glob"), ("hook_loc", "hook_glob")):
+            assert np.allclose(rk[key_l], ls_ref, rtol=1e-4, atol=0), (key_l, rk[key_l], ls_ref)
+            assert abs(float(rk[key_g]) - gsq_ref) <= 1e-4 * gsq_ref
+
+
+def test_ddp_hook_single_gpu():
+    """World 1 (the driver's one-GPU run): the hook's reduction is K2 with r = 1 -- the result is
+    the local gradient, the statistics its norm, read both after a host sync and through
+    CannikinHookState.gns_stats() -- against the oracle."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    ranks = _run(1)
+    assert int(ranks[0]["buckets"]) >= 2
+    assert np.array_equal(ranks[0]["got"], ranks[0]["gi"])  # r = 1: g = fmaf(1, g_0, 0) exactly
+    _check_oracle(ranks)
+
+
+def test_ddp_hook_equals_full_batch_gradient():
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(torch.cuda.device_count(), 8)
+    ranks = _run(world)
+    _check_oracle(ranks)
     ref = ranks[0]["ref"].astype(np.float64)
     scale = np.max(np.abs(ref))
     for k in range(world):
