@@ -182,7 +182,8 @@ cannikin_status cannikin_weighted_allreduce(cannikin_ctx* ctx, void* bucket, siz
  * star's "NCCL reduce-scatter/all-gather with the r_i scaling and norm partials fused into the
  * pre- and post-kernels"): pre-kernel y = r_i g_i in fp32 + |g_i|^2 partials -> ncclReduceScatter
  * (fp32 sum) -> post-kernel (one rounding to dt, |g|^2 partials) -> ncclAllGather of the shards
- * and of the 2 statistics per rank -> fixed-order accumulation (identical bits on every rank).
+ * and of the 2 statistics and the fp32 share per rank -> fixed-order accumulation (identical bits
+ * on every rank; with CANNIKIN_INIT_CHECK_RATIOS the gathered shares are checked to sum to 1).
  * Same arguments, contract and statistics as cannikin_weighted_allreduce (Eq. 9, P:328-331;
  * Eq. 10 inputs), except: the fp32 summation order is NCCL's, so the result bits differ
  * from the peer-memory kernels by fp32 rounding (same tolerances); the bucket may be any device

@@ -10,10 +10,11 @@
 //   ncclReduceScatter(y, sum, fp32), in place: rank k owns y[k L, (k+1) L)      (Eq. 9)
 //   post:       round the owned shard once to the bucket dtype; per-CTA partials of |g|^2 from
 //               the fp32 sums
-//   stats:      one CTA sums both partial tables in fixed order -> x = {|g_i|^2, |g|^2_shard}
-//   ncclAllGather(x, 2 doubles) and ncclAllGather(shard, L elements of the bucket dtype)
+//   stats:      one CTA sums both partial tables in fixed order -> x = {|g_i|^2, |g|^2_shard, r_i}
+//   ncclAllGather(x, 3 doubles) and ncclAllGather(shard, L elements of the bucket dtype)
 //   add:        every rank adds |g_j|^2 = x_j[0] and |g|^2 = sum_k x_k[1] (rank order) to the
-//               ctx accumulator: identical bits on every rank.
+//               ctx accumulator: identical bits on every rank; with CANNIKIN_INIT_CHECK_RATIOS it
+//               also checks sum_k x_k[2] (the fp32 shares NCCL scaled with) against 1.
 // The fp32 sum's order is NCCL's (ring/tree), not rank order, so the result bits differ from the
 // K3 variants by fp32 rounding (within the fp32 1e-5 / bf16 1e-2 tolerances; tests/).  NVLink
 // bytes: the reduce-scatter moves fp32 even for bf16 buckets (2x the all-gather's bytes), the
@@ -110,10 +111,10 @@ __global__ void __launch_bounds__(kK4Threads) k4_post_kernel(const float* shard,
   if (threadIdx.x == 0) part[blockIdx.x] = v1[0];
 }
 
-// x = {sum of the pre partials, sum of the post partials}, fixed order
+// x = {sum of the pre partials, sum of the post partials, r_i}, fixed order
 __global__ void __launch_bounds__(kK4Threads) k4_stats_kernel(const double* pre, int npre,
                                                               const double* post, int npost,
-                                                              double* x) {
+                                                              float r, double* x) {
   __shared__ double red[64];
   double v[2] = {0.0, 0.0};
   for (int i = threadIdx.x; i < npre; i += kK4Threads) v[0] += pre[i];
@@ -122,18 +123,26 @@ __global__ void __launch_bounds__(kK4Threads) k4_stats_kernel(const double* pre,
   if (threadIdx.x == 0) {
     x[0] = v[0];
     x[1] = v[1];
+    x[2] = (double)r;
   }
 }
 
-// ctx accumulator (running row 0) += {|g_j|^2 = xr[2j]}, |g|^2 = sum_k xr[2k+1] in rank order
-__global__ void k4_add_kernel(const double* xr, int W, Ctrl* c) {
+// ctx accumulator (running row 0) += {|g_j|^2 = xr[3j]}, |g|^2 = sum_k xr[3k+1] in rank order;
+// check_r: the ranks' fp32 shares xr[3k+2] must sum to 1 within 2^-23 (as the K3 variants check;
+// a violation is recorded as code 7 and reported as DOMAIN, the reduction still runs)
+__global__ void k4_add_kernel(const double* xr, int W, Ctrl* c, int check_r) {
   if (threadIdx.x != 0) return;
-  double gs = 0.0;
+  double gs = 0.0, rs = 0.0;
   for (int k = 0; k < W; ++k) {
-    c->cta_acc[0][k] = c->cta_acc[0][k] + xr[2 * k];
-    gs += xr[2 * k + 1];
+    c->cta_acc[0][k] = c->cta_acc[0][k] + xr[3 * k];
+    gs += xr[3 * k + 1];
+    rs += xr[3 * k + 2];
   }
   c->cta_acc[0][W] = c->cta_acc[0][W] + gs;
+  if (check_r && fabs(rs - 1.0) > 0x1p-23) {
+    c->rsum_bad = rs;
+    atomicCAS(&c->error_code, 0, 7);
+  }
 }
 
 static int k4_grid(const cannikin_ctx* ctx, size_t vecs) {
@@ -147,7 +156,7 @@ static int k4_grid(const cannikin_ctx* ctx, size_t vecs) {
 size_t k4_buffer_bytes(int world, size_t n) {
   const size_t L = ((n + world - 1) / world + 7) / 8 * 8;
   const size_t padded = L * world;
-  return padded * 4 + padded * 4 /* gather (<= fp32) */ + (2 * kK4MaxBlocks + 2 + 2 * kMaxWorld) * 8;
+  return padded * 4 + padded * 4 /* gather (<= fp32) */ + (2 * kK4MaxBlocks + 3 + 3 * kMaxWorld) * 8;
 }
 
 #define K4_CUDA(expr)                                                                        \
@@ -177,7 +186,7 @@ cannikin_status launch_k4(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dt
   double* pre = reinterpret_cast<double*>(gbuf + padded * 4);
   double* post = pre + kK4MaxBlocks;
   double* xs = post + kK4MaxBlocks;
-  double* xr = xs + 2;
+  double* xr = xs + 3;
   ncclComm_t comm = static_cast<ncclComm_t>(ctx->nccl_comm);
   const ncclDataType_t ndt = dt == CANNIKIN_F32 ? ncclFloat32 : ncclBfloat16;
   const size_t cnt = n > me * L ? (n - me * L < L ? n - me * L : L) : 0;
@@ -215,13 +224,13 @@ cannikin_status launch_k4(cannikin_ctx* ctx, void* bucket, size_t n, cannikin_dt
     else
       k4_post_kernel<__nv_bfloat16><<<gpost, kK4Threads, 0, st>>>(y + me * L, cnt, dst, post);
   }
-  k4_stats_kernel<<<1, kK4Threads, 0, st>>>(pre, gpre, post, gpost, xs);
+  k4_stats_kernel<<<1, kK4Threads, 0, st>>>(pre, gpre, post, gpost, (float)r_i, xs);
   K4_CUDA(cudaGetLastError());
   K4_NCCL(ncclGroupStart());
-  K4_NCCL(ncclAllGather(xs, xr, 2, ncclFloat64, comm, st));
+  K4_NCCL(ncclAllGather(xs, xr, 3, ncclFloat64, comm, st));
   K4_NCCL(ncclAllGather(dst, direct ? bucket : static_cast<void*>(gbuf), L, ndt, comm, st));
   K4_NCCL(ncclGroupEnd());
-  k4_add_kernel<<<1, 32, 0, st>>>(xr, W, ctx->ctrl);
+  k4_add_kernel<<<1, 32, 0, st>>>(xr, W, ctx->ctrl, ctx->check_ratios);
   K4_CUDA(cudaGetLastError());
   if (!direct) K4_CUDA(cudaMemcpyAsync(bucket, gbuf, n * esz, cudaMemcpyDeviceToDevice, st));
   ctx->last_launches = 5;
