@@ -371,6 +371,36 @@ class ClockSampler:
 BIDIR_WRITE_GBS = {2: 690.8, 4: 671.4}
 
 
+def a2a_ceiling(ctx, heap_bytes, n, steps, busbw, barrier, stream, dist, torch):
+    """The all-to-all peer-write ceiling of this box at this N, measured live with
+    cannikin_probe_a2a_write (every rank writes heap/n bytes into every peer at once; per-direction
+    GB/s = (n-1) x bytes / time, max over ranks); falls back to the earlier tools/nvlink_bw.cu
+    figures if the probe is unavailable."""
+    try:
+        per = (heap_bytes // n) // 16 * 16
+        for _ in range(2):
+            ctx.probe_a2a_write(per, stream.cuda_stream)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(3, min(steps, 20))
+        e0.record(stream)
+        for _ in range(reps):
+            ctx.probe_a2a_write(per, stream.cuda_stream)
+        e1.record(stream)
+        barrier()
+        t = torch.tensor([e0.elapsed_time(e1) / reps], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gbs = (n - 1) * per / (float(t.item()) * 1e-3) / 1e9
+        return {"peak": round(gbs, 1), "frac": round(busbw / gbs, 4),
+                "kind": f"live {n}-GPU all-to-all peer writes per direction "
+                        f"(cannikin_probe_a2a_write, {per >> 20} MiB per peer, this run)"}
+    except Exception as e:  # noqa: BLE001
+        if n not in BIDIR_WRITE_GBS:
+            return {"unavailable": str(e)[:200]}
+        return {"peak": BIDIR_WRITE_GBS[n], "frac": round(busbw / BIDIR_WRITE_GBS[n], 4),
+                "kind": f"earlier {n}-GPU all-to-all write probe (tools/nvlink_bw.cu)"}
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -739,10 +769,9 @@ def main():
                 "kernel_ms": round(kmean, 4), "kernel_ms_dist": kdist,
                 "traffic": ncu_traffic(f"{args.config}_w{n}_{cfg['dtype']}"),
                 # an all-reduce loads BOTH directions at once; the same SM-driven copy with both
-                # directions busy peaks lower than the one-way 770 (tools/nvlink_bw.cu)
-                "bidir_ceiling": None if n not in BIDIR_WRITE_GBS else {
-                    "peak": BIDIR_WRITE_GBS[n], "frac": round(busbw / BIDIR_WRITE_GBS[n], 4),
-                    "kind": f"measured {n}-GPU all-to-all peer writes per direction"}}
+                # directions busy peaks lower than the one-way 770: measured live, this run
+                "bidir_ceiling": a2a_ceiling(ctx, N * s, n, args.steps, busbw, barrier, stream,
+                                             dist, torch)}
 
     # ---- DDP baseline (equal split, NCCL average) on the same bucket, N > 1
     ddp = None

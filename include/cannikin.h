@@ -284,6 +284,16 @@ cannikin_status cannikin_ddp_allreduce_mean(cannikin_ctx* ctx, void* bucket, siz
  * P:158-165) on homogeneous GPUs, as Cluster C's dummy load does.  Errors: DOMAIN, CUDA. */
 cannikin_status cannikin_emulate_compute(double seconds, void* stream);
 
+/* Bench utility (not part of the method): the NVLink ceiling K3 runs against, measured on this
+ * ctx's peer mappings.  Every rank writes `bytes_per_peer` bytes of its heap into its own slot of
+ * EVERY peer's scratch half at once (the all-to-all write pattern of a two-shot all-reduce, both
+ * directions of every link loaded); per-direction GB/s = (world-1) * bytes_per_peer / elapsed.
+ * COLLECTIVE (every rank, the same bytes_per_peer, no reduction in flight: it overwrites the
+ * peers' scratch = staging area).  bytes_per_peer: a multiple of 16, world * bytes_per_peer <=
+ * heap_bytes.  Enqueued on `stream`, no synchronisation (time it with events and a barrier).
+ * Errors: INVALID (world == 1, in-process group, size), CUDA. */
+cannikin_status cannikin_probe_a2a_write(cannikin_ctx* ctx, size_t bytes_per_peer, void* stream);
+
 /* Diagnostics (tracing): per-CTA device timeline of the last two-shot (world > 1) or emulated-rank
  * (LDG variant) kernel on this ctx, %globaltimer ns: [start, entry barrier passed (two-shot only),
  * data done, exit barrier passed / partials written, end (last CTA only)] (LL128: [start,

@@ -632,6 +632,22 @@ extern "C" int cannikin_last_launch_count(cannikin_ctx* ctx) { return ctx ? ctx-
 
 extern "C" const char* cannikin_last_variant(cannikin_ctx* ctx) { return ctx ? ctx->last_variant : ""; }
 
+extern "C" cannikin_status cannikin_probe_a2a_write(cannikin_ctx* ctx, size_t bytes_per_peer,
+                                                    void* stream) {
+  if (!ctx) return fail(CANNIKIN_ERR_INVALID, "probe_a2a_write: ctx == NULL");
+  if (ctx->world < 2 || ctx->in_process)
+    return fail(CANNIKIN_ERR_INVALID, "probe_a2a_write: needs a multi-process ctx (world > 1)");
+  if (bytes_per_peer == 0 || bytes_per_peer % 16 ||
+      (size_t)ctx->world * bytes_per_peer > ctx->heap_bytes)
+    return fail(CANNIKIN_ERR_INVALID, "probe_a2a_write: %zu bytes per peer (heap %zu, world %d)",
+                bytes_per_peer, ctx->heap_bytes, ctx->world);
+  CK_CUDA(cudaSetDevice(ctx->device));
+  CK_CUDA(cannikin::launch_a2a_write(ctx, bytes_per_peer, S(stream)));
+  ctx->last_launches = 1;
+  ctx->last_variant = "a2a_write_probe";
+  return CANNIKIN_OK;
+}
+
 extern "C" cannikin_status cannikin_emulate_compute(double seconds, void* stream) {
   if (!(seconds >= 0.0) || seconds > 60.0)
     return fail(CANNIKIN_ERR_DOMAIN, "emulate_compute: %g s outside [0, 60]", seconds);

@@ -257,6 +257,16 @@ def main():
             np.array([chk["ok_val"], chk["bad_val"], chk["ok_after_val"]]))
     dist.barrier()
     ctx2.close()
+    # the bench's live NVLink ceiling probe runs (collective) and leaves the ctx usable
+    ctx.probe_a2a_write(1 << 20)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = ta.bucket_tensor(ctx, 4099, torch.float32)
+    t.fill_(float(rank + 1))
+    ta.weighted_allreduce(ctx, t, 1.0 / world)
+    ctx.gns_stats()
+    np.save(os.path.join(args.out, f"rank{rank}_probe.npy"), t.cpu().numpy())
+    ta.free_bucket_tensor(ctx, t)
     # DDP baseline semantics: mean of the ranks' buffers
     x = torch.full((1000,), float(rank + 1), device="cuda")
     ta.ddp_allreduce_mean(ctx, x)

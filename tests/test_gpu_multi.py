@@ -96,6 +96,15 @@ def test_ddp_baseline_mean(results):
     assert np.allclose(x, (world + 1) / 2)
 
 
+def test_probe_then_reduce(results):
+    """cannikin_probe_a2a_write (the bench's live NVLink ceiling) runs collectively and a reduction
+    right after it is correct: mean of rank+1 over the ranks."""
+    world, d = results
+    for r in range(world):
+        x = np.load(os.path.join(d, f"rank{r}_probe.npy"))
+        assert np.allclose(x, (world + 1) / 2, rtol=1e-6)
+
+
 def test_no_out_of_bounds_writes(results):
     """Guard bands around heap buckets (compute-sanitizer is closed on this pool)."""
     world, d = results
