@@ -36,13 +36,15 @@ for stage in "$@"; do
       timeout 600 python bench.py --bucket-mb 25 > gpurun_out/bench_b25.jsonl 2> gpurun_out/bench_b25.err
       echo "bench b25 exit $?"; tail -1 gpurun_out/bench_b25.jsonl | cut -c1-400 ;;
     launches_bench)
+      timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_plain.log 2>&1 &&
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-        --log-file gpurun_out/launches_bench.csv python bench.py --steps 3 --warmup 3 \
+        --log-file gpurun_out/launches_bench.csv python bench.py --steps 3 --warmup 3 --no-cpu \
         > gpurun_out/launches_bench.log 2>&1
       echo "ncu bench launches exit $?" ;;
     ncu_k2)
+      timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_plain2.log 2>&1 &&
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:wsum_local -s 3 -c 1 \
-        -o gpurun_out/ncu_k2 -f python bench.py --steps 3 --warmup 3 > gpurun_out/ncu_k2.log 2>&1
+        -o gpurun_out/ncu_k2 -f python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_k2.log 2>&1
       echo "ncu k2 exit $?" ;;
     bench_multi)
       timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 \
