@@ -32,8 +32,6 @@ def main():
     ap.add_argument("--grids", default="0,148,296,444,592,740,888")
     ap.add_argument("--altu-grids", default="0")
     ap.add_argument("--tma", type=int, default=1)
-    ap.add_argument("--tails", default="",
-                    help="CANNIKIN_K2_TAIL percentages (an experiment that was reverted; see DESIGN)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     want = args.shapes.split(",")
@@ -46,18 +44,13 @@ def main():
         out = torch.empty_like(gs[0])
         st = torch.zeros(nr + 1, dtype=torch.float64, device="cuda")
         nbytes = (nr + 1) * N * (4 if dt == "f32" else 2)
-        variants = [("tma", None, 0, 1)] if args.tma else []
-        variants += [("ldg", int(g), 0, dyn) for g in args.grids.split(",") for dyn in (1, 0)]
-        variants += [("ldg", int(g), 1, 1) for g in args.altu_grids.split(",") if g]
-        if args.tails:
-            variants = [("ldg", 0, 0, -int(t) - 1) for t in args.tails.split(",")]
-        for var, grid, altu, dyn in variants:
-            tail = -dyn - 1 if dyn < 0 else 0
-            os.environ["CANNIKIN_K2_TAIL"] = str(tail)
+        variants = [("tma", None, 0)] if args.tma else []
+        variants += [("ldg", int(g), 0) for g in args.grids.split(",")]
+        variants += [("ldg", int(g), 1) for g in args.altu_grids.split(",") if g]
+        for var, grid, altu in variants:
             if grid is not None:
                 os.environ["CANNIKIN_LOCAL_GRID"] = str(grid)
             os.environ["CANNIKIN_K2_NT"] = "1024" if altu else "256"
-            os.environ["CANNIKIN_K2_DYN"] = str(dyn)
             ctx = ck.Context(world=1, device=0)
             for _ in range(3):
                 ta.weighted_sum_local(ctx, gs, r, out, st[:nr], st[nr:], variant=var)
@@ -77,7 +70,7 @@ def main():
                 times += [a.elapsed_time(c) for a, c in evs]
             t = statistics.median(times)
             print(json.dumps({"shape": name, "ranks": nr, "N": N, "dtype": dt, "variant": var,
-                              "grid": grid, "alt_u": altu, "dyn": dyn, "tail_pct": tail,
+                              "grid": grid, "nt1024": altu,
                               "ms": round(t, 4),
                               "GBps": round(nbytes / (t * 1e-3) / 1e9, 1)}), flush=True)
             del g
