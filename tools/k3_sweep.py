@@ -54,6 +54,7 @@ def main():
     ap.add_argument("--sizes-mb", default="1,4,16,64,256,1024")
     ap.add_argument("--total", type=int, default=TOTAL)
     ap.add_argument("--nvls", action="store_true", help="also time the NVLS kernel (fp32)")
+    ap.add_argument("--gated", default="0", help="0, 1 or 0,1: CANNIKIN_INIT_GATED_ENTRY")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     lr = int(os.environ.get("LOCAL_RANK", rank))
@@ -64,8 +65,9 @@ def main():
     N = args.total
     b = list(range(1, world + 1))
     r = b[rank] / sum(b)
-    combos = [(int(g), v) for g in args.grids.split(",") for v in args.variants.split(",")]
-    for grid, var in combos:
+    combos = [(int(g), v, int(gt)) for g in args.grids.split(",") for v in args.variants.split(",")
+              for gt in args.gated.split(",")]
+    for grid, var, gated in combos:
         knobs = ("CANNIKIN_AR_PUSH", "CANNIKIN_AR_DYN", "CANNIKIN_AR_LL", "CANNIKIN_AR_LL128")
         if var == "auto":
             for k in knobs:
@@ -80,7 +82,7 @@ def main():
                 os.environ["CANNIKIN_AR_PUSH"] = "1"
             elif var != "k4":
                 os.environ["CANNIKIN_AR_DYN"] = var
-        ctx = ta.init_distributed_context(heap_bytes=N * s, grid=grid)
+        ctx = ta.init_distributed_context(heap_bytes=N * s, grid=grid, gated=bool(gated))
         bucket = ta.bucket_tensor(ctx, N, tdt)
         mcb = ta.McBucket(N, tdt) if args.nvls else None
         if mcb is not None:
@@ -118,6 +120,7 @@ def main():
             bus = lambda t: N * s / (t * 1e-3) * 2 * (world - 1) / world / 1e9  # noqa: E731
             if rank == 0:
                 print(json.dumps({"world": world, "dtype": args.dtype, "grid": grid, "variant": var,
+                                  "gated": bool(gated),
                                   "bucket_MB": mb, "buckets": nb, "total_MB": round(N * s / 2**20),
                                   "ours_ms": round(t_ours, 4), "nccl_ms": round(t_nccl, 4),
                                   "ours_busbw": round(bus(t_ours), 1),
