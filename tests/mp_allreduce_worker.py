@@ -58,9 +58,10 @@ def from_dev(t, dtype):
     return t.cpu().numpy()
 
 
-FULL = {  # BASELINE configs at full size in the bench launch configuration: (N, dtype, seed)
-    "c4": (110_000_000, "bf16", 9),
-    "c5": (354_823_168, "f32", 19),
+FULL = {  # BASELINE configs at full size in the bench launch configurations: (N, dtype, seed, MB)
+    "c4": (110_000_000, "bf16", 9, 0),
+    "c5": (354_823_168, "f32", 19, 0),
+    "c4b25": (110_000_000, "bf16", 9, 25),  # the bench's bucketed_25mb sidecar: 9 calls (LL128)
 }
 
 
@@ -72,7 +73,7 @@ def full_case(ctx, rank, world, out, cfg):
     norms; every rank saves its statistics."""
     import parity
 
-    N, dt, seed = FULL[cfg]
+    N, dt, seed, bucket_mb = FULL[cfg]
     tdt = torch.bfloat16 if dt == "bf16" else torch.float32
     b = b_for(world, seed)
     B = sum(b)
@@ -82,7 +83,14 @@ def full_case(ctx, rank, world, out, cfg):
     ins = [torch.empty_like(g) for _ in range(world)]
     dist.all_gather(ins, g)  # plumbing: every rank's input of record, for the oracle on rank 0
     del g
-    ta.weighted_allreduce(ctx, bucket, b[rank] / B)
+    if bucket_mb == 0:
+        ta.weighted_allreduce(ctx, bucket, b[rank] / B)
+    else:
+        be = int(bucket_mb * 2**20) // (2 if dt == "bf16" else 4)
+        be -= be % 8
+        cuts = list(range(0, N, be)) + [N]
+        for a, c in zip(cuts[:-1], cuts[1:]):
+            ta.weighted_allreduce(ctx, bucket[a:c], b[rank] / B)
     loc, glob = ctx.gns_stats()
     outs = [torch.empty_like(bucket) for _ in range(world)]
     dist.all_gather(outs, bucket)
@@ -101,7 +109,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", required=True)
     ap.add_argument("--grid", type=int, default=0)
-    ap.add_argument("--full", default="", choices=["", "c4", "c5"])
+    ap.add_argument("--full", default="", choices=["", "c4", "c5", "c4b25"])
     ap.add_argument("--variants", action="store_true")
     ap.add_argument("--mixed", action="store_true")
     ap.add_argument("--gated", action="store_true",
@@ -169,7 +177,7 @@ def main():
         dist.destroy_process_group()
         return
     if args.full:
-        N, dt, _ = FULL[args.full]
+        N, dt, _, _ = FULL[args.full]
         ctx = ta.init_distributed_context(heap_bytes=N * (2 if dt == "bf16" else 4) + 4096,
                                           grid=args.grid)
         full_case(ctx, rank, world, args.out, args.full)

@@ -257,12 +257,13 @@ def test_errors(ctx):
     assert e.value.name == "UNSUPPORTED"
 
 
-@pytest.mark.parametrize("variant", ["ldg", "tma"])
+@pytest.mark.parametrize("variant,bucket_mb", [("ldg", 0), ("tma", 0), ("ldg", 25)])
 @pytest.mark.parametrize("nr", [8])
-def test_full_size_c4(ctx, nr, variant):
-    """configs[3] at full size in the bench launch configuration: 110M bf16, 8 emulated ranks.
-    EVERY element against the oracle (chunked, tests/parity.py); the norms against the oracle
-    over the whole vectors."""
+def test_full_size_c4(ctx, nr, variant, bucket_mb):
+    """configs[3] at full size in the bench launch configurations: 110M bf16, 8 emulated ranks, as
+    one launch and (bench --bucket-mb 25) as 9 PDL-chained 25 MB buckets accumulating the
+    statistics.  EVERY element against the oracle (chunked, tests/parity.py); the norms against
+    the oracle over the whole vectors."""
     N = 110_000_000
     b = [37, 29, 21, 12, 9, 8, 3, 1]
     gs = synth.device_gns_gradients(nr, N, b, seed=0, dtype="bf16")
@@ -270,7 +271,15 @@ def test_full_size_c4(ctx, nr, variant):
     out = torch.empty(N, dtype=torch.bfloat16, device="cuda")
     local = torch.zeros(nr, dtype=torch.float64, device="cuda")
     glob = torch.zeros(1, dtype=torch.float64, device="cuda")
-    ta.weighted_sum_local(ctx, gs, r, out, local, glob, variant=variant)
+    if bucket_mb == 0:
+        ta.weighted_sum_local(ctx, gs, r, out, local, glob, variant=variant)
+    else:
+        be = int(bucket_mb * 2**20) // 2
+        be -= be % 8
+        cuts = list(range(0, N, be)) + [N]
+        for i, (a, c) in enumerate(zip(cuts[:-1], cuts[1:])):
+            ta.weighted_sum_local(ctx, [g[a:c] for g in gs], r, out[a:c], local, glob,
+                                  accumulate=i > 0, chain=i > 0, variant=variant)
     torch.cuda.synchronize()
     _, lsum, gsum = parity.compare_full([out], gs, r, "bf16", TOL["bf16"], chunk=10_000_000)
     assert np.allclose(local.cpu().numpy(), lsum, rtol=1e-4)

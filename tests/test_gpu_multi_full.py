@@ -1,5 +1,6 @@
 """Multi-GPU parity at full size in the bench launch configuration (zero-copy heap bucket, default
-grid) for configs[3] (110M bf16) and configs[4] (355M fp32, one 1.42 GB bucket): EVERY element
+grid) for configs[3] (110M bf16, one bucket, and the bench's 25 MB buckets) and configs[4]
+(355M fp32, one 1.42 GB bucket): EVERY element
 against the oracle (chunked, in the worker's rank 0; the other ranks' results bitwise equal to
 rank 0's), the norm statistics against the oracle over the whole vectors, identical statistics on
 every rank."""
@@ -28,10 +29,10 @@ def _port():
     return p
 
 
-TOL = {"c4": ("bf16", 1e-2), "c5": ("f32", 1e-5)}
+TOL = {"c4": ("bf16", 1e-2), "c5": ("f32", 1e-5), "c4b25": ("bf16", 1e-2)}
 
 
-@pytest.mark.parametrize("cfg", ["c4", "c5"])
+@pytest.mark.parametrize("cfg", ["c4", "c5", "c4b25"])
 def test_full_size_multi(cfg):
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
