@@ -287,12 +287,16 @@ cannikin_status cannikin_emulate_compute(double seconds, void* stream);
 /* Bench utility (not part of the method): the NVLink ceiling K3 runs against, measured on this
  * ctx's peer mappings.  Every rank writes `bytes_per_peer` bytes of its heap into its own slot of
  * EVERY peer's scratch half at once (the all-to-all write pattern of a two-shot all-reduce, both
- * directions of every link loaded); per-direction GB/s = (world-1) * bytes_per_peer / elapsed.
+ * directions of every link loaded), `repeat` times over the same ranges in one launch (1..1024:
+ * long transfers amortise the launch and ramp), by ctas_per_sm (1..4) x SMs CTAs of 512 threads,
+ * each writing to every peer in turn; per-direction GB/s = (world-1) * bytes_per_peer * repeat /
+ * elapsed.
  * COLLECTIVE (every rank, the same bytes_per_peer, no reduction in flight: it overwrites the
  * peers' scratch = staging area).  bytes_per_peer: a multiple of 16, world * bytes_per_peer <=
  * heap_bytes.  Enqueued on `stream`, no synchronisation (time it with events and a barrier).
- * Errors: INVALID (world == 1, in-process group, size), CUDA. */
-cannikin_status cannikin_probe_a2a_write(cannikin_ctx* ctx, size_t bytes_per_peer, void* stream);
+ * Errors: INVALID (world == 1, in-process group, size, repeat, ctas_per_sm), CUDA. */
+cannikin_status cannikin_probe_a2a_write(cannikin_ctx* ctx, size_t bytes_per_peer, int repeat,
+                                         int ctas_per_sm, void* stream);
 
 /* Diagnostics (tracing): per-CTA device timeline of the last two-shot (world > 1) or emulated-rank
  * (LDG variant) kernel on this ctx, %globaltimer ns: [start, entry barrier passed (two-shot only),

@@ -108,7 +108,7 @@ SIGNATURES = {
     "cannikin_last_launch_count": (_I, [_P]),
     "cannikin_last_variant": (ctypes.c_char_p, [_P]),
     "cannikin_emulate_compute": (_I, [_D, _P]),
-    "cannikin_probe_a2a_write": (_I, [_P, _Z, _P]),
+    "cannikin_probe_a2a_write": (_I, [_P, _Z, _I, _I, _P]),
     "cannikin_trace": (_I, [_P, ctypes.POINTER(ctypes.c_uint64), _I, _IP]),
     "cannikin_gns_estimate": (_I, [_DP, _D, _LP, _I, ctypes.POINTER(_GnsResult)]),
     "cannikin_gns_estimate_corrected": (_I, [_DP, _D, _LP, _I, ctypes.POINTER(_GnsResult)]),
@@ -293,9 +293,11 @@ class Context:
     def last_variant(self) -> str:
         return lib().cannikin_last_variant(self._h).decode()
 
-    def probe_a2a_write(self, bytes_per_peer: int, stream=None):
+    def probe_a2a_write(self, bytes_per_peer: int, repeat: int = 1, ctas_per_sm: int = 2,
+                        stream=None):
         """cannikin_probe_a2a_write (bench utility, COLLECTIVE): all-to-all peer writes."""
-        _check(lib().cannikin_probe_a2a_write(self._h, int(bytes_per_peer), _stream(stream)))
+        _check(lib().cannikin_probe_a2a_write(self._h, int(bytes_per_peer), int(repeat),
+                                              int(ctas_per_sm), _stream(stream)))
 
 
 def weighted_allreduce_group(ctxs, ptrs, n: int, dtype: int, r, stream=None):

@@ -633,7 +633,7 @@ extern "C" int cannikin_last_launch_count(cannikin_ctx* ctx) { return ctx ? ctx-
 extern "C" const char* cannikin_last_variant(cannikin_ctx* ctx) { return ctx ? ctx->last_variant : ""; }
 
 extern "C" cannikin_status cannikin_probe_a2a_write(cannikin_ctx* ctx, size_t bytes_per_peer,
-                                                    void* stream) {
+                                                    int repeat, int ctas_per_sm, void* stream) {
   if (!ctx) return fail(CANNIKIN_ERR_INVALID, "probe_a2a_write: ctx == NULL");
   if (ctx->world < 2 || ctx->in_process)
     return fail(CANNIKIN_ERR_INVALID, "probe_a2a_write: needs a multi-process ctx (world > 1)");
@@ -641,8 +641,11 @@ extern "C" cannikin_status cannikin_probe_a2a_write(cannikin_ctx* ctx, size_t by
       (size_t)ctx->world * bytes_per_peer > ctx->heap_bytes)
     return fail(CANNIKIN_ERR_INVALID, "probe_a2a_write: %zu bytes per peer (heap %zu, world %d)",
                 bytes_per_peer, ctx->heap_bytes, ctx->world);
+  if (repeat < 1 || repeat > 1024 || ctas_per_sm < 1 || ctas_per_sm > 4)
+    return fail(CANNIKIN_ERR_INVALID, "probe_a2a_write: repeat %d / ctas_per_sm %d out of range",
+                repeat, ctas_per_sm);
   CK_CUDA(cudaSetDevice(ctx->device));
-  CK_CUDA(cannikin::launch_a2a_write(ctx, bytes_per_peer, S(stream)));
+  CK_CUDA(cannikin::launch_a2a_write(ctx, bytes_per_peer, repeat, ctas_per_sm, S(stream)));
   ctx->last_launches = 1;
   ctx->last_variant = "a2a_write_probe";
   return CANNIKIN_OK;

@@ -17,29 +17,29 @@ struct A2aArgs {
   const uint4* src;       // this rank's heap (any contents)
   uint4* dst[kMaxWorld];  // peer p's scratch + rank * bytes_per_peer, for the W-1 peers
   int npeers;
+  int repeat;             // passes over the segments (long transfers amortise the launch)
   size_t nvec;            // 16-byte vectors per peer
 };
 
-// CTA c writes to peer c % npeers; 4 vectors in flight per thread
+// Every CTA writes to every peer, interleaved (as the K3 kernels do): vector v of each peer's
+// segment in turn, the W-1 loads of an index issued together
+template <int NP>
 __global__ void __launch_bounds__(512) a2a_write_kernel(const A2aArgs a) {
-  const int k = blockIdx.x % a.npeers;
-  const int cta = blockIdx.x / a.npeers, nct = gridDim.x / a.npeers;
-  const uint4* s = a.src + (size_t)k * a.nvec;
-  uint4* d = a.dst[k];
-  const size_t stride = (size_t)nct * blockDim.x;
-  size_t i = (size_t)cta * blockDim.x + threadIdx.x;
-  for (; i + 3 * stride < a.nvec; i += 4 * stride) {
-    const uint4 x0 = s[i], x1 = s[i + stride], x2 = s[i + 2 * stride], x3 = s[i + 3 * stride];
-    d[i] = x0;
-    d[i + stride] = x1;
-    d[i + 2 * stride] = x2;
-    d[i + 3 * stride] = x3;
-  }
-  for (; i < a.nvec; i += stride) d[i] = s[i];
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (int rep = 0; rep < a.repeat; ++rep)
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.nvec; i += stride) {
+      uint4 x[NP];
+#pragma unroll
+      for (int k = 0; k < NP; ++k) x[k] = a.src[(size_t)k * a.nvec + i];
+#pragma unroll
+      for (int k = 0; k < NP; ++k) a.dst[k][i] = x[k];
+    }
 }
 
-cudaError_t launch_a2a_write(cannikin_ctx* ctx, size_t bytes_per_peer, cudaStream_t st) {
+cudaError_t launch_a2a_write(cannikin_ctx* ctx, size_t bytes_per_peer, int repeat,
+                             int ctas_per_sm, cudaStream_t st) {
   A2aArgs a{};
+  a.repeat = repeat;
   a.src = reinterpret_cast<const uint4*>(ctx->base + ctx->user_off);
   a.npeers = 0;
   for (int j = 0; j < ctx->world; ++j) {
@@ -48,8 +48,20 @@ cudaError_t launch_a2a_write(cannikin_ctx* ctx, size_t bytes_per_peer, cudaStrea
                                                   (size_t)ctx->rank * bytes_per_peer);
   }
   a.nvec = bytes_per_peer / 16;
-  const int grid = (ctx->num_sms / a.npeers) * a.npeers;  // whole CTAs per peer
-  a2a_write_kernel<<<grid, 512, 0, st>>>(a);
+  // every CTA sends to every peer (a CTA per SM sending to one peer each -- the
+  // tools/nvlink_bw.cu form -- measured 606 GB/s at W = 4 against K3's 642)
+  const int grid = ctas_per_sm * ctx->num_sms;
+  switch (a.npeers) {
+#define CANNIKIN_CASE(K)                                   \
+  case K:                                                  \
+    a2a_write_kernel<K><<<grid, 512, 0, st>>>(a);          \
+    break;
+    CANNIKIN_CASE(1) CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5)
+    CANNIKIN_CASE(6) CANNIKIN_CASE(7)
+#undef CANNIKIN_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

@@ -266,7 +266,8 @@ def main():
     dist.barrier()
     ctx2.close()
     # the bench's live NVLink ceiling probe runs (collective) and leaves the ctx usable
-    ctx.probe_a2a_write(1 << 20)
+    for cps in (1, 2, 4):
+        ctx.probe_a2a_write(1 << 20, 3, cps)
     torch.cuda.synchronize()
     dist.barrier()
     t = ta.bucket_tensor(ctx, 4099, torch.float32)
