@@ -198,6 +198,144 @@ def hetero_sm_compare(N, s, tdt, rank, world, local_rank, B, iters, dist, ta, ck
     return out
 
 
+# One GPU shared by heterogeneous tenants (the paper's Cluster C shares GPUs among jobs,
+# P:603-608): disjoint SM partitions in Table 1's A100 : V100 : P100 proportion, rounded
+# to the 8-SM granularity of sm_100 green contexts, a few SMs left to the reduction.
+SHARED_GPU_MIX = ["A100", "V100", "P100"]
+SHARED_GPU_SMS = [[80, 32, 24], [64, 24, 16], [48, 16, 16]]  # the first the device can split
+
+
+def hetero_shared_gpu(ctx, N, tdt, B, iters, ta, ck, torch):
+    """Step time of Cannikin against equal-split DDP for 3 ranks sharing ONE GPU on disjoint SM
+    partitions (cannikin_green_partitions), real compute, no injected delays: the single-GPU
+    counterpart of hetero_sm_compare.  Rank i runs a synthetic bf16 GEMM stack (each sample = T
+    tokens of width H; forward NB GEMMs, backward NB chunks of two GEMMs) on its partition's stream;
+    bucket j of the C4 gradient is reduced by K2 over the three ranks' buckets on a comm stream as
+    soon as every rank's backward chunk j is done (§3.2.3 overlap).  Cannikin: the
+    measured-model loop (epoch 0 even split, epoch 1 Eq. 8, epoch 2 OptPerf from models the analyzer
+    LEARNED from per-rank CUDA-event timings), K2 with r_i = b_i / B; DDP: b_i = B/n, K2
+    with r_i = 1/n (the mean, Eq. 2).  Prediction error: the analyzer's Eq. 7 prediction against
+    the measured step."""
+    import statistics
+
+    n, NB, T, H = len(SHARED_GPU_MIX), 9, 512, 2048
+    green, errs = None, []
+    for counts in SHARED_GPU_SMS:
+        try:
+            green = ck.GreenPartitions(counts, device=torch.cuda.current_device())
+            break
+        except ck.CannikinError as e:
+            errs.append(str(e))
+    if green is None:
+        raise RuntimeError("; ".join(errs))
+    try:
+        rs = [torch.cuda.ExternalStream(h) for h in green.streams]
+        cs = torch.cuda.Stream()
+        master = torch.cuda.current_stream()
+        gen = torch.Generator(device="cuda").manual_seed(7)
+        Wt = [torch.randn(H, H, device="cuda", dtype=torch.bfloat16, generator=gen) * 0.02
+              for _ in range(NB)]
+        acts = [[torch.randn(B * T, H, device="cuda", dtype=torch.bfloat16, generator=gen) * 0.1
+                 for _ in range(NB + 1)] for _ in range(n)]
+        dx = [torch.empty(B * T, H, device="cuda", dtype=torch.bfloat16) for _ in range(n)]
+        dw = [[torch.empty(H, H, device="cuda", dtype=torch.bfloat16) for _ in range(NB)]
+              for _ in range(n)]
+        grads = [torch.randn(N, device="cuda", dtype=torch.float32, generator=gen).to(tdt)
+                 for _ in range(n)]
+        out = torch.empty(N, device="cuda", dtype=tdt)
+        st = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+        cuts = [j * (N // NB - (N // NB) % 8) for j in range(NB)] + [N]
+        E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+        def step(b, r):
+            t0, t9 = E(), E()
+            fw = [(E(), E()) for _ in range(n)]  # forward start / end per rank
+            ch = [[E() for _ in range(NB)] for _ in range(n)]  # backward chunk j done per rank
+            cm = [(E(), E()) for _ in range(NB)]  # reduction of bucket j start / end
+            t0.record(master)
+            for i in range(n):
+                rs[i].wait_stream(master)
+                with torch.cuda.stream(rs[i]):
+                    M = b[i] * T
+                    fw[i][0].record(rs[i])
+                    for l in range(NB):
+                        torch.matmul(acts[i][l][:M], Wt[l], out=acts[i][l + 1][:M])
+                    fw[i][1].record(rs[i])
+                    for j in range(NB):
+                        l = NB - 1 - j
+                        torch.matmul(acts[i][l + 1][:M], Wt[l].t(), out=dx[i][:M])
+                        torch.matmul(acts[i][l][:M].t(), acts[i][l + 1][:M], out=dw[i][l])
+                        ch[i][j].record(rs[i])
+            for j in range(NB):
+                for i in range(n):
+                    cs.wait_event(ch[i][j])
+                a, c = cuts[j], cuts[j + 1]
+                cm[j][0].record(cs)
+                ta.weighted_sum_local(ctx, [g[a:c] for g in grads], r, out[a:c], st[:n], st[n:],
+                                      accumulate=j > 0, stream=cs)
+                cm[j][1].record(cs)
+            for i in range(n):
+                master.wait_stream(rs[i])
+            master.wait_stream(cs)
+            t9.record(master)
+            torch.cuda.synchronize()
+            t_o = sum(cm[j][0].elapsed_time(cm[j][1]) for j in range(NB - 1)) * 1e-3
+            t_u = cm[NB - 1][0].elapsed_time(cm[NB - 1][1]) * 1e-3
+            per_rank = []
+            for i in range(n):
+                a_t = fw[i][0].elapsed_time(fw[i][1]) * 1e-3
+                P_t = fw[i][1].elapsed_time(ch[i][NB - 1]) * 1e-3
+                gam = fw[i][1].elapsed_time(ch[i][0]) * 1e-3 / P_t
+                per_rank.append((a_t, P_t, min(max(gam, 0.0), 0.99), t_o, t_u))
+            return per_rank, t0.elapsed_time(t9)
+
+        def run(b, r, count, an=None, gid0=0):
+            steps = []
+            for it in range(count + 2):
+                per_rank, ms = step(b, r)
+                if it < 2:
+                    continue
+                if an is not None:
+                    for i in range(n):
+                        an.observe(i, gid0 + it, b[i], *per_rank[i])
+                steps.append(ms)
+            return statistics.median(steps)
+
+        b_eq = [B // n + (1 if i < B % n else 0) for i in range(n)]
+        ddp_ms = run(b_eq, [1.0 / n] * n, iters)
+        an = ck.Analyzer(n)
+        epochs = []
+        for ep in range(3):
+            plan = an.plan(B)
+            meas = run(plan["b"], [x / B for x in plan["b"]], iters, an, 100 * ep)
+            epochs.append({"epoch": ep, "phase": plan["phase"], "b": plan["b"],
+                           "measured_ms": round(meas, 4),
+                           "predicted_ms": None if plan["T_pred"] != plan["T_pred"]
+                           else round(plan["T_pred"] * 1e3, 4)})
+        nodes, comm = an.models()
+        last = epochs[-1]
+        return {"cannikin_ms": last["measured_ms"], "ddp_ms": round(ddp_ms, 4),
+                "saving": round(1.0 - last["measured_ms"] / ddp_ms, 4),
+                "predicted_cannikin_ms": last["predicted_ms"],
+                "prediction_error": (None if last["predicted_ms"] is None else
+                                     round(abs(last["predicted_ms"] - last["measured_ms"])
+                                           / last["measured_ms"], 4)),
+                "b_cannikin": last["b"], "b_ddp": b_eq, "epochs": epochs, "buckets": NB,
+                "mix": SHARED_GPU_MIX, "sm_partitions": green.sms,
+                "partition_attempts_refused": errs,
+                "learned_ms_per_sample": [round((q + k) * 1e3, 4) for q, _, k, _ in nodes],
+                "learned_comm": {"gamma": round(comm[0], 4), "t_o_ms": round(comm[1] * 1e3, 4),
+                                 "t_u_ms": round(comm[2] * 1e3, 4)},
+                "compute": f"bf16 GEMM stack, {T} tokens x {H} wide per sample, {NB} layers",
+                "note": "3 ranks sharing one GPU on disjoint SM partitions (green contexts; "
+                        "Cluster C, P:603-608), real compute, split from models learned from "
+                        "measured timings; reduction = K2 over the ranks' buckets; median step of "
+                        "the last epoch"}
+    finally:
+        torch.cuda.synchronize()
+        green.close()
+
+
 def bucketed_sidecar(launch, N, s, n, world, bucket_mb, steps, peak, alg_bytes, dist, torch):
     """The paper's bucketed regime (DDP-style buckets) on the bench gradient: the step's
     reduction cut into buckets of `bucket_mb` per rank, one library call per bucket, captured in
@@ -835,6 +973,11 @@ def main():
             nvls = {"unavailable": str(e)[:200]}
 
     hetero = None
+    if world == 1 and not args.no_hetero:
+        try:
+            hetero = hetero_shared_gpu(ctx, N, tdt, cfg["B"], 6, ta, ck, torch)
+        except Exception as e:  # green contexts unavailable: report, do not sink the bench line
+            hetero = {"unavailable": str(e)[:300]}
     if world > 1 and not args.no_hetero:
         try:
             hetero = hetero_sm_compare(N, s, tdt, rank, world, local_rank, max(B, world), 6, dist,

@@ -284,6 +284,20 @@ cannikin_status cannikin_ddp_allreduce_mean(cannikin_ctx* ctx, void* bucket, siz
  * P:158-165) on homogeneous GPUs, as Cluster C's dummy load does.  Errors: DOMAIN, CUDA. */
 cannikin_status cannikin_emulate_compute(double seconds, void* stream);
 
+/* Bench utility (not part of the method): DISJOINT SM partitions of one GPU for heterogeneous
+ * ranks that share it -- the single-GPU analog of the paper's Cluster C and north_star's
+ * "per-rank compute-rate caps (SM-partitioned contexts)".  Creates n CUDA green contexts on
+ * `device`, partition i holding sm_counts[i] SMs (rounded up to the architecture's granularity, 8
+ * on sm_90+), split off one after another so they never overlap, and one non-blocking stream per
+ * partition: streams[i] (a CUstream / cudaStream_t; kernels launched on it run on partition i's
+ * SMs), sm_got[i] = the SMs it received.  The handle owns the contexts and streams; release it
+ * with cannikin_green_destroy (after the streams are idle).  Errors: INVALID (n outside 1..64,
+ * NULL), UNSUPPORTED (driver without green contexts, or the counts do not fit), CUDA. */
+typedef struct cannikin_green cannikin_green;
+cannikin_status cannikin_green_partitions(int device, int n, const int* sm_counts,
+                                          cannikin_green** out, void** streams, int* sm_got);
+cannikin_status cannikin_green_destroy(cannikin_green* green);
+
 /* Bench utility (not part of the method): the NVLink ceiling K3 runs against, measured on this
  * ctx's peer mappings.  Every rank writes `bytes_per_peer` bytes of its heap into its own slot of
  * EVERY peer's scratch half at once (the all-to-all write pattern of a two-shot all-reduce, both

@@ -109,6 +109,8 @@ SIGNATURES = {
     "cannikin_last_variant": (ctypes.c_char_p, [_P]),
     "cannikin_emulate_compute": (_I, [_D, _P]),
     "cannikin_probe_a2a_write": (_I, [_P, _Z, _I, _I, _P]),
+    "cannikin_green_partitions": (_I, [_I, _I, _IP, ctypes.POINTER(_P), ctypes.POINTER(_P), _IP]),
+    "cannikin_green_destroy": (_I, [_P]),
     "cannikin_trace": (_I, [_P, ctypes.POINTER(ctypes.c_uint64), _I, _IP]),
     "cannikin_gns_estimate": (_I, [_DP, _D, _LP, _I, ctypes.POINTER(_GnsResult)]),
     "cannikin_gns_estimate_corrected": (_I, [_DP, _D, _LP, _I, ctypes.POINTER(_GnsResult)]),
@@ -307,6 +309,28 @@ def weighted_allreduce_group(ctxs, ptrs, n: int, dtype: int, r, stream=None):
     hs = (_P * w)(*[c._h.value for c in ctxs])
     ps = (_P * w)(*ptrs)
     _check(lib().cannikin_weighted_allreduce_group(hs, w, ps, n, dtype, _dbl(r), _stream(stream)))
+
+
+class GreenPartitions:
+    """cannikin_green_partitions (bench utility): disjoint SM partitions of one GPU, one stream
+    each.  `streams` are raw cudaStream_t handles (use torch.cuda.ExternalStream), `sms` the SMs
+    each partition received."""
+
+    def __init__(self, sm_counts, device: int = 0):
+        n = len(sm_counts)
+        h = _P()
+        st = (_P * n)()
+        got = (ctypes.c_int * n)()
+        _check(lib().cannikin_green_partitions(device, n, (ctypes.c_int * n)(*sm_counts),
+                                               ctypes.byref(h), st, got))
+        self._h = h
+        self.streams = [int(st[i]) for i in range(n)]
+        self.sms = list(got)
+
+    def close(self):
+        if self._h:
+            _check(lib().cannikin_green_destroy(self._h))
+            self._h = None
 
 
 def emulate_compute(seconds: float, stream=None):

@@ -21,7 +21,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "cannikin")
 LIB = os.path.join(HERE, "libcannikin.so")
 
-CUDA_SOURCES = ["wsum_local.cu", "wsum_local_tma.cu", "twoshot.cu", "ll.cu", "ll128.cu", "nccl_path.cu", "nvls.cu", "emulate.cu", "gate.cu", "probe.cu",
+CUDA_SOURCES = ["wsum_local.cu", "wsum_local_tma.cu", "twoshot.cu", "ll.cu", "ll128.cu", "nccl_path.cu", "nvls.cu", "emulate.cu", "gate.cu", "probe.cu", "green.cu",
                 "api.cu"]
 HOST_SOURCES = ["host_solvers.cpp", "analyzer.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
