@@ -360,3 +360,33 @@ def test_full_size_c5(ctx):
     _, lsum, gsum = parity.compare_full([out], gs, r, "f32", TOL["f32"], chunk=20_000_000)
     assert np.allclose(local.cpu().numpy(), lsum, rtol=1e-4)
     assert abs(float(glob.cpu()[0]) - gsum) <= 1e-4 * gsum
+
+
+def test_green_partitions_are_disjoint(ctx):
+    """cannikin_green_partitions (the bench's shared-GPU heterogeneity harness): kernels launched on
+    partition i's stream run only on partition i's SMs, and the partitions do not overlap -- read
+    from K2's own per-CTA %smid trace."""
+    green = ck.GreenPartitions([16, 8])
+    try:
+        assert green.sms == [16, 8]
+        N = 1 << 22
+        gs = synth.gns_gradients(2, N, [3, 5], seed=3)
+        ins = [to_dev(g, "f32") for g in gs]
+        out = torch.empty(N, device="cuda")
+        local = torch.zeros(2, dtype=torch.float64, device="cuda")
+        glob = torch.zeros(1, dtype=torch.float64, device="cuda")
+        used = []
+        for h in green.streams:
+            st = torch.cuda.ExternalStream(h)
+            st.wait_stream(torch.cuda.current_stream())
+            ta.weighted_sum_local(ctx, ins, [0.375, 0.625], out, local, glob, variant="ldg",
+                                  stream=st)
+            torch.cuda.synchronize()
+            check(gs, [0.375, 0.625], "f32", out, local, glob)
+            used.append({int(t[1]) for t in ctx.trace()})
+        assert 0 < len(used[0]) <= 16 and 0 < len(used[1]) <= 8, used
+        assert not (used[0] & used[1]), used
+    finally:
+        torch.cuda.synchronize()
+        green.close()
+
