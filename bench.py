@@ -336,6 +336,48 @@ def hetero_shared_gpu(ctx, N, tdt, B, iters, ta, ck, torch):
         green.close()
 
 
+# C4's "adaptive global batch via GNS" (BASELINE configs[3]): candidate total batches, B0 = 9
+ADAPTIVE_CANDS = [9, 16, 32, 64, 96, 128, 192, 256, 384, 512, 768, 1024]
+
+
+def adaptive_batch_sidecar(ctx, N, n, epochs, steps, synth, ck, ta, torch):
+    """The paper's outer loop on the bench gradient (one GPU, n emulated ranks, K2): the true noise
+    scale trS/|G|^2 rises 50 -> 5000 over the epochs (the shape of fig:gns); every step
+    the ranks' mean gradients for their b_i are drawn from the V1 recipe, K2 reduces them and
+    returns the norms, the library estimates G and S (Theorem 1) and updates the EMA (reading Q26);
+    at the end of each epoch the total batch is chosen by goodput (reading Q27) and split
+    by opt_split.  Reports per epoch B, the split, the true and estimated B_noise."""
+    models = hetero_models(n)
+    comm = (1.0 / 9, 8 * 65e-6, 65e-6)
+    out = torch.empty(N, dtype=torch.bfloat16, device="cuda")
+    st = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+    ema = ck.GnsEma(0.9)
+    B = max(ADAPTIVE_CANDS[0], n)
+    rows = []
+    for e in range(epochs):
+        trS = 50.0 * (100.0 ** (e / max(1, epochs - 1)))
+        split = ck.opt_split(models, comm, B)["b"]
+        for k in range(steps):
+            gs = synth.device_gns_gradients(n, N, split, G2=1.0, trS=trS, seed=1000 * e + k,
+                                            dtype="bf16")
+            ta.weighted_sum_local(ctx, gs, [x / B for x in split], out, st[:n], st[n:])
+            v = st.tolist()
+            est = ck.gns_estimate(v[:n], v[n], split)
+            ema.update(est["G2"], est["trS"])
+            del gs
+        nxt = ck.choose_batch(models, comm, ADAPTIVE_CANDS, ADAPTIVE_CANDS[0], ema.B_noise)
+        rows.append({"epoch": e, "B": B, "split": split, "true_B_noise": round(trS, 1),
+                     "est_B_noise": round(est["B_noise"], 1), "ema_B_noise": round(ema.B_noise, 1),
+                     "next_B": nxt["B"]})
+        B = nxt["B"]
+    torch.cuda.empty_cache()
+    last_err = max(abs(r["est_B_noise"] - r["true_B_noise"]) / r["true_B_noise"] for r in rows)
+    return {"epochs": rows, "B_path": [r["B"] for r in rows] + [B],
+            "max_rel_err_last_step_B_noise": round(last_err, 4),
+            "note": "synthetic noise-scale schedule 50 -> 5000; B chosen by goodput from the EMA "
+                    "of the Theorem-1 estimates computed from the K2 statistics"}
+
+
 def bucketed_sidecar(launch, N, s, n, world, bucket_mb, steps, peak, alg_bytes, dist, torch):
     """The paper's bucketed regime (DDP-style buckets) on the bench gradient: the step's
     reduction cut into buckets of `bucket_mb` per rank, one library call per bucket, captured in
@@ -972,6 +1014,13 @@ def main():
         except Exception as e:  # multicast unavailable on this system
             nvls = {"unavailable": str(e)[:200]}
 
+    adaptive = None
+    if world == 1 and not args.no_hetero and cfg["dtype"] == "bf16":
+        try:
+            adaptive = adaptive_batch_sidecar(ctx, N, n, 6, 3, synth, ck, ta, torch)
+        except Exception as e:  # a sidecar must not sink the bench line
+            adaptive = {"unavailable": str(e)[:200]}
+
     hetero = None
     if world == 1 and not args.no_hetero:
         try:
@@ -1059,7 +1108,7 @@ def main():
                        "host_overlap": "host half of step t overlaps device half of step t+1"},
             "roofline": roof, "bucketed_25mb": bucketed, "cpu_baseline": cpu, "e2e": e2e,
             "ddp_baseline": ddp,
-            "step_vs_ddp": hetero, "nvls_f32": nvls,
+            "step_vs_ddp": hetero, "adaptive_batch": adaptive, "nvls_f32": nvls,
             # K2 / K3 per bucket, plus (N > 1) the statistics-finalize kernel per step
             "gpu_launches": (launches_per_step() + (1 if world > 1 else 0)) * args.steps,
             "clocks": clk.summary(),
