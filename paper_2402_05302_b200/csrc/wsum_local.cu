@@ -154,6 +154,12 @@ static int occupancy_grid(int num_sms) {
 template <typename T, int NR, int U, int NT>
 static cudaError_t launch_nt(const LocalArgs& a, int num_sms, int grid_override, cudaStream_t st) {
   int grid = grid_override > 0 ? grid_override : occupancy_grid<T, NR, U, NT>(num_sms);
+  // small passes (<= 32 MB of traffic, L2-resident, latency-bound): two CTAs per SM -- fewer
+  // partial rows for the last CTA and less launch drain; C1 (3 x 4 MB fp32) 11.6 -> 9.7 us
+  // (profiles/r02/k2_small_grids.jsonl).  A function of (n, ranks, dtype) only: deterministic.
+  if (grid_override <= 0 && (size_t)(NR + 1) * a.nvec * 16 <= ((size_t)32 << 20) &&
+      grid > 2 * num_sms)
+    grid = 2 * num_sms;
   // do not launch CTAs that would own no vector (keeps tiny buckets cheap)
   const size_t need = (a.nvec + NT - 1) / NT;
   if ((size_t)grid > need) grid = need < 1 ? 1 : (int)need;

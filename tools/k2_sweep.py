@@ -18,7 +18,7 @@ import cannikin_synth as synth  # noqa: E402
 import paper_2402_05302_b200 as ck  # noqa: E402
 from paper_2402_05302_b200 import torch_api as ta  # noqa: E402
 
-SHAPES = [("c4", 8, 110_000_000, "bf16"), ("c5", 8, 354_823_168, "f32"), ("c3", 8, 25_557_032, "f32"),
+SHAPES = [("c1", 3, 1 << 20, "f32"), ("c4", 8, 110_000_000, "bf16"), ("c5", 8, 354_823_168, "f32"), ("c3", 8, 25_557_032, "f32"),
           ("c2", 2, 11_689_512, "f32"), ("c1-big", 3, 1 << 26, "f32"), ("c4x3", 3, 110_000_000, "bf16"),
           ("c4f32", 8, 110_000_000, "f32"), ("c5bf16", 8, 354_823_168, "bf16"),
           ("c4x2", 8, 220_000_000, "bf16"), ("c4q", 8, 27_500_000, "bf16"),
