@@ -7,6 +7,11 @@
 #     bench     default bench line, and --bucket-mb 25     -> gpurun_out/bench_*.jsonl
 #     ncu_k2    ncu --set full of the bench's K2 launch    -> gpurun_out/ncu_k2.ncu-rep
 #     bench_multi  bench at N = all GPUs (torchrun)        -> gpurun_out/bench_n<N>.jsonl
+#     nvls_bf16 the bf16 NVLS characterisation probe       -> gpurun_out/nvls_bf16_n<N>.jsonl
+#     configs   every BASELINE config at N = 1, 2, 4       -> gpurun_out/configs_matrix.jsonl
+#     sweep     11-size C5 bucket sweep, f32/bf16, W=N, 2  -> gpurun_out/k3_c5sweep_*.jsonl
+#     ddp       ResNet-50 DDP hook, SM caps, gated vs 24   -> gpurun_out/ddp_step_sm_r50_*.jsonl
+#     k2_ab / k3_ab  A/B of builds in build/variants/*.so  -> gpurun_out/k2_ab.jsonl, k3_ab.jsonl
 set -u
 mkdir -p gpurun_out
 NG=$(nvidia-smi -L | wc -l)
@@ -50,6 +55,54 @@ for stage in "$@"; do
       timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 \
         --master-port 29533 bench.py --gpus $NG > gpurun_out/bench_n${NG}.jsonl 2> gpurun_out/bench_n${NG}.err
       echo "bench n$NG exit $?"; tail -1 gpurun_out/bench_n${NG}.jsonl | cut -c1-600 ;;
+    nvls_bf16)
+      timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 \
+        --master-port 29552 tools/nvls_bf16_probe.py > gpurun_out/nvls_bf16_n${NG}.jsonl 2>&1
+      echo "nvls bf16 exit $?" ;;
+    configs)
+      : > gpurun_out/configs_matrix.jsonl
+      for cfg in c1 c2 c3 c4 c5; do
+        CUDA_VISIBLE_DEVICES=0 timeout 600 python bench.py --config $cfg --no-hetero --no-e2e --no-cpu \
+          2>/dev/null | grep '^{' >> gpurun_out/configs_matrix.jsonl
+        for W in 2 4; do
+          [ "$NG" -ge $W ] || continue
+          CUDA_VISIBLE_DEVICES=$(seq -s, 0 $((W - 1))) timeout 600 python -m torch.distributed.run --nnodes=1 \
+            --nproc-per-node $W --master-addr 127.0.0.1 --master-port $((29710 + W)) bench.py --gpus $W \
+            --config $cfg --no-hetero --no-e2e --no-nvls 2>/dev/null | grep '^{' >> gpurun_out/configs_matrix.jsonl
+        done
+      done
+      echo "configs: $(wc -l < gpurun_out/configs_matrix.jsonl) lines" ;;
+    sweep)
+      for dt in f32 bf16; do for W in $NG 2; do
+        CUDA_VISIBLE_DEVICES=$(seq -s, 0 $((W - 1))) timeout 900 python -m torch.distributed.run --nnodes=1 \
+          --nproc-per-node $W --master-addr 127.0.0.1 --master-port 29630 tools/k3_sweep.py --dtype $dt \
+          --sizes-mb 1,2,4,8,16,32,64,128,256,512,1024 --variants auto > gpurun_out/k3_c5sweep_${dt}_n${W}.jsonl 2>&1
+        echo "sweep $dt W=$W exit $?"
+      done; done ;;
+    ddp)
+      for W in $NG 2; do
+        for mode in gated ungated24; do
+          extra=$([ $mode = gated ] && echo "" || echo "--ungated --grid 24")
+          CUDA_VISIBLE_DEVICES=$(seq -s, 0 $((W - 1))) timeout 900 python -m torch.distributed.run --nnodes=1 \
+            --nproc-per-node $W --master-addr 127.0.0.1 --master-port 29735 tools/ddp_step.py --model resnet50 \
+            --img 224 --B $((128 * W)) --hetero sm $extra > gpurun_out/ddp_step_sm_r50_n${W}_${mode}.jsonl 2>&1
+          echo "ddp W=$W $mode exit $?"
+        done
+      done ;;
+    k2_ab)
+      : > gpurun_out/k2_ab.jsonl
+      for rep in 1 2 3; do for lib in build/variants/*.so; do
+        CANNIKIN_LIB=$PWD/$lib timeout 300 python tools/k2_vs_pattern.py --sets synth --k2-grids 0 \
+          --pattern-grids 592 --tag $(basename $lib .so) 2>/dev/null | grep '^{' >> gpurun_out/k2_ab.jsonl
+      done; done ;;
+    k3_ab)
+      : > gpurun_out/k3_ab.jsonl
+      for rep in 1 2 3; do for lib in build/variants/*.so; do
+        CANNIKIN_LIB=$PWD/$lib timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG \
+          --master-addr 127.0.0.1 --master-port $((29700 + rep)) bench.py --gpus $NG --no-hetero --no-e2e \
+          --no-nvls --steps 30 2>/dev/null | grep '^{' | sed "s/^{/{\"lib\": \"$(basename $lib .so)\", /" \
+          >> gpurun_out/k3_ab.jsonl
+      done; done ;;
     *) echo "unknown stage $stage" ;;
   esac
 done
