@@ -150,6 +150,30 @@ def main():
                      launches=launches, staged=staged)
             if not staged:
                 ta.free_bucket_tensor(ctx, x)
+        # the same ctx inside a CUDA graph: [fill, reduce] (gate + reduction kernel when gated)
+        # captured once, replayed three times with a late rank each time; the epochs live on the
+        # device, so every replay is a fresh, correct reduction (LL, LL128 and two-shot sizes)
+        graph_ok = []
+        for Ng in (1000, 300_001, 5_000_011):
+            x = ta.bucket_tensor(ctx, Ng, torch.float32)
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                x.fill_(float(rank + 1))
+                ta.weighted_allreduce(ctx, x, 1.0 / world)
+            for rep in range(3):
+                dist.barrier()
+                if args.gated and rank == rep % world:
+                    ck.emulate_compute(2e-3, torch.cuda.current_stream().cuda_stream)
+                g.replay()
+                torch.cuda.synchronize()
+                graph_ok.append(bool(torch.allclose(x, torch.full_like(x, (world + 1) / 2))))
+            ctx.gns_stats()
+            del g
+            ta.free_bucket_tensor(ctx, x)
+        np.save(os.path.join(args.out, f"rank{rank}_graph_replays.npy"), np.array(graph_ok))
         dist.barrier()
         ctx.close()
         dist.destroy_process_group()

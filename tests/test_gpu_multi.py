@@ -184,3 +184,6 @@ def test_mixed_sequence_of_sizes_dtypes_and_variants(gated):
             assert np.array_equal(ranks[k]["loc"], ranks[0]["loc"]), (t, k)
         # launches of the call: the reduction (+ 2 staging copies) (+ the gate kernel)
         assert int(ranks[0]["launches"]) in ((2, 4) if gated else (1, 3)), (t, ranks[0]["launches"])
+    for k in range(world):  # graph-captured reductions, replayed (late rank when gated)
+        ok = np.load(os.path.join(d, f"rank{k}_graph_replays.npy"))
+        assert ok.size == 9 and ok.all(), (k, ok)
