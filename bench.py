@@ -551,6 +551,34 @@ class ClockSampler:
 BIDIR_WRITE_GBS = {2: 690.8, 4: 671.4}
 
 
+def pattern_ceiling(gs, out, N, s, achieved, ck, torch):
+    """The bare memory pattern of K2 (cannikin_probe_stream_pattern: the same n + 1 streams of
+    16-byte vectors, integer adds, no arithmetic of the method) timed on the bench's own buffers
+    right after the timed region -- the HBM ceiling K2's traffic can reach in this run's memory
+    state; best of three grids, back-to-back launches, CUDA events."""
+    try:
+        ptrs = [g.data_ptr() for g in gs]
+        nbytes = N * s // 16 * 16
+        tried = {}
+        for cps in (3, 4, 5):
+            for _ in range(3):
+                ck.probe_stream_pattern(ptrs, out.data_ptr(), nbytes, cps)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(10):
+                ck.probe_stream_pattern(ptrs, out.data_ptr(), nbytes, cps)
+            e1.record()
+            torch.cuda.synchronize()
+            tried[f"{cps}_ctas_per_sm"] = round((len(gs) + 1) * nbytes / (e0.elapsed_time(e1) / 10 * 1e-3) / 1e9, 1)
+        best = max(tried.values())
+        return {"peak": best, "frac": round(achieved / best, 4), "tried": tried,
+                "kind": "live bare n:1 stream pattern on the same buffers after the timed region "
+                        "(cannikin_probe_stream_pattern), best of three grids"}
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": str(e)[:200]}
+
+
 def a2a_ceiling(ctx, heap_bytes, n, steps, busbw, barrier, stream, dist, torch):
     """The all-to-all peer-write ceiling of this box at this N, measured live with
     cannikin_probe_a2a_write (every rank writes heap/n bytes into every peer at once; per-direction
@@ -944,7 +972,8 @@ def main():
                            f"wsum_local_kernel (K2), {nb} PDL-chained bucket launches per step, "
                            "timed as one chain: kernel_ms = chain / launches"),
                 "kernel_ms": round(kmean, 4), "kernel_ms_dist": kdist,
-                "traffic": ncu_traffic(f"{args.config}_n{n}_{cfg['dtype']}_b{launches_per_step()}")}
+                "traffic": ncu_traffic(f"{args.config}_n{n}_{cfg['dtype']}_b{launches_per_step()}"),
+                "pattern_ceiling": pattern_ceiling(gs, out, N, s, achieved, ck, torch)}
     else:
         busbw = (N * s / len(cuts[:-1])) / (kmean * 1e-3) * 2 * (n - 1) / n / 1e9
         roof = {"bound": "nvlink", "achieved": round(busbw, 1), "peak": 770.0, "unit": "GB/s",

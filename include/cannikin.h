@@ -301,6 +301,16 @@ cannikin_status cannikin_green_partitions(int device, int n, const int* sm_count
                                           cannikin_green** out, void** streams, int* sm_got);
 cannikin_status cannikin_green_destroy(cannikin_green* green);
 
+/* Bench utility (not part of the method): the bare memory pattern of the emulated-rank pass --
+ * n_in (1..CANNIKIN_MAX_EMULATED) device streams of `bytes` read and one written, 16-byte
+ * vectors, grid-stride over ctas_per_sm (1..8) x SMs CTAs of 256 threads, integer adds of the
+ * words (no method arithmetic; `out` receives meaningless data).  Timed on the very buffers
+ * cannikin_weighted_sum_local reduces, it is the HBM ceiling that pass can reach in the same
+ * memory-system state.  bytes: a multiple of 16; pointers 16-byte aligned.  Enqueued on `stream`.
+ * Errors: INVALID, CUDA. */
+cannikin_status cannikin_probe_stream_pattern(const void* const* in, int n_in, void* out,
+                                              size_t bytes, int ctas_per_sm, void* stream);
+
 /* Bench utility (not part of the method): the NVLink ceiling K3 runs against, measured on this
  * ctx's peer mappings.  Every rank writes `bytes_per_peer` bytes of its heap into its own slot of
  * EVERY peer's scratch half at once (the all-to-all write pattern of a two-shot all-reduce, both

@@ -109,6 +109,7 @@ SIGNATURES = {
     "cannikin_last_variant": (ctypes.c_char_p, [_P]),
     "cannikin_emulate_compute": (_I, [_D, _P]),
     "cannikin_probe_a2a_write": (_I, [_P, _Z, _I, _I, _P]),
+    "cannikin_probe_stream_pattern": (_I, [ctypes.POINTER(_P), _I, _P, _Z, _I, _P]),
     "cannikin_green_partitions": (_I, [_I, _I, _IP, ctypes.POINTER(_P), ctypes.POINTER(_P), _IP]),
     "cannikin_green_destroy": (_I, [_P]),
     "cannikin_trace": (_I, [_P, ctypes.POINTER(ctypes.c_uint64), _I, _IP]),
@@ -331,6 +332,13 @@ class GreenPartitions:
         if self._h:
             _check(lib().cannikin_green_destroy(self._h))
             self._h = None
+
+
+def probe_stream_pattern(in_ptrs, out_ptr: int, nbytes: int, ctas_per_sm: int = 4, stream=None):
+    """cannikin_probe_stream_pattern (bench utility): the bare n:1 memory pattern of K2."""
+    n = len(in_ptrs)
+    _check(lib().cannikin_probe_stream_pattern((_P * n)(*in_ptrs), n, out_ptr, int(nbytes),
+                                               int(ctas_per_sm), _stream(stream)))
 
 
 def emulate_compute(seconds: float, stream=None):

@@ -632,6 +632,24 @@ extern "C" int cannikin_last_launch_count(cannikin_ctx* ctx) { return ctx ? ctx-
 
 extern "C" const char* cannikin_last_variant(cannikin_ctx* ctx) { return ctx ? ctx->last_variant : ""; }
 
+extern "C" cannikin_status cannikin_probe_stream_pattern(const void* const* in, int n_in, void* out,
+                                                        size_t bytes, int ctas_per_sm,
+                                                        void* stream) {
+  if (!in || !out || n_in < 1 || n_in > CANNIKIN_MAX_EMULATED || bytes % 16 ||
+      ctas_per_sm < 1 || ctas_per_sm > 8)
+    return fail(CANNIKIN_ERR_INVALID, "probe_stream_pattern: bad arguments");
+  for (int j = 0; j < n_in; ++j)
+    if (!in[j] || reinterpret_cast<uintptr_t>(in[j]) % 16)
+      return fail(CANNIKIN_ERR_INVALID, "probe_stream_pattern: in[%d] NULL or misaligned", j);
+  if (reinterpret_cast<uintptr_t>(out) % 16)
+    return fail(CANNIKIN_ERR_INVALID, "probe_stream_pattern: out misaligned");
+  int dev = 0, sms = 0;
+  CK_CUDA(cudaGetDevice(&dev));
+  CK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK_CUDA(cannikin::launch_stream_pattern(in, n_in, out, bytes, ctas_per_sm * sms, S(stream)));
+  return CANNIKIN_OK;
+}
+
 extern "C" cannikin_status cannikin_probe_a2a_write(cannikin_ctx* ctx, size_t bytes_per_peer,
                                                     int repeat, int ctas_per_sm, void* stream) {
   if (!ctx) return fail(CANNIKIN_ERR_INVALID, "probe_a2a_write: ctx == NULL");

@@ -54,6 +54,8 @@ cudaError_t launch_ll_group(cannikin_ctx* const* ctxs, int W, void* const* bucke
 cudaError_t launch_ll128_group(cannikin_ctx* const* ctxs, int W, void* const* buckets, size_t n,
                                cannikin_dtype dt, const double* r, cudaStream_t st);
 cudaError_t launch_gate(cannikin_ctx* ctx, cudaStream_t st);
+cudaError_t launch_stream_pattern(const void* const* in, int n_in, void* out, size_t bytes,
+                                  int grid, cudaStream_t st);
 cudaError_t launch_a2a_write(cannikin_ctx* ctx, size_t bytes_per_peer, int repeat,
                              int ctas_per_sm, cudaStream_t st);
 cudaError_t launch_stats_finalize(cannikin_ctx* ctx, double* out, cudaStream_t st);

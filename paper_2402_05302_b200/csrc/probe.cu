@@ -65,4 +65,60 @@ cudaError_t launch_a2a_write(cannikin_ctx* ctx, size_t bytes_per_peer, int repea
   return cudaGetLastError();
 }
 
+// The bare memory pattern of K2: n_in streams read, one written, 16-byte vectors, grid-stride,
+// integer adds (no method arithmetic) -- the ceiling K2's traffic can reach on the same buffers in
+// the same memory-system state (tools/hbm_probe*.cu).
+struct PatternArgs {
+  const char* in[16];
+  char* out;
+  size_t nvec;
+};
+
+template <int NR>
+__global__ void __launch_bounds__(256) stream_pattern_kernel(const PatternArgs a) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < a.nvec; v += stride) {
+    uint4 x[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(x[j].x), "=r"(x[j].y), "=r"(x[j].z), "=r"(x[j].w)
+                   : "l"(a.in[j] + v * 16));
+    }
+    uint4 s = x[0];
+#pragma unroll
+    for (int j = 1; j < NR; ++j) {
+      s.x += x[j].x;
+      s.y += x[j].y;
+      s.z += x[j].z;
+      s.w += x[j].w;
+    }
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(a.out + v * 16),
+                 "r"(s.x), "r"(s.y), "r"(s.z), "r"(s.w)
+                 : "memory");
+  }
+}
+
+cudaError_t launch_stream_pattern(const void* const* in, int n_in, void* out, size_t bytes,
+                                  int grid, cudaStream_t st) {
+  PatternArgs a{};
+  for (int j = 0; j < n_in; ++j) a.in[j] = static_cast<const char*>(in[j]);
+  a.out = static_cast<char*>(out);
+  a.nvec = bytes / 16;
+  switch (n_in) {
+#define CANNIKIN_CASE(K)                                              \
+  case K:                                                             \
+    stream_pattern_kernel<K><<<grid, 256, 0, st>>>(a);                \
+    break;
+    CANNIKIN_CASE(1) CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5)
+    CANNIKIN_CASE(6) CANNIKIN_CASE(7) CANNIKIN_CASE(8) CANNIKIN_CASE(9) CANNIKIN_CASE(10)
+    CANNIKIN_CASE(11) CANNIKIN_CASE(12) CANNIKIN_CASE(13) CANNIKIN_CASE(14) CANNIKIN_CASE(15)
+    CANNIKIN_CASE(16)
+#undef CANNIKIN_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace cannikin

@@ -390,3 +390,14 @@ def test_green_partitions_are_disjoint(ctx):
         torch.cuda.synchronize()
         green.close()
 
+
+
+def test_stream_pattern_probe():
+    """cannikin_probe_stream_pattern (the bench's live HBM ceiling for K2): out = word-wise integer
+    sum of the inputs, every vector including a ragged grid-stride tail."""
+    n = 3 * 65536 + 40  # 32-bit words; a multiple of 4 (16-byte vectors)
+    ins = [torch.full((n,), k + 1, dtype=torch.int32, device="cuda") for k in range(5)]
+    out = torch.zeros(n, dtype=torch.int32, device="cuda")
+    ck.probe_stream_pattern([t.data_ptr() for t in ins], out.data_ptr(), n * 4, 2)
+    torch.cuda.synchronize()
+    assert torch.all(out == 15)
