@@ -12,6 +12,7 @@
 #     sweep     11-size C5 bucket sweep, f32/bf16, W=N, 2  -> gpurun_out/k3_c5sweep_*.jsonl
 #     ddp       ResNet-50 DDP hook, SM caps, gated vs 24   -> gpurun_out/ddp_step_sm_r50_*.jsonl
 #     k2_ab / k3_ab  A/B of builds in build/variants/*.so  -> gpurun_out/k2_ab.jsonl, k3_ab.jsonl
+#     stress    80k random-size calls per W, bit-exact       -> gpurun_out/stress.jsonl
 set -u
 mkdir -p gpurun_out
 NG=$(nvidia-smi -L | wc -l)
@@ -103,6 +104,14 @@ for stage in "$@"; do
           --no-nvls --steps 30 2>/dev/null | grep '^{' | sed "s/^{/{\"lib\": \"$(basename $lib .so)\", /" \
           >> gpurun_out/k3_ab.jsonl
       done; done ;;
+    stress)
+      : > gpurun_out/stress.jsonl
+      for W in 2 $NG; do for v in auto ll ll128 twoshot; do
+        ME=$([ $v = ll ] && echo 131072 || echo 4194304)
+        CUDA_VISIBLE_DEVICES=$(seq -s, 0 $((W - 1))) timeout 900 python -m torch.distributed.run --nnodes=1 \
+          --master-addr 127.0.0.1 --nproc-per-node $W --master-port $((29800 + W)) tools/stress_allreduce.py \
+          --calls 10000 --variant $v --max-elems $ME 2>&1 | grep '^{' >> gpurun_out/stress.jsonl
+      done; done; cat gpurun_out/stress.jsonl ;;
     *) echo "unknown stage $stage" ;;
   esac
 done
