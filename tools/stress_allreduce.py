@@ -20,6 +20,7 @@ import torch
 import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2402_05302_b200 as ck  # noqa: E402
 from paper_2402_05302_b200 import torch_api as ta  # noqa: E402
 
 
@@ -29,6 +30,7 @@ def main():
     ap.add_argument("--batch", type=int, default=20)
     ap.add_argument("--variant", default="auto", choices=["auto", "ll", "ll128", "twoshot"])
     ap.add_argument("--max-elems", type=int, default=4 << 20)
+    ap.add_argument("--gated", action="store_true", help="CANNIKIN_INIT_GATED_ENTRY, a late rank")
     args = ap.parse_args()
     knobs = {"ll": ("1", "0"), "ll128": ("0", "1"), "twoshot": ("0", "0")}
     if args.variant in knobs:
@@ -38,7 +40,8 @@ def main():
     lr = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(lr)
     dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
-    ctx = ta.init_distributed_context(heap_bytes=args.max_elems * 4 * args.batch + (1 << 20))
+    ctx = ta.init_distributed_context(heap_bytes=args.max_elems * 4 * args.batch + (1 << 20),
+                                      gated=args.gated)
     rng = np.random.default_rng(1234)  # same sequence on every rank
     bad, done, moved = 0, 0, 0
     while done < args.calls:
@@ -62,7 +65,9 @@ def main():
             bufs.append((x, want))
         torch.cuda.synchronize()
         dist.barrier()
-        for (x, _), (n, dt, r) in zip(bufs, jobs):
+        for t, ((x, _), (n, dt, r)) in enumerate(zip(bufs, jobs)):
+            if args.gated and rank == (done + t) % world and t % 5 == 0:
+                ck.emulate_compute(2e-4, torch.cuda.current_stream().cuda_stream)  # late rank
             ta.weighted_allreduce(ctx, x, r[rank])
         torch.cuda.synchronize()
         ctx.gns_stats()
@@ -76,7 +81,8 @@ def main():
     t = torch.tensor([bad, done, moved], device="cuda", dtype=torch.float64)
     dist.all_reduce(t)
     if rank == 0:
-        print(json.dumps({"world": world, "variant": args.variant, "calls": int(t[1].item()) // world,
+        print(json.dumps({"world": world, "variant": args.variant, "gated": args.gated,
+                          "calls": int(t[1].item()) // world,
                           "elements": int(t[2].item()) // world, "mismatching_calls": int(t[0].item()),
                           "max_elems": args.max_elems}), flush=True)
     dist.barrier()
