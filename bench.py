@@ -354,6 +354,7 @@ def adaptive_batch_sidecar(ctx, N, n, epochs, steps, synth, ck, ta, torch):
     ema = ck.GnsEma(0.9)
     B = max(ADAPTIVE_CANDS[0], n)
     rows = []
+    errs_t1, errs_cor = [], []
     for e in range(epochs):
         trS = 50.0 * (100.0 ** (e / max(1, epochs - 1)))
         split = ck.opt_split(models, comm, B)["b"]
@@ -363,6 +364,9 @@ def adaptive_batch_sidecar(ctx, N, n, epochs, steps, synth, ck, ta, torch):
             ta.weighted_sum_local(ctx, gs, [x / B for x in split], out, st[:n], st[n:])
             v = st.tolist()
             est = ck.gns_estimate(v[:n], v[n], split)
+            cor = ck.gns_estimate(v[:n], v[n], split, corrected=True)  # §8(f)-4, reading Q31
+            errs_t1.append(abs(est["B_noise"] - trS) / trS)
+            errs_cor.append(abs(cor["B_noise"] - trS) / trS)
             ema.update(est["G2"], est["trS"])
             del gs
         nxt = ck.choose_batch(models, comm, ADAPTIVE_CANDS, ADAPTIVE_CANDS[0], ema.B_noise)
@@ -374,6 +378,9 @@ def adaptive_batch_sidecar(ctx, N, n, epochs, steps, synth, ck, ta, torch):
     last_err = max(abs(r["est_B_noise"] - r["true_B_noise"]) / r["true_B_noise"] for r in rows)
     return {"epochs": rows, "B_path": [r["B"] for r in rows] + [B],
             "max_rel_err_last_step_B_noise": round(last_err, 4),
+            "mean_rel_err_B_noise": {"theorem1": round(sum(errs_t1) / len(errs_t1), 5),
+                                     "corrected_weights": round(sum(errs_cor) / len(errs_cor), 5),
+                                     "steps": len(errs_t1)},
             "note": "synthetic noise-scale schedule 50 -> 5000; B chosen by goodput from the EMA "
                     "of the Theorem-1 estimates computed from the K2 statistics"}
 
