@@ -340,17 +340,21 @@ def hetero_shared_gpu(ctx, N, tdt, B, iters, ta, ck, torch):
 ADAPTIVE_CANDS = [9, 16, 32, 64, 96, 128, 192, 256, 384, 512, 768, 1024]
 
 
-def adaptive_batch_sidecar(ctx, N, n, epochs, steps, synth, ck, ta, torch):
+def adaptive_batch_sidecar(ctx, N, n, epochs, steps, synth, ck, ta, torch, rank=0, world=1,
+                           bucket=None):
     """The paper's outer loop on the bench gradient (one GPU, n emulated ranks, K2): the true noise
     scale trS/|G|^2 rises 50 -> 5000 over the epochs (the shape of fig:gns); every step
     the ranks' mean gradients for their b_i are drawn from the V1 recipe, K2 reduces them and
     returns the norms, the library estimates G and S (Theorem 1) and updates the EMA (reading Q26);
     at the end of each epoch the total batch is chosen by goodput (reading Q27) and split
-    by opt_split.  Reports per epoch B, the split, the true and estimated B_noise."""
+    by opt_split.  Reports per epoch B, the split, the true and estimated B_noise.  world > 1: one
+    rank per GPU, each draws its own mean gradient into the heap bucket and K3 reduces it (the
+    statistics, hence every estimate and every choice, are identical on all ranks)."""
     models = hetero_models(n)
     comm = (1.0 / 9, 8 * 65e-6, 65e-6)
-    out = torch.empty(N, dtype=torch.bfloat16, device="cuda")
-    st = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+    if world == 1:
+        out = torch.empty(N, dtype=torch.bfloat16, device="cuda")
+        st = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
     ema = ck.GnsEma(0.9)
     B = max(ADAPTIVE_CANDS[0], n)
     rows = []
@@ -359,10 +363,18 @@ def adaptive_batch_sidecar(ctx, N, n, epochs, steps, synth, ck, ta, torch):
         trS = 50.0 * (100.0 ** (e / max(1, epochs - 1)))
         split = ck.opt_split(models, comm, B)["b"]
         for k in range(steps):
-            gs = synth.device_gns_gradients(n, N, split, G2=1.0, trS=trS, seed=1000 * e + k,
-                                            dtype="bf16")
-            ta.weighted_sum_local(ctx, gs, [x / B for x in split], out, st[:n], st[n:])
-            v = st.tolist()
+            if world == 1:
+                gs = synth.device_gns_gradients(n, N, split, G2=1.0, trS=trS, seed=1000 * e + k,
+                                                dtype="bf16")
+                ta.weighted_sum_local(ctx, gs, [x / B for x in split], out, st[:n], st[n:])
+                v = st.tolist()
+            else:
+                gs = synth.device_gns_gradients(n, N, split, G2=1.0, trS=trS, seed=1000 * e + k,
+                                                dtype="bf16", ranks=[rank])
+                bucket.copy_(gs[0])
+                ta.weighted_allreduce(ctx, bucket, split[rank] / B)
+                loc, glob = ctx.gns_stats()
+                v = list(loc) + [glob]
             est = ck.gns_estimate(v[:n], v[n], split)
             cor = ck.gns_estimate(v[:n], v[n], split, corrected=True)  # §8(f)-4, reading Q31
             errs_t1.append(abs(est["B_noise"] - trS) / trS)
@@ -1051,9 +1063,14 @@ def main():
             nvls = {"unavailable": str(e)[:200]}
 
     adaptive = None
-    if world == 1 and not args.no_hetero and cfg["dtype"] == "bf16":
+    if not args.no_hetero and cfg["dtype"] == "bf16":
         try:
-            adaptive = adaptive_batch_sidecar(ctx, N, n, 6, 3, synth, ck, ta, torch)
+            keep = None if world == 1 else bucket.clone()  # the bench bucket, restored after
+            adaptive = adaptive_batch_sidecar(ctx, N, n, 6, 3, synth, ck, ta, torch, rank=rank,
+                                              world=world, bucket=None if world == 1 else bucket)
+            if keep is not None:
+                bucket.copy_(keep)
+                del keep
         except Exception as e:  # a sidecar must not sink the bench line
             adaptive = {"unavailable": str(e)[:200]}
 
