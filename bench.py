@@ -781,7 +781,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of a CUDA graph")
-    ap.add_argument("--no-hetero", action="store_true", help="skip the step-time-vs-DDP comparison")
+    ap.add_argument("--no-hetero", action="store_true",
+                    help="skip the step-time-vs-DDP comparison and the adaptive-batch sidecar")
     ap.add_argument("--hetero-grid", type=int, default=0,
                     help="step-vs-DDP: CTAs of the reduction kernels (0 = one per SM)")
     ap.add_argument("--hetero-ungated", action="store_true",
