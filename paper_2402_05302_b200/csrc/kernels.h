@@ -7,6 +7,26 @@
 
 namespace cannikin {
 
+// Launch with programmatic stream serialization (PDL): the kernel may be launched while its
+// predecessor in the stream is still running if that predecessor triggers early
+// (griddepcontrol.launch_dependents); the kernel itself executes griddepcontrol.wait before
+// touching memory, so the ordering is that of a plain launch and only the launch latency is
+// hidden.  A predecessor that never triggers releases it at completion.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // Arguments of a single-launch in-process group (cannikin_weighted_allreduce_group): the per-rank
 // arguments of every rank, one grid of world x grid CTAs; CTA c serves rank c / grid as its CTA
 // c % grid, so the ranks' CTAs are co-resident by construction (one kernel).

@@ -95,6 +95,10 @@ __device__ __forceinline__ void ll_body(const LLArgs& a, const int b, const int 
   __shared__ float s_r[W];
   __shared__ uint32_t s_e;
   const int tid = threadIdx.x, me = a.rank;
+  // programmatic dependent launch (launch_pdl): the next call may be launched now; this one
+  // waits for its predecessor before touching memory (profiles/r02/k3_pdl_all_ab.jsonl, k3_pdl_ab.jsonl)
+  dev::pdl_launch_dependents();
+  dev::pdl_wait();
   if (tid == 0) {
     s_e = (uint32_t)(__ldcg(&a.ctrl->ll_epoch) + 1);
     a.ctrl->trace[b][0] = dev::globaltimer_ns();
@@ -219,6 +223,12 @@ CANNIKIN_GROUP_ENTRY((typename T, int W), (T, W), (kLLThreads, 1), ll_kernel, ll
                      ll_body, LLArgs)
 
 // a[0] (single launch) or a[0..W-1] (in-process group: one launch of W x grid CTAs)
+#define LL_LAUNCH_ONE(K)                                                                    \
+  {                                                                                         \
+    cudaError_t e_ = launch_pdl(ll_kernel<T, K>, dim3(grid), dim3(kLLThreads), st, a[0]);   \
+    if (e_ != cudaSuccess) return e_;                                                       \
+  }
+
 template <typename T>
 static cudaError_t dispatch_ll(int W, const LLArgs* a, int grid, bool group, cudaStream_t st) {
   switch (W) {
@@ -230,7 +240,7 @@ static cudaError_t dispatch_ll(int W, const LLArgs* a, int grid, bool group, cud
       g.grid = grid;                                                         \
       ll_group_kernel<T, K><<<K * grid, kLLThreads, 0, st>>>(g);             \
     } else {                                                                 \
-      ll_kernel<T, K><<<grid, kLLThreads, 0, st>>>(a[0]);                    \
+      LL_LAUNCH_ONE(K);                                                      \
     }                                                                        \
     return cudaGetLastError();
     CANNIKIN_CASE(2) CANNIKIN_CASE(3) CANNIKIN_CASE(4) CANNIKIN_CASE(5) CANNIKIN_CASE(6)

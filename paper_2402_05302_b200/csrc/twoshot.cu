@@ -148,6 +148,10 @@ __device__ __forceinline__ void twoshot_body(const ArArgs& a, const int b, const
   __shared__ float s_r[W];
   __shared__ uint64_t s_ep;
   const int tid = threadIdx.x;
+  // programmatic dependent launch (launch_pdl): the next call may be launched now; this one
+  // waits for its predecessor before touching memory (profiles/r02/k3_pdl_all_ab.jsonl, k3_pdl_ab.jsonl)
+  dev::pdl_launch_dependents();
+  dev::pdl_wait();
 
   if (tid == 0) {
     s_ep = a.ctrl->epoch[b] + 1;
@@ -279,6 +283,10 @@ __device__ __forceinline__ void twoshot_dyn_body(const ArArgs& a, const int b, c
     return c;
   };
   const unsigned my_chunks = nchunks_of(a.rank);
+  // programmatic dependent launch (launch_pdl): the next call may be launched now; this one
+  // waits for its predecessor before touching memory (profiles/r02/k3_pdl_all_ab.jsonl, k3_pdl_ab.jsonl)
+  dev::pdl_launch_dependents();
+  dev::pdl_wait();
 
   if (tid == 0) {
     s_ep = a.ctrl->epoch[b] + 1;
@@ -447,6 +455,10 @@ __device__ __forceinline__ void twoshot_push_body(const PushArgs& a, const int b
   const int tid = threadIdx.x, NT = blockDim.x;
   auto shard_lo = [&](int k) -> size_t { return a.L * k; };
   auto shard_hi = [&](int k) -> size_t { return (k == W - 1) ? a.nvec : a.L * (k + 1); };
+  // programmatic dependent launch (launch_pdl): the next call may be launched now; this one
+  // waits for its predecessor before touching memory (profiles/r02/k3_pdl_all_ab.jsonl, k3_pdl_ab.jsonl)
+  dev::pdl_launch_dependents();
+  dev::pdl_wait();
   if (tid == 0) {
     s_ep = a.ctrl->epoch[b] + 1;
     a.ctrl->trace[b][0] = dev::globaltimer_ns();
@@ -747,10 +759,11 @@ template <typename T, int W>
 static cudaError_t launch_plan(const ArPlan& p, cudaStream_t st) {
   constexpr int U = u_default_ar<W>();
   constexpr int UP = W <= 2 ? 4 : 2;
-  if (p.kind == 0) twoshot_kernel<T, W, U, kArThreads><<<p.grid, kArThreads, 0, st>>>(p.ar);
-  else if (p.kind == 1) twoshot_dyn_kernel<T, W, U><<<p.grid, kArThreads, 0, st>>>(p.ar);
-  else twoshot_push_kernel<T, W, UP><<<p.grid, kArThreads, 0, st>>>(p.push);
-  return cudaGetLastError();
+  if (p.kind == 0)
+    return launch_pdl(twoshot_kernel<T, W, U, kArThreads>, dim3(p.grid), dim3(kArThreads), st, p.ar);
+  if (p.kind == 1)
+    return launch_pdl(twoshot_dyn_kernel<T, W, U>, dim3(p.grid), dim3(kArThreads), st, p.ar);
+  return launch_pdl(twoshot_push_kernel<T, W, UP>, dim3(p.grid), dim3(kArThreads), st, p.push);
 }
 
 // p[0..W-1]: the plans of ranks 0..W-1 of an in-process group, one launch of W x grid CTAs
